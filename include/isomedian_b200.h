@@ -1,0 +1,126 @@
+/*
+ * isomedian_b200.h -- C ABI of the B200 rank-order (circular median) filter.
+ *
+ * Drop-in native boundary for the hot path of the reference package
+ * `isomedian` (arXiv 2505.22938).  One call replaces the body of
+ *   filter_image(image, FilterParams)          /root/reference/pkg/src/isomedian/tiling.py:213-249
+ * i.e. padding (tiling.py:134-145), tiling (tiling.py:94-131), the per-tile
+ * ordinal transform (ordinal.py:126-172: _rank_by_bucket :62-79,
+ * _rank_by_radix16 :82-106, float_order_key :109-123) and the per-tile
+ * selection (core.py:175-221 _process_tile, the numba native boundary
+ * declared at core.py:176-181), plus the per-channel recursion
+ * (tiling.py:219-221) for HWC images and image batches.
+ *
+ * The host prologue stays with the caller, exactly as in the reference:
+ * validation and error messages (tiling.py:216-226, kernels.py:36-42),
+ * kernel rasterization (kernels.py:127-182 make_kernel) and target ranks
+ * (kernels.py:185-192, tiling.py:165-177) are computed on the host and
+ * passed in (the Python mirror lives in paper_2505_22938_b200/).
+ *
+ * Conventions: plain C types only; every pointer in imf_image.data and
+ * target_map is DEVICE memory for imf_filter and HOST memory for
+ * imf_filter_host; kernel tables are host memory.  No call allocates
+ * except imf_filter_host; no call throws; all return an IMF_* status.
+ * Calls are re-entrant (no mutable global state besides a launch counter).
+ */
+#ifndef ISOMEDIAN_B200_H
+#define ISOMEDIAN_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define IMF_OK 0
+#define IMF_ERR_INVALID 1     /* bad argument (host-side validation should catch first) */
+#define IMF_ERR_CUDA 2        /* CUDA runtime error */
+#define IMF_ERR_DEFECT 3      /* pivot/count scan exhausted: core.py:31-36 ScanDefectError */
+#define IMF_ERR_WORKSPACE 4   /* workspace too small */
+#define IMF_ERR_UNSUPPORTED 5 /* geometry the kernels cannot tile (e.g. radius > 124) */
+
+#define IMF_DTYPE_U8 0
+#define IMF_DTYPE_U16 1
+#define IMF_DTYPE_F32 2
+
+#define IMF_BOUNDARY_REPLICATE 0 /* np.pad(mode="edge") by r: tiling.py:134-140 */
+#define IMF_BOUNDARY_VALID 1     /* output (H-2r, W-2r): tiling.py:102-105,141-144 */
+
+#define IMF_SHAPE_CIRCLE 0  /* kernels.py:70-71 */
+#define IMF_SHAPE_SQUARE 1  /* kernels.py:72-73 */
+#define IMF_SHAPE_POLYGON 2 /* kernels.py:45-64,74-78 (rasterized by the caller) */
+
+/* Rasterized kernel = reference KernelShape (kernels.py:81-124).  Row spans
+ * are half-open [row_xlo, row_xhi); column extents inclusive. */
+typedef struct imf_kernel {
+    int32_t shape_code;
+    int32_t radius; /* 0..124 (kernels.py:24) */
+    int32_t area;
+    int32_t nrows;
+    const int32_t* row_dy;
+    const int32_t* row_xlo;
+    const int32_t* row_xhi;
+    int32_t ncols;
+    const int32_t* col_dx;
+    const int32_t* col_ytop;
+    const int32_t* col_ybot;
+} imf_kernel;
+
+/* A batch of (H, W, C) images; strides in ELEMENTS (any layout, e.g. HWC
+ * interleaved or planar).  One (H, W) plane per (batch, channel) is filtered
+ * independently, as the reference's per-channel recursion does. */
+typedef struct imf_image {
+    void* data;
+    int32_t dtype;
+    int32_t batch, height, width, channels;
+    int64_t stride_b, stride_y, stride_x, stride_c;
+} imf_image;
+
+typedef struct imf_options {
+    int32_t boundary;      /* IMF_BOUNDARY_* */
+    int32_t tile_size;     /* output tile side; 0 = auto.  Output-neutral (tiling.py:110-119) */
+    int32_t seed_rows;     /* seed rows per tile; 0 = auto (tuning knob, output-neutral) */
+    int32_t seeds_per_row; /* direct seeds per seed row; 0 = auto */
+    int32_t reserved[4];
+} imf_options;
+
+/* Bytes of device workspace imf_filter needs for this problem. */
+size_t imf_workspace_size(const imf_image* src, const imf_kernel* kernel, const imf_options* opt);
+
+/*
+ * Filter `src` into `dst` (device memory, distinct buffers) on `stream`
+ * (a cudaStream_t, NULL = legacy default stream).  Selection rank per output
+ * pixel: `target` when target_map is NULL, else target_map[y*out_w + x]
+ * (device int32, shared by every plane).  [tmin, tmax] must bound the targets
+ * in use (both == target for a scalar percentile).  The call is asynchronous;
+ * scan defects are reported by imf_workspace_status() after the stream
+ * completes.
+ */
+int imf_filter(const imf_image* src, imf_image* dst, const imf_kernel* kernel, int32_t target,
+               const int32_t* target_map, int32_t tmin, int32_t tmax, const imf_options* opt,
+               void* workspace, size_t workspace_bytes, void* stream);
+
+/* Synchronizes `stream` and returns IMF_OK or IMF_ERR_DEFECT for the last
+ * imf_filter that used `workspace`. */
+int imf_workspace_status(void* workspace, void* stream);
+
+/*
+ * Synchronous host-memory variant for FFI callers (cgo / JNI / ctypes): copies
+ * src to the current device, filters, copies the result back to dst.  Device
+ * buffers come from the stream-ordered pool (cudaMallocAsync).  Host buffers
+ * should be pinned for full copy bandwidth.
+ */
+int imf_filter_host(const imf_image* src, imf_image* dst, const imf_kernel* kernel, int32_t target,
+                    const int32_t* target_map, int32_t tmin, int32_t tmax, const imf_options* opt,
+                    void* stream);
+
+const char* imf_strerror(int status);
+int imf_version(void);                  /* 100 * major + minor */
+const char* imf_last_error(void);       /* detail of the last IMF_ERR_CUDA on this thread */
+uint64_t imf_launch_count(void);        /* kernels launched by this process (diagnostic) */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ISOMEDIAN_B200_H */

@@ -1,0 +1,112 @@
+// imf_common.cuh -- shared device definitions for the B200 rank-order filter.
+//
+// Layout vocabulary:
+//   tile      one T_w x T_h block of output pixels of one channel of one image;
+//             it reads an input tile of S_w x S_h = (T_w+2r) x (T_h+2r) pixels,
+//             coordinates clamped to the image (replicate == np.pad "edge",
+//             tiling.py:134-140) or shifted by r (valid mode, tiling.py:102-105).
+//   key       u32 order key of a pixel: the value for u8/u16, the float order key
+//             for f32 (ordinal.py:109-123) -- no float compare ever runs on device.
+//   omega     the rank -> position map (the paper's omnigram), u16 per rank,
+//             packed x | y << 8 (ordinal.py:56-59); S_w, S_h <= 256.
+//   Iq        the quantized ordinal image: Iq[y*S_w + x] = clamp((rank >> qs) - qb, 0, 255).
+//             Comparisons against pivots that are multiples of 2^qs with
+//             (pivot >> qs) - qb in [1, 255] are exact.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace imf {
+
+enum Dtype : int { DT_U8 = 0, DT_U16 = 1, DT_F32 = 2 };
+
+struct Geom {
+    const void* src;
+    void* dst;
+    int dtype;
+    int B, H, W, C;
+    long long s_b, s_y, s_x, s_c;  // source strides, elements
+    long long d_b, d_y, d_x, d_c;  // destination strides, elements
+    int out_h, out_w;
+    int vshift;                    // r in valid mode, 0 in replicate mode
+    int r;
+    int Tw, Th, Sw, Sh, N, Npad;   // Npad: N rounded up to a multiple of 64
+    int tiles_x, tiles_y;
+    long long tile_begin;          // first tile of this launch (chunking)
+};
+
+struct TileCoord {
+    int b, c, ty, tx;
+    int oy0, ox0;                  // output origin of the tile
+    const char* src;               // image (b, c) base
+};
+
+struct SelParams {
+    int circle;          // 1: arithmetic circle test (kernels.py:70-71); 0: span table
+    int R2;              // r*(r+1): 4(dx^2+dy^2) <= (2r+1)^2  <=>  dx^2+dy^2 <= r(r+1)
+    int ncols, nrows;
+    int target;          // scalar target rank (tiling.py:176-177 / kernels.py:191-192)
+    const int* tmap;     // per-pixel target ranks [out_h*out_w] or nullptr
+    int qs, qb, P_lo, P_hi;
+    int G, K;            // seed rows per tile, direct seeds per seed row
+    const int* ktab;     // [ncols pairs (VE,VX)][nrows pairs (HP,HM)][2r+1 spans]
+    int* status;         // device status word (1 = scan defect)
+};
+
+__device__ __forceinline__ TileCoord tile_coord(const Geom& g, long long t) {
+    TileCoord tc;
+    tc.tx = (int)(t % g.tiles_x); t /= g.tiles_x;
+    tc.ty = (int)(t % g.tiles_y); t /= g.tiles_y;
+    tc.c = (int)(t % g.C); t /= g.C;
+    tc.b = (int)t;
+    tc.oy0 = tc.ty * g.Th;
+    tc.ox0 = tc.tx * g.Tw;
+    int esz = g.dtype == DT_U8 ? 1 : (g.dtype == DT_U16 ? 2 : 4);
+    tc.src = (const char*)g.src + (tc.b * g.s_b + tc.c * g.s_c) * esz;
+    return tc;
+}
+
+// Image coordinates of input-tile pixel (ly, lx), clamped to the image.
+__device__ __forceinline__ long long src_offset(const Geom& g, const TileCoord& tc, int ly, int lx) {
+    int y = tc.oy0 + ly - g.r + g.vshift;
+    int x = tc.ox0 + lx - g.r + g.vshift;
+    y = y < 0 ? 0 : (y >= g.H ? g.H - 1 : y);
+    x = x < 0 ? 0 : (x >= g.W ? g.W - 1 : x);
+    return (long long)y * g.s_y + (long long)x * g.s_x;
+}
+
+__device__ __forceinline__ uint32_t float_key(uint32_t u) {
+    // ordinal.py:120: (u >> 31) ? ~u : u | 0x80000000
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+__device__ __forceinline__ uint32_t load_key(const Geom& g, const TileCoord& tc, int ly, int lx) {
+    long long o = src_offset(g, tc, ly, lx);
+    if (g.dtype == DT_U8) return __ldg((const uint8_t*)tc.src + o);
+    if (g.dtype == DT_U16) return __ldg((const uint16_t*)tc.src + o);
+    return float_key(__ldg((const uint32_t*)tc.src + o));
+}
+
+// y = i / Sw, x = i % Sw for i < 65536, Sw <= 256, via an exact float reciprocal
+// ((i + 0.5)/Sw sits >= 1/512 away from an integer; float error < 2^-15).
+__device__ __forceinline__ void lin_to_xy(int i, int Sw, float invS, int& x, int& y) {
+    y = __float2int_rz(((float)i + 0.5f) * invS);
+    x = i - y * Sw;
+}
+
+// omega is stored in 128-byte segments (64 ranks); the eight 16-byte chunks of
+// segment s are XOR-swizzled by (s & 7) so that lanes scanning different
+// segments with 16-byte loads hit different bank groups.
+__device__ __forceinline__ int omega_index(int v) {
+    int s = v >> 6, w = v & 63;
+    int chunk = (w >> 3) ^ (s & 7);
+    return (s << 6) | (chunk << 3) | (w & 7);
+}
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+    unsigned m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+}  // namespace imf

@@ -1,0 +1,341 @@
+"""Drop-in entry point: ``filter_image(image, FilterParams)`` on the B200.
+
+Mirrors the public surface of the reference ``isomedian.tiling``
+(/root/reference/pkg/src/isomedian/tiling.py) -- same dataclass fields and
+defaults, same validation order, same exception types and messages -- and
+replaces everything below the host prologue (padding, tiling, the thread
+pool, the per-tile ordinal transform and selection, tiling.py:228-249) with
+one call into the CUDA extension (C ABI: include/isomedian_b200.h).
+
+``forwarding``, ``workers`` and ``footprint_mask`` are accepted and
+output-neutral, exactly as in the reference (test_tiling.py:71-85,113-116);
+the GPU tiles independently.  ``tile_size`` keeps the reference validation
+(tiling.py:110-117) and is passed to the kernels as the output-tile side.
+
+Inputs may be numpy arrays or torch tensors (CPU or CUDA); the result has the
+same kind (and device).  There is no CPU fallback: without the extension or a
+GPU the call raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .kernels import MAX_RADIUS, ShapeSpec, make_kernel, target_rank
+
+MAX_TILE_SIDE = 256
+DEFAULT_OUTPUT_TILE = 64
+
+
+class ScanDefectError(RuntimeError):
+    """A segment scan ran off the end of the rank array (core.py:31-36).
+
+    Signals an internal invariant violation (never an input-data condition).
+    """
+
+
+@dataclass(frozen=True)
+class FilterParams:
+    """Filter-level parameters: kernel, percentile, boundary, and tiling.
+
+    Same fields, defaults and validation as tiling.py:27-45.
+    """
+
+    shape: ShapeSpec
+    percentile: float | np.ndarray = 0.5
+    boundary: str = "replicate"
+    forwarding: bool = True
+    tile_size: int | None = None
+    workers: int | None = None
+    footprint_mask: bool = False
+
+    def __post_init__(self):
+        if self.boundary not in ("replicate", "valid"):
+            raise ValueError(f"unknown boundary mode {self.boundary!r}")
+        if np.isscalar(self.percentile) or np.ndim(self.percentile) == 0:
+            p = float(self.percentile)
+            if not 0.0 <= p <= 1.0:
+                raise ValueError("percentile must be in [0, 1]")
+
+
+@dataclass(frozen=True)
+class TileGrid:
+    """Reference-compatible tile grid summary (tiling.py:81-91)."""
+
+    out_h: int
+    out_w: int
+    tile_size: int
+    forwarding: bool
+
+
+def decompose(image_shape: tuple[int, int], params: FilterParams) -> TileGrid:
+    """Validate radius / output size / tile size like tiling.py:94-131."""
+    r = params.shape.radius
+    if r > MAX_RADIUS:
+        raise ValueError(
+            f"radius {r} exceeds the maximum of {MAX_RADIUS} (input tiles "
+            "are capped at 256 pixels per side)")
+    h, w = image_shape
+    if params.boundary == "valid":
+        h, w = h - 2 * r, w - 2 * r
+        if h <= 0 or w <= 0:
+            raise ValueError("image smaller than the kernel in valid mode")
+    if h <= 0 or w <= 0:
+        raise ValueError("image is empty")
+    seed_extra = 1 if params.forwarding else 0
+    if params.tile_size is not None:
+        t = params.tile_size
+        if t < 1:
+            raise ValueError("tile size must be positive")
+        if t + 2 * r + seed_extra > MAX_TILE_SIDE:
+            raise ValueError(
+                f"tile size {t} with radius {r} exceeds the "
+                f"{MAX_TILE_SIDE}-pixel input tile cap")
+    else:
+        t = min(DEFAULT_OUTPUT_TILE, MAX_TILE_SIDE - 2 * r - seed_extra)
+    return TileGrid(out_h=h, out_w=w, tile_size=t, forwarding=params.forwarding)
+
+
+def pad_image(image: np.ndarray, r: int, mode: str) -> np.ndarray:
+    """Host padding helper kept for API parity (tiling.py:134-145).
+
+    The GPU path never materializes the padded image: replicate padding is a
+    coordinate clamp inside the tile load.
+    """
+    if mode == "replicate":
+        if r == 0:
+            return image
+        pads = ((r, r), (r, r)) + ((0, 0),) * (image.ndim - 2)
+        return np.pad(image, pads, mode="edge")
+    if mode == "valid":
+        if image.shape[0] < 2 * r + 1 or image.shape[1] < 2 * r + 1:
+            raise ValueError("image smaller than the kernel in valid mode")
+        return image
+    raise ValueError(f"unknown boundary mode {mode!r}")
+
+
+# ----------------------------------------------------------------- helpers
+
+_DTYPES = {np.dtype(np.uint8): 0, np.dtype(np.uint16): 1, np.dtype(np.float32): 2}
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _is_tensor(x) -> bool:
+    try:
+        import torch
+    except ImportError:  # pragma: no cover
+        return False
+    return isinstance(x, torch.Tensor)
+
+
+def _np_dtype_of(x) -> np.dtype:
+    if _is_tensor(x):
+        torch = _torch()
+        m = {torch.uint8: np.uint8, torch.uint16: np.uint16, torch.float32: np.float32}
+        if x.dtype not in m:
+            return np.dtype(str(x.dtype).replace("torch.", ""))
+        return np.dtype(m[x.dtype])
+    return x.dtype
+
+
+def _check_dtype(dt):
+    if dt not in _DTYPES:
+        raise ValueError(f"unsupported image dtype {dt}; use uint8, uint16, or float32")
+
+
+def _target_spec(area: int, percentile, out_shape, device):
+    """(scalar target, device target map or None, tmin, tmax) -- tiling.py:165-177."""
+    if np.isscalar(percentile) or np.ndim(percentile) == 0:
+        t = target_rank(area, float(percentile))
+        return t, None, t, t
+    if _is_tensor(percentile):
+        pmap = percentile.detach().cpu().numpy().astype(np.float64)
+    else:
+        pmap = np.asarray(percentile, dtype=np.float64)
+    if pmap.shape != tuple(out_shape):
+        raise ValueError(
+            f"percentile map shape {pmap.shape} does not match the output "
+            f"shape {tuple(out_shape)}")
+    if pmap.min() < 0.0 or pmap.max() > 1.0:
+        raise ValueError("percentile map values must lie in [0, 1]")
+    targets = np.clip(np.floor(pmap * (area - 1) + 0.5).astype(np.int64), 0, area - 1)
+    torch = _torch()
+    tmap = torch.from_numpy(targets.astype(np.int32)).to(device)
+    return 0, tmap, int(targets.min()), int(targets.max())
+
+
+class _Workspace:
+    """Per-device cached workspace (grown on demand)."""
+
+    def __init__(self):
+        self.buf = {}
+        self.lock = threading.Lock()
+
+    def get(self, device, nbytes: int):
+        torch = _torch()
+        key = device.index if device.index is not None else torch.cuda.current_device()
+        with self.lock:
+            cur = self.buf.get(key)
+            if cur is None or cur.numel() < nbytes:
+                cur = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=device)
+                self.buf[key] = cur
+            return cur
+
+
+_WS = _Workspace()
+
+
+def _kernel_struct(kernel):
+    keep = [np.ascontiguousarray(a, dtype=np.int32) for a in
+            (kernel.row_dy, kernel.row_xlo, kernel.row_xhi, kernel.col_dx,
+             kernel.col_ytop, kernel.col_ybot)]
+    ks = _lib.ImfKernel(kernel.shape_code, kernel.radius, kernel.area, len(kernel.row_dy),
+                        keep[0].ctypes.data, keep[1].ctypes.data, keep[2].ctypes.data,
+                        len(kernel.col_dx), keep[3].ctypes.data, keep[4].ctypes.data,
+                        keep[5].ctypes.data)
+    return ks, keep
+
+
+def _image_struct(t, dt_code, batched: bool, has_c: bool):
+    """imf_image for a CUDA tensor of shape ([B,] H, W[, C])."""
+    shape = list(t.shape)
+    strides = list(t.stride())
+    if not has_c:
+        shape.append(1)
+        strides.append(0)
+    if not batched:
+        shape.insert(0, 1)
+        strides.insert(0, 0)
+    b, h, w, c = shape
+    sb, sy, sx, sc = strides
+    return _lib.ImfImage(t.data_ptr(), dt_code, b, h, w, c, sb, sy, sx, sc)
+
+
+def run_device(src, params: FilterParams, out=None, *, batched: bool = False, stream=None,
+               check: bool = True, kernel=None):
+    """Filter a CUDA tensor ([B,] H, W[, C]) into a new (or given) CUDA tensor.
+
+    Host prologue (validation, kernel, targets) is the caller's job except for
+    the target map; this is the device half of :func:`filter_image`.
+    """
+    torch = _torch()
+    L = _lib.lib()
+    dt = _np_dtype_of(src)
+    dt_code = _DTYPES[dt]
+    kernel = kernel or make_kernel(params.shape)
+    r = params.shape.radius
+    has_c = src.dim() == (4 if batched else 3)
+    h, w = src.shape[1:3] if batched else src.shape[0:2]
+    valid = params.boundary == "valid"
+    out_h, out_w = (h - 2 * r, w - 2 * r) if valid else (h, w)
+    if out is None:
+        oshape = list(src.shape)
+        hy = 1 if batched else 0
+        oshape[hy], oshape[hy + 1] = out_h, out_w
+        out = torch.empty(oshape, dtype=src.dtype, device=src.device)
+    target, tmap, tmin, tmax = _target_spec(kernel.area, params.percentile, (out_h, out_w),
+                                            src.device)
+    ks, keep = _kernel_struct(kernel)
+    simg = _image_struct(src, dt_code, batched, has_c)
+    dimg = _image_struct(out, dt_code, batched, has_c)
+    opt = _lib.ImfOptions(1 if valid else 0, int(params.tile_size or 0), 0, 0)
+    need = L.imf_workspace_size(ctypes.byref(simg), ctypes.byref(ks), ctypes.byref(opt))
+    if need == 0:
+        raise ValueError("unsupported filter geometry for the CUDA engine")
+    ws = _WS.get(src.device, need)
+    if stream is None:
+        stream = torch.cuda.current_stream(src.device)
+    sptr = ctypes.c_void_p(stream.cuda_stream)
+    st = L.imf_filter(ctypes.byref(simg), ctypes.byref(dimg), ctypes.byref(ks), target,
+                      None if tmap is None else tmap.data_ptr(), tmin, tmax, ctypes.byref(opt),
+                      ws.data_ptr(), ws.numel(), sptr)
+    if st != _lib.IMF_OK:
+        raise RuntimeError(f"imf_filter failed: {_lib.strerror(st)}")
+    if check:
+        st = L.imf_workspace_status(ws.data_ptr(), sptr)
+        if st == _lib.IMF_ERR_DEFECT:
+            raise ScanDefectError("segment scan exhausted while solving tile; "
+                                  "pivot/count state was inconsistent")
+        if st != _lib.IMF_OK:
+            raise RuntimeError(f"imf_filter failed: {_lib.strerror(st)}")
+    del keep, tmap
+    return out
+
+
+def _validate_plane(shape2d, dt, has_nan, params: FilterParams):
+    """tiling.py:222-233 checks for one 2D plane, in the reference order."""
+    if len(shape2d) != 2 or shape2d[0] * shape2d[1] == 0:
+        raise ValueError("image must be a non-empty 2D or 3D array")
+    if dt == np.float32 and has_nan():
+        raise ValueError("image contains NaN; NaN has no rank under the "
+                         "total order used by this filter")
+    kernel = make_kernel(params.shape)
+    grid = decompose(tuple(shape2d), params)
+    if params.boundary == "valid":
+        pad_image_check(shape2d, params.shape.radius)
+    if not (np.isscalar(params.percentile) or np.ndim(params.percentile) == 0):
+        pshape = tuple(np.shape(params.percentile))
+        if pshape != (grid.out_h, grid.out_w):
+            raise ValueError(
+                f"percentile map shape {pshape} does not match the output "
+                f"shape {(grid.out_h, grid.out_w)}")
+    return kernel, grid
+
+
+def pad_image_check(shape2d, r):
+    if shape2d[0] < 2 * r + 1 or shape2d[1] < 2 * r + 1:
+        raise ValueError("image smaller than the kernel in valid mode")
+
+
+def filter_image(image, params: FilterParams):
+    """Rank-order filter a full image on the GPU (drop-in for tiling.py:213)."""
+    is_t = _is_tensor(image)
+    if not is_t:
+        image = np.asarray(image)
+    dt = _np_dtype_of(image)
+    _check_dtype(dt)
+    ndim = image.dim() if is_t else image.ndim
+    shape = tuple(image.shape)
+    if is_t:
+        has_nan = lambda: bool(_torch().isnan(image).any()) if dt == np.float32 else False
+    else:
+        has_nan = lambda: bool(np.isnan(image).any())
+    if ndim == 3:
+        if shape[2] == 0:
+            raise ValueError("need at least one array to concatenate")
+        kernel, _ = _validate_plane(shape[:2], dt, has_nan, params)
+    else:
+        kernel, _ = _validate_plane(shape, dt, has_nan, params)
+
+    torch = _torch()
+    if not torch.cuda.is_available():
+        raise RuntimeError("the B200 rank-order filter needs a CUDA device (no CPU fallback)")
+    if is_t and image.is_cuda:
+        return run_device(image, params, kernel=kernel)
+    if is_t:
+        src = image.to("cuda", non_blocking=False)
+        return run_device(src, params, kernel=kernel).cpu()
+    src = torch.from_numpy(np.ascontiguousarray(image)).to("cuda")
+    return run_device(src, params, kernel=kernel).cpu().numpy()
+
+
+def filter_batch(images, params: FilterParams, out=None, *, check: bool = True, stream=None):
+    """Filter a CUDA batch (B, H, W[, C]) in one launch sequence (images share params)."""
+    if not images.is_cuda:
+        raise ValueError("filter_batch expects a CUDA tensor")
+    dt = _np_dtype_of(images)
+    _check_dtype(dt)
+    kernel, _ = _validate_plane(tuple(images.shape[1:3]), dt,
+                                lambda: bool(_torch().isnan(images).any()) if dt == np.float32
+                                else False, params)
+    return run_device(images, params, out=out, batched=True, check=check, stream=stream,
+                      kernel=kernel)
