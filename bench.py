@@ -1,0 +1,398 @@
+#!/usr/bin/env python
+"""bench.py -- B200 rank-order (circular median) filter benchmark.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload c2|c1|c3|c4|c5] [--radius R]
+
+Contract:
+* one process per GPU (torchrun for N > 1; NCCL only for the barrier and the
+  max-over-ranks reduction of the timings -- the path itself has no collective);
+* a "step" = one pass of the filter over one batch of synthetic input: by
+  default the BASELINE c2 workload (3840x2160 u16 RGB, circle r=48, median),
+  one image per rank (weak scaling: each rank filters its own frame);
+* `value`: whole-job megapixels/s with the input resident in HBM, timed with
+  CUDA events per step, L2 flushed (256 MiB memset) between steps, max over
+  ranks; `e2e`: the same metric through the public call with pinned HOST
+  buffers, H2D + filter + D2H inside the timed region;
+* `roofline`: the selection kernel (K2) against the integer-pipe peak measured
+  on the box (imf_int_peak), work W(r) = 4*C(r) + 384 int ops per channel-pixel
+  (SURVEY.md 8(d)), K2 time from CUDA events around each K2 launch;
+* `cpu_baseline`: the reference algorithm restated in C (oracle/, all host
+  threads) on the same c2 frame -- rank 0, N = 1 only;
+* `--impl reference`: that CPU reference alone, rank 0 only, same metric.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests", "golden"))
+
+import cases as C  # noqa: E402  (deterministic synthetic inputs)
+
+WORKLOADS = {
+    "c1": dict(desc="512x512 u8 gray, circle r=8, median, replicate", spec=("circle", 8, 0, 0.0)),
+    "c2": dict(desc="3840x2160 u16 RGB, circle r=48, median, replicate",
+               spec=("circle", 48, 0, 0.0)),
+    "c3": dict(desc="2048x2048 f32 gray, circle r={r}, median, replicate",
+               spec=("circle", 48, 0, 0.0)),
+    "c4": dict(desc="3840x2160 u8 RGB, 12-gon r=32, median, replicate",
+               spec=("regular_polygon", 32, 12, 0.0)),
+    "c5": dict(desc="batch of 64 7680x4320 u16 gray, circle r=64, median; images split across "
+                    "ranks", spec=("circle", 64, 0, 0.0)),
+}
+DT_NAME = {np.dtype(np.uint8): "u8", np.dtype(np.uint16): "u16", np.dtype(np.float32): "f32"}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--radius", type=int, default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def workload_inputs(name, rank, world):
+    """Per-rank host images (list) and the spec for the workload."""
+    spec = WORKLOADS[name]["spec"]
+    if name == "c5":
+        idx = list(range(rank, 64, world))
+        return [C.baseline_input("c5", i) for i in idx], spec
+    return [C.baseline_input(name)], spec
+
+
+def workload_spec(args):
+    spec = WORKLOADS[args.workload]["spec"]
+    if args.radius is not None:
+        spec = (spec[0], args.radius, spec[2], spec[3])
+    return spec
+
+
+def mp_of(images):
+    return sum(im.shape[0] * im.shape[1] for im in images) / 1e6
+
+
+def chp_of(images):
+    return sum(im.shape[0] * im.shape[1] * (im.shape[2] if im.ndim == 3 else 1)
+               for im in images) / 1e6
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled while the timed region runs."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.out = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.out.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self.th.join(timeout=2)
+
+    def summary(self):
+        sm, mx, reasons = [], 0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.out:
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = max(mx, float(f[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def work_per_chpx(kernel):
+    """W(r) = 4*C + 384 int ops per channel-pixel (SURVEY.md 8(d), S-bar = 1)."""
+    return 4 * len(kernel.col_dx) + 384
+
+
+def load_ncu_traffic():
+    p = os.path.join(ROOT, "profiles", "ncu_select_c2.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get("dram_bytes_per_launch"), d.get("source")
+    except (OSError, ValueError):
+        return None, None
+
+
+def cpu_reference_run(images, spec, threads):
+    import oracle  # CPU baseline leg only (test infrastructure)
+    from paper_2505_22938_b200 import ShapeSpec
+    shape = ShapeSpec(*spec)
+    t0 = time.perf_counter()
+    for im in images:
+        oracle.fast_filter(im, shape, 0.5, "replicate", threads=threads)
+    return time.perf_counter() - t0
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    spec = workload_spec(args)
+    images, _ = workload_inputs(args.workload, 0, 1)
+    if args.workload == "c5":
+        images = images[:2]  # bounded sample
+    threads = os.cpu_count() or 1
+    for _ in range(args.warmup):
+        cpu_reference_run(images, spec, threads)
+    total = 0.0
+    for _ in range(args.steps):
+        total += cpu_reference_run(images, spec, threads)
+    mp = mp_of(images)
+    value = mp * args.steps / total
+    im0 = images[0]
+    line = {
+        "impl": "reference",
+        "metric": "megapixels/sec circular median (r=8..100, 8/16-bit/f32)",
+        "value": round(value, 4), "unit": "MP/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(1e3 * total / args.steps, 2),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": DT_NAME[im0.dtype], "data": "synthetic (numpy default_rng seeds, SURVEY.md 8(d))",
+        "config": {"workload": f"{args.workload}: {WORKLOADS[args.workload]['desc'].format(r=spec[1])}",
+                   "images_per_step": len(images)},
+        "cpu_baseline": {"value": round(value, 4), "unit": "MP/s", "cores": threads,
+                         "kind": "port",
+                         "sample": f"{len(images)} full {args.workload} image(s) per step "
+                                   "(reference fast engine restated in C, oracle/, pthreads "
+                                   "over tile columns, forwarding on)"},
+        "e2e": {"value": round(value, 4), "unit": "MP/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2505_22938_b200 import FilterParams, ShapeSpec, _lib, filter_batch, make_kernel
+    from paper_2505_22938_b200.tiling import run_device, workspace_for
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    spec = workload_spec(args)
+    params = FilterParams(shape=ShapeSpec(*spec))
+    kernel = make_kernel(params.shape)
+    images, _ = workload_inputs(args.workload, rank, world)
+    host = torch.from_numpy(np.stack(images))          # (B, H, W[, C])
+    host_pin = host.pin_memory()
+    src = host_pin.to(dev)
+    out = torch.empty_like(src)
+    out_pin = torch.empty_like(host_pin).pin_memory()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    L = _lib.lib()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def step(profile=False):
+        if profile:
+            return run_device(src, params, out=out, batched=True, check=False, kernel=kernel,
+                              profile=True)
+        return run_device(src, params, out=out, batched=True, check=False, kernel=kernel)
+
+    # ---- device-resident timing -------------------------------------------
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    ws = workspace_for(dev)
+    if L.imf_workspace_status(ws.data_ptr(), ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)):
+        raise RuntimeError("scan defect during warm-up")
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    sort_ms = select_ms = 0.0
+    k2_launches = 0
+    launches0 = L.imf_launch_count()
+    barrier()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.zero_()
+            evs[i][0].record()
+            step(profile=True)
+            evs[i][1].record()
+            a, b, n = ctypes.c_float(), ctypes.c_float(), ctypes.c_int32()
+            L.imf_profile_last(ctypes.byref(a), ctypes.byref(b), ctypes.byref(n), None, None, None)
+            sort_ms += a.value
+            select_ms += b.value
+            k2_launches += n.value
+        barrier()
+    launches = L.imf_launch_count() - launches0
+    dev_ms = sum(e0.elapsed_time(e1) for e0, e1 in evs)
+    t = torch.tensor([dev_ms, sort_ms, select_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dev_ms_max, sort_max, select_max = t.tolist()
+
+    # ---- end-to-end through the public call with host buffers ---------------
+    e2e = None
+    if not args.no_e2e:
+        def e2e_step():
+            src.copy_(host_pin, non_blocking=True)
+            run_device(src, params, out=out, batched=True, check=False, kernel=kernel)
+            out_pin.copy_(out, non_blocking=True)
+        for _ in range(args.warmup):
+            e2e_step()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.steps):
+            e2e_step()
+        e1.record()
+        barrier()
+        e2e_ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
+        e2e = e2e_ms.item()
+    st = L.imf_workspace_status(ws.data_ptr(), ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+    if st:
+        raise RuntimeError(f"scan defect / error in timed region: {_lib.strerror(st)}")
+
+    # ---- parity spot check of the timed output (c2: golden digest) ----------
+    parity = None
+    if rank == 0 and args.workload in ("c1", "c2") and args.radius is None:
+        with open(os.path.join(ROOT, "tests", "golden", "golden.json")) as f:
+            gold = json.load(f)["baseline"][args.workload]
+        parity = C.digest(out_pin[0].numpy()) == gold
+
+    peak = ctypes.c_double()
+    L.imf_int_peak(ctypes.byref(peak), None)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank != 0:
+        return 0
+
+    mp_rank = mp_of(images)
+    chp_rank = chp_of(images)
+    total_mp = mp_rank * world  # weak scaling: every rank filters its own batch
+    value = total_mp * args.steps / (dev_ms_max * 1e-3)
+    ch_value = chp_rank * world * args.steps / (dev_ms_max * 1e-3)
+    W = work_per_chpx(kernel)
+    k2_ops = chp_rank * 1e6 * W * args.steps  # per rank
+    achieved = k2_ops / (select_max * 1e-3)
+    traffic, tsrc = load_ncu_traffic()
+    im0 = images[0]
+    line = {
+        "metric": "megapixels/sec circular median (r=8..100, 8/16-bit/f32)",
+        "value": round(value, 2), "unit": "MP/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(dev_ms_max / args.steps, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": DT_NAME[im0.dtype],
+        "data": "synthetic (numpy default_rng seeds per SURVEY.md 8(d); no model weights)",
+        "config": {"workload": f"{args.workload}: {WORKLOADS[args.workload]['desc'].format(r=spec[1])}",
+                   "images_per_rank": len(images), "channels": int(im0.shape[2]) if im0.ndim == 3 else 1,
+                   "kernel_area": kernel.area, "kernel_cols": len(kernel.col_dx),
+                   "l2": "flushed between timed steps (256 MiB memset, outside the events)",
+                   "parallelism": f"replicas/shards x{world} (no collective on the path)"},
+        "ch_mp_per_s": round(ch_value, 2),
+        "gpu_launches": int(launches),
+        "kernel_ms_per_step": {"sort_k1": round(sort_max / args.steps, 4),
+                               "select_k2": round(select_max / args.steps, 4)},
+        "roofline": {"bound": "int32", "kernel": "k2_select",
+                     "achieved": round(achieved / 1e12, 3),
+                     "peak": round(peak.value / 1e12, 3), "unit": "Tops/s",
+                     "frac": round(achieved / peak.value, 4),
+                     "work_per_chpx": W,
+                     "peak_source": "measured on this GPU: imf_int_peak (IADD3 chains)",
+                     "path_frac": round(ch_value * 1e6 * W / peak.value, 4),
+                     "traffic": traffic, "traffic_source": tsrc},
+        "clocks": clk.summary(),
+        "parity_digest_ok": parity,
+    }
+    hbm = 2 * im0.dtype.itemsize * ch_value * 1e6 / 1e9
+    line["roofline_hbm"] = {"achieved": round(hbm, 2), "unit": "GB/s",
+                            "note": "algorithmic bytes = read+write once per channel-pixel"}
+    if e2e is not None:
+        e2e_value = total_mp * args.steps / (e2e * 1e-3)
+        line["e2e"] = {"value": round(e2e_value, 2), "unit": "MP/s",
+                       "h2d_bytes_per_step": int(host.numel() * host.element_size()),
+                       "d2h_bytes_per_step": int(out_pin.numel() * out_pin.element_size())}
+    if world == 1 and not args.no_cpu_baseline:
+        spec_c = spec
+        cpu_imgs = images if args.workload != "c5" else images[:1]
+        threads = os.cpu_count() or 1
+        secs = cpu_reference_run(cpu_imgs, spec_c, threads)
+        line["cpu_baseline"] = {"value": round(mp_of(cpu_imgs) / secs, 4), "unit": "MP/s",
+                                "cores": threads, "kind": "port",
+                                "sample": f"{len(cpu_imgs)} full {args.workload} image(s), one pass "
+                                          f"({secs:.2f} s): reference fast engine restated in C "
+                                          "(oracle/), pthreads over tile columns"}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -120,6 +120,15 @@ int imf_version(void);                  /* 100 * major + minor */
 const char* imf_last_error(void);       /* detail of the last IMF_ERR_CUDA on this thread */
 uint64_t imf_launch_count(void);        /* kernels launched by this process (diagnostic) */
 
+/* Per-kernel device time of the last imf_filter on this thread that ran with
+ * opt->reserved[0] & 1 (events on its stream; that call synchronizes). */
+int imf_profile_last(float* sort_ms, float* select_ms, int32_t* launches, int64_t* tiles,
+                     int32_t* tile_side, int32_t* qshift);
+
+/* Measured int32 add throughput of the current device (ops/s): the
+ * denominator of the selection kernel's integer roofline. */
+int imf_int_peak(double* ops_per_s, double* ms);
+
 #ifdef __cplusplus
 }
 #endif

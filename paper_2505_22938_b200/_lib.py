@@ -23,7 +23,8 @@ IMF_ERR_WORKSPACE = 4
 IMF_ERR_UNSUPPORTED = 5
 
 EXPORTED = ("imf_workspace_size", "imf_filter", "imf_workspace_status", "imf_filter_host",
-            "imf_strerror", "imf_version", "imf_last_error", "imf_launch_count")
+            "imf_strerror", "imf_version", "imf_last_error", "imf_launch_count",
+            "imf_profile_last", "imf_int_peak")
 
 _i32p = ctypes.POINTER(ctypes.c_int32)
 
@@ -79,6 +80,11 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.imf_last_error.restype = ctypes.c_char_p
     lib.imf_launch_count.argtypes = []
     lib.imf_launch_count.restype = ctypes.c_uint64
+    lib.imf_profile_last.argtypes = [P(ctypes.c_float), P(ctypes.c_float), P(ctypes.c_int32),
+                                     P(ctypes.c_int64), P(ctypes.c_int32), P(ctypes.c_int32)]
+    lib.imf_profile_last.restype = ctypes.c_int
+    lib.imf_int_peak.argtypes = [P(ctypes.c_double), P(ctypes.c_double)]
+    lib.imf_int_peak.restype = ctypes.c_int
     return lib
 
 

@@ -17,6 +17,14 @@ using namespace imf;
 static std::atomic<uint64_t> g_launches{0};
 static thread_local char g_err[256];
 
+struct ProfileRec {
+    float sort_ms = 0.f, select_ms = 0.f;
+    int launches = 0;
+    long long tiles = 0, chunk = 0;
+    int tile = 0, qs = 0;
+};
+static thread_local ProfileRec g_prof;
+
 static int cuda_fail(cudaError_t e, const char* where) {
     snprintf(g_err, sizeof(g_err), "%s: %s", where, cudaGetErrorString(e));
     return IMF_ERR_CUDA;
@@ -31,11 +39,10 @@ constexpr size_t kOmegaScratchTarget = 96ull << 20;  // stays mostly L2-resident
 
 struct Plan {
     Geom g;
-    int G, K, k2_threads, k1_threads;
-    bool k1_gmem;
+    int G, k2_threads, k1_threads;
+    bool k1_gmem, k1_count, omg;
     size_t k1_smem, k2_smem, k1_gs_per_tile;
     long long total_tiles, chunk_tiles;
-    int qs, qb, P_lo, P_hi;
     size_t ws_ktab, ws_omega, ws_k1g, ws_total;
     int ktab_n;
 };
@@ -47,8 +54,12 @@ int env_int(const char* name, int dflt) {
 
 int dtype_size(int dt) { return dt == IMF_DTYPE_U8 ? 1 : (dt == IMF_DTYPE_U16 ? 2 : 4); }
 
-int make_plan(const imf_image* src, const imf_kernel* k, const imf_options* opt, int tmin, int tmax,
-              Plan* pl) {
+// Tile geometry: output tile side T (input side S = T + 2r <= 255 so ranks,
+// positions and 16-bit histogram counters fit), seed rows G, and whether omega
+// stays in global memory (OMG).  Among feasible shapes pick the one with the
+// most output pixels per sorted input pixel (T^2 / S^2, the sort amortization,
+// SURVEY.md App. C), slightly preferring omega in shared memory.
+int make_plan(const imf_image* src, const imf_kernel* k, const imf_options* opt, Plan* pl) {
     if (!src || !k || !opt) return IMF_ERR_INVALID;
     if (src->dtype < 0 || src->dtype > 2) return IMF_ERR_INVALID;
     const int r = k->radius;
@@ -59,35 +70,37 @@ int make_plan(const imf_image* src, const imf_kernel* k, const imf_options* opt,
     const int valid = opt->boundary == IMF_BOUNDARY_VALID;
     const int out_h = valid ? H - 2 * r : H, out_w = valid ? W - 2 * r : W;
     if (out_h < 1 || out_w < 1) return IMF_ERR_INVALID;
-    if (tmin < 0 || tmax >= k->area || tmin > tmax) return IMF_ERR_INVALID;
 
     Plan& p = *pl;
     memset(&p, 0, sizeof(p));
-    int T = opt->tile_size > 0 ? opt->tile_size : env_int("IMF_TILE", 64);
-    T = std::min(T, 256 - 2 * r);
-    T = std::max(T, 1);
+    const int Tmax = std::max(1, std::min(opt->tile_size > 0 ? opt->tile_size : env_int("IMF_TILE", 64),
+                                          255 - 2 * r));
     const int G0 = opt->seed_rows > 0 ? opt->seed_rows : env_int("IMF_SEED_ROWS", 4);
-    for (;; T = T > 8 ? T - 4 : T - 1) {
-        if (T < 1) return IMF_ERR_UNSUPPORTED;
+    double best = -1.0;
+    for (int T = Tmax; T >= 1; T--) {
         const int S = T + 2 * r;
         const int N = S * S, Npad = (N + 63) & ~63;
         const int G = std::max(1, std::min(G0, T));
-        int K = opt->seeds_per_row > 0 ? opt->seeds_per_row : env_int("IMF_SEEDS", std::max(1, T / 16));
-        K = std::max(1, std::min(K, T));
-        const int thr = ((T * G * 2 + 31) / 32) * 32;
-        const int k2thr = std::min(thr, 512);
-        const size_t k2s = k2_smem_bytes(N, Npad, k->ncols, k->nrows, r, G, K, T, k2thr / 32);
-        if (k2s > kSmemMax) continue;
-        p.g.Tw = p.g.Th = T;
-        p.g.Sw = p.g.Sh = S;
-        p.g.N = N;
-        p.g.Npad = Npad;
-        p.G = G;
-        p.K = K;
-        p.k2_threads = k2thr;
-        p.k2_smem = k2s;
-        break;
+        const int thr = std::min(((T * G * 2 + 31) / 32) * 32, 512);
+        for (int omg = 0; omg < 2; omg++) {
+            const size_t k2s = k2_smem_bytes(N, Npad, k->ncols, k->nrows, r, G, T, T, omg != 0);
+            if (k2s > kSmemMax) continue;
+            const double score = (double)T * T / ((double)S * S) * (omg ? 0.9 : 1.0);
+            if (score > best) {
+                best = score;
+                p.g.Tw = p.g.Th = T;
+                p.g.Sw = p.g.Sh = S;
+                p.g.N = N;
+                p.g.Npad = Npad;
+                p.G = G;
+                p.k2_threads = thr;
+                p.k2_smem = k2s;
+                p.omg = omg != 0;
+            }
+        }
+        if (best > 0 && T * 2 < Tmax) break;  // smaller tiles only lose amortization
     }
+    if (best < 0) return IMF_ERR_UNSUPPORTED;
     Geom& g = p.g;
     g.dtype = src->dtype;
     g.B = src->batch;
@@ -107,36 +120,22 @@ int make_plan(const imf_image* src, const imf_kernel* k, const imf_options* opt,
     p.total_tiles = (long long)g.tiles_x * g.tiles_y * g.C * g.B;
 
     p.k1_threads = kK1Threads;
-    p.k1_gmem = k1_smem_bytes(g.dtype, g.Npad, p.k1_threads / 32, false) > kSmemMax;
-    p.k1_smem = k1_smem_bytes(g.dtype, g.Npad, p.k1_threads / 32, p.k1_gmem);
+    p.k1_count = g.dtype != DT_F32 && k1_count_smem_bytes(g.dtype, g.Npad) <= kSmemMax;
+    p.k1_gmem = !p.k1_count && k1_smem_bytes(g.dtype, g.Npad, p.k1_threads / 32, false) > kSmemMax;
+    p.k1_smem = p.k1_count ? k1_count_smem_bytes(g.dtype, g.Npad)
+                           : k1_smem_bytes(g.dtype, g.Npad, p.k1_threads / 32, p.k1_gmem);
     p.k1_gs_per_tile = p.k1_gmem ? k1_gscratch_bytes(g.dtype, g.Npad) : 0;
 
-    // Quantization of the ordinal image: smallest qs >= 6 such that
-    // every pivot nearest a possible solution rank in [tmin, N - area + tmax] has
-    // (P >> qs) - qb within [1, 255].  Pivots are clamped to [P_lo, P_hi] anyway,
-    // so exactness never depends on this choice -- only the refine distance does.
-    const int lo = tmin, hi = g.N - k->area + tmax;
-    int qs = 6, qb = 0;
-    for (; qs < 16; qs++) {
-        qb = std::max(0, (lo >> qs) - 1);
-        const int pmax = ((hi + (1 << (qs - 1))) >> qs) - qb;
-        if (pmax <= 255) break;
-    }
-    p.qs = qs;
-    p.qb = qb;
-    p.P_lo = (qb + 1) << qs;
-    const int ncap = ((g.N + (1 << qs) - 1) >> qs) << qs;
-    p.P_hi = std::max(p.P_lo, std::min((qb + 255) << qs, ncap));
-
     p.ktab_n = 2 * k->ncols + 2 * k->nrows + 2 * r + 1;
-    const size_t per_tile = 2 * (size_t)g.Npad + p.k1_gs_per_tile;
+    const size_t slot = 2 * (size_t)(g.Npad + 2 * OMEGA_SLOT_PAD);
+    const size_t per_tile = slot + p.k1_gs_per_tile;
     long long chunk = (long long)(kOmegaScratchTarget / per_tile);
     chunk = std::max<long long>(chunk, 148);
     chunk = std::min<long long>(chunk, p.total_tiles);
     chunk = std::min<long long>(chunk, 65535LL * 1024);
     p.chunk_tiles = chunk;
     p.ws_ktab = ((size_t)p.ktab_n * 4 + 255) & ~(size_t)255;
-    p.ws_omega = (size_t)chunk * 2 * g.Npad;
+    p.ws_omega = (((size_t)chunk * slot) + 255) & ~(size_t)255;
     p.ws_k1g = (size_t)chunk * p.k1_gs_per_tile;
     p.ws_total = kStatusBytes + p.ws_ktab + p.ws_omega + p.ws_k1g;
     return IMF_OK;
@@ -182,8 +181,12 @@ cudaError_t set_attrs() {
     if (!e) e = allow_smem(k1_sort<DT_U16, true>, optin);
     if (!e) e = allow_smem(k1_sort<DT_F32, false>, optin);
     if (!e) e = allow_smem(k1_sort<DT_F32, true>, optin);
-    if (!e) e = allow_smem(k2_select<true>, optin);
-    if (!e) e = allow_smem(k2_select<false>, optin);
+    if (!e) e = allow_smem(k1_count<DT_U8>, optin);
+    if (!e) e = allow_smem(k1_count<DT_U16>, optin);
+    if (!e) e = allow_smem(k2_select<true, false>, optin);
+    if (!e) e = allow_smem(k2_select<false, false>, optin);
+    if (!e) e = allow_smem(k2_select<true, true>, optin);
+    if (!e) e = allow_smem(k2_select<false, true>, optin);
     if (!e) g_attr_done = true;
     return e;
 }
@@ -192,6 +195,13 @@ void launch_k1(const Plan& p, const Geom& g, int nblocks, uint16_t* omega, unsig
                cudaStream_t s) {
     const dim3 grid(nblocks), block(p.k1_threads);
     const long long gs = (long long)p.k1_gs_per_tile;
+    if (p.k1_count) {
+        if (g.dtype == DT_U8)
+            k1_count<DT_U8><<<grid, block, p.k1_smem, s>>>(g, omega);
+        else
+            k1_count<DT_U16><<<grid, block, p.k1_smem, s>>>(g, omega);
+        return;
+    }
     switch (g.dtype * 2 + (p.k1_gmem ? 1 : 0)) {
         case 0:
         case 1: k1_sort<DT_U8, false><<<grid, block, p.k1_smem, s>>>(g, omega, k1g, gs); break;
@@ -208,7 +218,7 @@ extern "C" {
 
 size_t imf_workspace_size(const imf_image* src, const imf_kernel* kernel, const imf_options* opt) {
     Plan p;
-    if (make_plan(src, kernel, opt, 0, kernel ? kernel->area - 1 : 0, &p) != IMF_OK) return 0;
+    if (make_plan(src, kernel, opt, &p) != IMF_OK) return 0;
     return p.ws_total;
 }
 
@@ -219,8 +229,10 @@ int imf_filter(const imf_image* src, imf_image* dst, const imf_kernel* kernel, i
     if (dst->dtype != src->dtype || dst->batch != src->batch || dst->channels != src->channels)
         return IMF_ERR_INVALID;
     if (!target_map) tmin = tmax = target;
+    if (tmin < 0 || tmax >= kernel->area || tmin > tmax || target < 0 || target >= kernel->area)
+        return IMF_ERR_INVALID;
     Plan p;
-    int st = make_plan(src, kernel, opt, tmin, tmax, &p);
+    int st = make_plan(src, kernel, opt, &p);
     if (st) return st;
     if (dst->height != p.g.out_h || dst->width != p.g.out_w) return IMF_ERR_INVALID;
     if (!workspace || workspace_bytes < p.ws_total) return IMF_ERR_WORKSPACE;
@@ -255,26 +267,72 @@ int imf_filter(const imf_image* src, imf_image* dst, const imf_kernel* kernel, i
     sp.nrows = kernel->nrows;
     sp.target = target;
     sp.tmap = target_map;
-    sp.qs = p.qs;
-    sp.qb = p.qb;
-    sp.P_lo = p.P_lo;
-    sp.P_hi = p.P_hi;
     sp.G = p.G;
-    sp.K = p.K;
     sp.ktab = ktab_d;
     sp.status = status;
 
+    // Optional per-kernel timing (opt->reserved[0] & 1): CUDA events recorded on
+    // `stream` around every launch; the call then synchronizes and leaves the
+    // sums in imf_profile_last().  Used by bench.py for the roofline figure.
+    const bool prof = (opt->reserved[0] & 1) != 0;
+    std::vector<cudaEvent_t> ev;
     for (long long t0 = 0; t0 < p.total_tiles; t0 += p.chunk_tiles) {
         const int nb = (int)std::min(p.chunk_tiles, p.total_tiles - t0);
         g.tile_begin = t0;
+        cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr;
+        if (prof) {
+            cudaEventCreate(&e0);
+            cudaEventCreate(&e1);
+            cudaEventCreate(&e2);
+            cudaEventRecord(e0, s);
+        }
         launch_k1(p, g, nb, omega, k1g, s);
-        if (sp.circle)
-            k2_select<true><<<nb, p.k2_threads, p.k2_smem, s>>>(g, sp, omega);
+        if (prof) cudaEventRecord(e1, s);
+        if (sp.circle && !p.omg)
+            k2_select<true, false><<<nb, p.k2_threads, p.k2_smem, s>>>(g, sp, omega);
+        else if (!p.omg)
+            k2_select<false, false><<<nb, p.k2_threads, p.k2_smem, s>>>(g, sp, omega);
+        else if (sp.circle)
+            k2_select<true, true><<<nb, p.k2_threads, p.k2_smem, s>>>(g, sp, omega);
         else
-            k2_select<false><<<nb, p.k2_threads, p.k2_smem, s>>>(g, sp, omega);
+            k2_select<false, true><<<nb, p.k2_threads, p.k2_smem, s>>>(g, sp, omega);
+        if (prof) {
+            cudaEventRecord(e2, s);
+            ev.push_back(e0);
+            ev.push_back(e1);
+            ev.push_back(e2);
+        }
         g_launches += 2;
     }
     if (cudaError_t e = cudaGetLastError()) return cuda_fail(e, "kernel launch");
+    if (prof) {
+        g_prof = ProfileRec{};
+        if (!ev.empty()) cudaEventSynchronize(ev.back());
+        for (size_t i = 0; i + 2 < ev.size(); i += 3) {
+            float a = 0.f, b = 0.f;
+            cudaEventElapsedTime(&a, ev[i], ev[i + 1]);
+            cudaEventElapsedTime(&b, ev[i + 1], ev[i + 2]);
+            g_prof.sort_ms += a;
+            g_prof.select_ms += b;
+            g_prof.launches += 1;
+        }
+        for (cudaEvent_t e : ev) cudaEventDestroy(e);
+        g_prof.tiles = p.total_tiles;
+        g_prof.tile = p.g.Tw;
+        g_prof.qs = p.omg ? 1 : 0;
+        g_prof.chunk = p.chunk_tiles;
+    }
+    return IMF_OK;
+}
+
+int imf_profile_last(float* sort_ms, float* select_ms, int32_t* launches, int64_t* tiles,
+                     int32_t* tile_side, int32_t* qshift) {
+    if (sort_ms) *sort_ms = g_prof.sort_ms;
+    if (select_ms) *select_ms = g_prof.select_ms;
+    if (launches) *launches = g_prof.launches;
+    if (tiles) *tiles = g_prof.tiles;
+    if (tile_side) *tile_side = g_prof.tile;
+    if (qshift) *qshift = g_prof.qs;
     return IMF_OK;
 }
 
@@ -303,7 +361,7 @@ int imf_filter_host(const imf_image* src, imf_image* dst, const imf_kernel* kern
     cudaStream_t s = (cudaStream_t)stream;
     if (!target_map) tmin = tmax = target;
     Plan p;
-    int st = make_plan(src, kernel, opt, tmin, tmax, &p);
+    int st = make_plan(src, kernel, opt, &p);
     if (st) return st;
     const size_t sb = extent_bytes(src), db = extent_bytes(dst);
     const size_t tb = target_map ? (size_t)p.g.out_h * p.g.out_w * 4 : 0;

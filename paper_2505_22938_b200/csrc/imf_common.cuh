@@ -20,6 +20,8 @@ namespace imf {
 
 enum Dtype : int { DT_U8 = 0, DT_U16 = 1, DT_F32 = 2 };
 
+constexpr int OMEGA_SLOT_PAD = 8;  // sentinel (0xffff) entries around each tile's omega
+
 struct Geom {
     const void* src;
     void* dst;
@@ -47,8 +49,7 @@ struct SelParams {
     int ncols, nrows;
     int target;          // scalar target rank (tiling.py:176-177 / kernels.py:191-192)
     const int* tmap;     // per-pixel target ranks [out_h*out_w] or nullptr
-    int qs, qb, P_lo, P_hi;
-    int G, K;            // seed rows per tile, direct seeds per seed row
+    int G;               // seed rows per tile
     const int* ktab;     // [ncols pairs (VE,VX)][nrows pairs (HP,HM)][2r+1 spans]
     int* status;         // device status word (1 = scan defect)
 };

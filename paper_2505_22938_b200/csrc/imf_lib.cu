@@ -3,3 +3,4 @@
 #include "imf_sort.cu"
 #include "imf_select.cu"
 #include "imf_api.cu"
+#include "imf_peak.cu"

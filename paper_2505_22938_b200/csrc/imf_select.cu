@@ -1,223 +1,140 @@
 // imf_select.cu -- K2: per-output-pixel rank selection on sm_100a.
 //
-// One CTA solves one T_w x T_h output tile from the tile's omega (K1 output):
+// One CTA solves one T_w x T_h output tile from the tile's omega (K1 output).
+// Shared memory holds the rank -> position map omega (u16 per rank, packed
+// x | y << 8, the paper's omnigram) and the full-precision
+// ordinal image I (u16 rank per pixel) of the (T+2r)^2 input tile.
 //
-//   0. stage omega (swizzled, 16-B chunks) and build the quantized ordinal
-//      image Iq in shared memory
-//   1. direct seeds: G seed rows x K seeds, one warp each: 32-bin histogram of
-//      Iq over the window -> a pivot with an exact count -> warp-collaborative
-//      64-rank segment refine (ballot/popc)          (core.py:47-60 _seed_state,
-//                                                      PAPER.md:285-287)
-//   2. seed rows: every column's count at its seed's pivot from a prefix of
-//      horizontal slide deltas, then a per-thread refine
-//                                                     (core.py:63-72 _slide_right)
-//   3. vertical sweeps up and down from each seed row, one thread per
-//      (column, group, direction): count update from the entering/exiting
-//      kernel-column pixels, refine, write C[m]       (core.py:75-84 _slide_down,
-//                                                      :87-146 _refine, :366)
+// Window state (the reference's pivot/count cursor, core.py module docstring
+// and :228-237): a pivot rank P and cnt = #{window pixels with rank < P}.
+// Because I keeps exact ranks, the pivot can be ANY rank, so after a window is
+// solved its state is simply (P, cnt) = (m, t): the solution rank and the
+// target rank (exactly t window pixels rank below the t-th smallest).  The
+// reference rounds the pivot to a multiple of 64 to fit its SIMD layout
+// (core.py:39-44); the output does not depend on the pivot choice because the
+// median is a selection, so both produce the same m.
 //
-// Pivot/count invariant (core.py module docstring): a window carries a pivot P
-// (multiple of 2^qs) and count = #{window pixels with rank < P}; every slide
-// keeps it exact, the refine walks 64-rank segments of omega from P to the
-// target rank.  Because the median is a selection, any exact walk returns the
-// same rank m, so the output equals the reference bit for bit.
+//   A. one direct seed per tile (window at the centre of the tile's middle
+//      seed row): every warp histograms part of the window into 32 rank bins
+//      (warp ballots), giving a pivot with an exact count, then a
+//      warp-collaborative omega scan to the target   (core.py:47-60, :87-146)
+//   B. the other seed rows' centre windows: vertical slide deltas at the seed
+//      pivot computed in parallel, prefix-summed, then warp-collaborative
+//      refines                                          (core.py:75-84)
+//   C. every seed-row window: horizontal slide deltas at its row's pivot in
+//      parallel, prefix-summed, per-thread refine      (core.py:63-72)
+//   D. vertical sweeps up and down from every seed row, one thread per
+//      (column, group, direction): slide + refine + write C[m]
+//                                                       (core.py:75-84, :87-146, :366)
+// The refine walks omega from the pivot toward the target rank testing
+// membership of each rank's pixel in the window (ordinal.py:175-199): eight
+// ranks per step per thread (phase C/D) or sixty-four per warp step (A/B).
 #include "imf_common.cuh"
 
 namespace imf {
 
-
-
 constexpr unsigned FULLM = 0xffffffffu;
+constexpr uint16_t OMEGA_SENTINEL = 0xffffu;  // (255, 255): outside every window (S <= 255)
+constexpr int OMEGA_PAD = 8;                  // sentinel entries on both sides of omega
 
 struct Ctx {
     const Geom* g;
     const SelParams* p;
-    const uint16_t* om;   // swizzled omega
-    const uint8_t* Iq;
-    const int* span;      // 2r+1 packed spans
+    const uint16_t* om;   // omega, om[-8..-1] and om[N..Npad+7] are sentinels
+    const uint16_t* I;    // ordinal image, row stride Sw
+    const int* span;      // 2r+1 packed spans (non-circle kernels)
     int N, Sw, r;
 };
 
 template <bool CIRCLE>
 __device__ __forceinline__ bool inside(const Ctx& c, int x, int y, int cx, int cy) {
     if (CIRCLE) {
-        int dx = x - cx, dy = y - cy;
+        const int dx = x - cx, dy = y - cy;
         return dx * dx + dy * dy <= c.p->R2;
     } else {
-        int dyi = y - cy + c.r;
+        const int dyi = y - cy + c.r;
         if ((unsigned)dyi > (unsigned)(2 * c.r)) return false;
-        int sp = c.span[dyi];
-        int xlo = (int)(short)(sp & 0xffff);
-        int w = sp >> 16;
-        return (unsigned)(x - cx - xlo) < (unsigned)w;
+        const int sp = c.span[dyi];
+        const int xlo = (int)(short)(sp & 0xffff);
+        return (unsigned)(x - cx - xlo) < (unsigned)(sp >> 16);
     }
 }
 
-// Occupancy mask of ranks [64s, 64s+64) in the window centred at (cx, cy)
-// (ordinal.py:188-199).  Sixteen-byte loads of the swizzled segment.
 template <bool CIRCLE>
-__device__ __forceinline__ uint64_t seg_mask(const Ctx& c, int s, int cx, int cy) {
-    const uint4* seg = reinterpret_cast<const uint4*>(c.om + (s << 6));
-    uint32_t lo = 0, hi = 0;
+__device__ __forceinline__ bool inside_e(const Ctx& c, uint32_t e, int cx, int cy) {
+    return inside<CIRCLE>(c, (int)(e & 0xffu), (int)(e >> 8), cx, cy);
+}
+
+// Membership bits of ranks v..v+7 (bit i = rank v+i); v in [-8, N].
+template <bool CIRCLE>
+__device__ __forceinline__ uint32_t test8(const Ctx& c, int v, int cx, int cy) {
+    uint32_t e[8];
 #pragma unroll
-    for (int ch = 0; ch < 8; ch++) {
-        uint4 v = seg[ch ^ (s & 7)];
-        uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    for (int i = 0; i < 8; i++) e[i] = c.om[v + i];
+    uint32_t m = 0;
 #pragma unroll
-        for (int q = 0; q < 4; q++) {
-            int b = ch * 8 + q * 2;
-            uint32_t e = w[q];
-            bool i0 = inside<CIRCLE>(c, e & 0xff, (e >> 8) & 0xff, cx, cy);
-            bool i1 = inside<CIRCLE>(c, (e >> 16) & 0xff, e >> 24, cx, cy);
-            if (b < 32) {
-                lo |= (i0 ? 1u : 0u) << b;
-                lo |= (i1 ? 1u : 0u) << (b + 1);
-            } else {
-                hi |= (i0 ? 1u : 0u) << (b - 32);
-                hi |= (i1 ? 1u : 0u) << (b - 31);
-            }
-        }
-    }
-    uint64_t m = ((uint64_t)hi << 32) | lo;
-    int rem = c.N - (s << 6);
-    if (rem < 64) m &= (rem <= 0) ? 0ull : ((1ull << rem) - 1ull);
+    for (int i = 0; i < 8; i++) m |= (inside_e<CIRCLE>(c, e[i], cx, cy) ? 1u : 0u) << i;
     return m;
 }
 
-__device__ __forceinline__ int kth_bit(uint64_t m, int need) {
-    uint32_t lo = (uint32_t)m, hi = (uint32_t)(m >> 32);
-    int pl = __popc(lo);
-    if (need < pl) return (int)__fns(lo, 0, need + 1);
-    return 32 + (int)__fns(hi, 0, need - pl + 1);
-}
-
-__device__ __forceinline__ int quant_pivot(const SelParams& p, int m) {
-    int P = ((m + (1 << (p.qs - 1))) >> p.qs) << p.qs;
-    return P < p.P_lo ? p.P_lo : (P > p.P_hi ? p.P_hi : P);
-}
-
-// Per-thread refine (core.py:87-146).  On entry (piv, cnt) is an exact state of
-// window (cx, cy); returns the solution rank m and re-anchors (piv, cnt) at the
-// quantized pivot nearest m.  Returns -1 on an inconsistent count.
+// Per-thread refine from an exact state (P, cnt): returns the t-th smallest
+// rank of the window (core.py:87-146 restated for exact pivots), or -1 if the
+// walk leaves [0, N) (inconsistent state: core.py:31-36 ScanDefectError).
 template <bool CIRCLE>
-__device__ int refine_thread(const Ctx& c, int cx, int cy, int& piv, int& cnt, int tgt) {
-    int s = piv >> 6, cc = cnt, pop;
-    uint64_t mask;
-    if (cc <= tgt) {
-        for (;;) {
-            if ((s << 6) >= c.N) return -1;
-            mask = seg_mask<CIRCLE>(c, s, cx, cy);
-            pop = __popcll(mask);
-            if (cc + pop > tgt) break;
-            cc += pop;
-            s++;
+__device__ int refine_thread(const Ctx& c, int cx, int cy, int P, int cnt, int t) {
+    if (cnt <= t) {
+        int need = t - cnt;  // members to skip at ranks >= P
+        for (int v = P; v < c.N; v += 8) {
+            const uint32_t m = test8<CIRCLE>(c, v, cx, cy);
+            const int pc = __popc(m);
+            if (need < pc) return v + (int)__fns(m, 0, need + 1);
+            need -= pc;
         }
-    } else {
-        for (;;) {
-            s--;
-            if (s < 0) return -1;
-            mask = seg_mask<CIRCLE>(c, s, cx, cy);
-            pop = __popcll(mask);
-            cc -= pop;
-            if (cc <= tgt) break;
-        }
+        return -1;
     }
-    const int m = (s << 6) + kth_bit(mask, tgt - cc);
-    int np = quant_pivot(*c.p, m);
-    int nc;
-    if (np == (s << 6)) {
-        nc = cc;
-    } else if (np == ((s + 1) << 6)) {
-        nc = cc + pop;
-    } else if (np > (s << 6)) {
-        nc = cc + pop;
-        for (int t = s + 1; (t << 6) < np; t++) nc += __popcll(seg_mask<CIRCLE>(c, t, cx, cy));
-    } else {
-        nc = cc;
-        for (int t = s - 1; (t << 6) >= np; t--) nc -= __popcll(seg_mask<CIRCLE>(c, t, cx, cy));
+    int need = cnt - t - 1;  // members to skip below P, counting downward
+    for (int v = P - 8; v > -8; v -= 8) {
+        const uint32_t m = test8<CIRCLE>(c, v, cx, cy);
+        const int pc = __popc(m);
+        if (need < pc) return v + (int)__fns(m, 0, pc - need);
+        need -= pc;
     }
-    piv = np;
-    cnt = nc;
-    return m;
+    return -1;
 }
 
-// Warp-collaborative segment occupancy: lane l tests ranks 64s+2l and 64s+2l+1.
+// Warp-collaborative refine: all lanes hold the same window;
+// lane l tests ranks v0+2l and v0+2l+1 of each 64-rank block.
 template <bool CIRCLE>
-__device__ __forceinline__ void seg_ballot(const Ctx& c, int s, int cx, int cy, int lane,
-                                           unsigned& b0, unsigned& b1, bool& in0, bool& in1) {
-    const uint32_t* om32 = reinterpret_cast<const uint32_t*>(c.om);
-    int ch = lane >> 2;
-    uint32_t e = om32[(s << 5) + (((ch ^ (s & 7)) << 2) | (lane & 3))];
-    int v = (s << 6) + 2 * lane;
-    in0 = v < c.N && inside<CIRCLE>(c, e & 0xff, (e >> 8) & 0xff, cx, cy);
-    in1 = v + 1 < c.N && inside<CIRCLE>(c, (e >> 16) & 0xff, e >> 24, cx, cy);
-    b0 = __ballot_sync(FULLM, in0);
-    b1 = __ballot_sync(FULLM, in1);
-}
-
-// Warp-collaborative refine: all lanes hold the same window.
-template <bool CIRCLE>
-__device__ int refine_warp(const Ctx& c, int cx, int cy, int& piv, int& cnt, int tgt) {
+__device__ int refine_warp(const Ctx& c, int cx, int cy, int P, int cnt, int t) {
     const int lane = threadIdx.x & 31;
-    int s = piv >> 6, cc = cnt, pop;
-    unsigned b0, b1;
-    bool in0, in1;
-    if (cc <= tgt) {
-        for (;;) {
-            if ((s << 6) >= c.N) return -1;
-            seg_ballot<CIRCLE>(c, s, cx, cy, lane, b0, b1, in0, in1);
-            pop = __popc(b0) + __popc(b1);
-            if (cc + pop > tgt) break;
-            cc += pop;
-            s++;
-        }
-    } else {
-        for (;;) {
-            s--;
-            if (s < 0) return -1;
-            seg_ballot<CIRCLE>(c, s, cx, cy, lane, b0, b1, in0, in1);
-            pop = __popc(b0) + __popc(b1);
-            cc -= pop;
-            if (cc <= tgt) break;
-        }
-    }
-    const int need = tgt - cc;
     const unsigned lt = lanemask_lt();
-    const int pre = __popc(b0 & lt) + __popc(b1 & lt);
-    const bool h0 = in0 && pre == need;
-    const bool h1 = in1 && pre + (in0 ? 1 : 0) == need;
-    const unsigned hb = __ballot_sync(FULLM, h0 || h1);
-    const int L = __ffs(hb) - 1;
-    const int off = __shfl_sync(FULLM, h0 ? 0 : 1, L);
-    const int m = (s << 6) + 2 * L + off;
-    int np = quant_pivot(*c.p, m);
-    int nc;
-    if (np == (s << 6)) {
-        nc = cc;
-    } else if (np == ((s + 1) << 6)) {
-        nc = cc + pop;
-    } else if (np > (s << 6)) {
-        nc = cc + pop;
-        for (int t = s + 1; (t << 6) < np; t++) {
-            seg_ballot<CIRCLE>(c, t, cx, cy, lane, b0, b1, in0, in1);
-            nc += __popc(b0) + __popc(b1);
+    const bool up = cnt <= t;
+    int need = up ? t - cnt : cnt - t - 1;
+    for (int v0 = up ? P : P - 64;; v0 += up ? 64 : -64) {
+        if (up ? v0 >= c.N : v0 + 64 <= 0) return -1;
+        const int v = v0 + 2 * lane;
+        const bool i0 = v >= 0 && v < c.N && inside_e<CIRCLE>(c, c.om[v], cx, cy);
+        const bool i1 = v + 1 >= 0 && v + 1 < c.N && inside_e<CIRCLE>(c, c.om[v + 1], cx, cy);
+        const unsigned b0 = __ballot_sync(FULLM, i0), b1 = __ballot_sync(FULLM, i1);
+        const int pc = __popc(b0) + __popc(b1);
+        if (need < pc) {
+            const int k = up ? need : pc - 1 - need;  // index from the bottom of the block
+            const int pre = __popc(b0 & lt) + __popc(b1 & lt);
+            const bool h0 = i0 && pre == k;
+            const bool h1 = i1 && pre + (i0 ? 1 : 0) == k;
+            const unsigned hb = __ballot_sync(FULLM, h0 || h1);
+            const int L = __ffs(hb) - 1;
+            const int off = __shfl_sync(FULLM, h0 ? 0 : 1, L);
+            return v0 + 2 * L + off;
         }
-    } else {
-        nc = cc;
-        for (int t = s - 1; (t << 6) >= np; t--) {
-            seg_ballot<CIRCLE>(c, t, cx, cy, lane, b0, b1, in0, in1);
-            nc -= __popc(b0) + __popc(b1);
-        }
+        need -= pc;
     }
-    piv = np;
-    cnt = nc;
-    return m;
 }
 
 __device__ __forceinline__ int target_at(const Geom& g, const SelParams& p, const TileCoord& tc,
                                          int row, int col) {
     if (!p.tmap) return p.target;
-    int y = min(tc.oy0 + row, g.out_h - 1), x = min(tc.ox0 + col, g.out_w - 1);
+    const int y = min(tc.oy0 + row, g.out_h - 1), x = min(tc.ox0 + col, g.out_w - 1);
     return __ldg(p.tmap + (long long)y * g.out_w + x);
 }
 
@@ -226,7 +143,7 @@ __device__ __forceinline__ void write_out(const Ctx& c, const TileCoord& tc, int
     const Geom& g = *c.g;
     const int oy = tc.oy0 + row, ox = tc.ox0 + col;
     if (oy >= g.out_h || ox >= g.out_w) return;
-    const uint32_t e = c.om[omega_index(m)];
+    const uint32_t e = c.om[m];
     const long long so = src_offset(g, tc, (int)(e >> 8), (int)(e & 0xff));
     const long long d = tc.b * g.d_b + (long long)oy * g.d_y + (long long)ox * g.d_x + tc.c * g.d_c;
     if (g.dtype == DT_U8) {
@@ -238,191 +155,231 @@ __device__ __forceinline__ void write_out(const Ctx& c, const TileCoord& tc, int
     }
 }
 
-template <bool CIRCLE>
+// Count change of a slide, from two offset tables: + [I[b+e] < P] - [I[b+x] < P].
+__device__ __forceinline__ int slide_delta(const uint16_t* __restrict__ Ib,
+                                           const int2* __restrict__ tab, int n, int P, bool swap) {
+    int d = 0;
+    if (!swap) {
+#pragma unroll 4
+        for (int k = 0; k < n; k++) {
+            const int2 o = tab[k];
+            d += ((int)Ib[o.x] < P) - ((int)Ib[o.y] < P);
+        }
+    } else {
+#pragma unroll 4
+        for (int k = 0; k < n; k++) {
+            const int2 o = tab[k];
+            d += ((int)Ib[o.y] < P) - ((int)Ib[o.x] < P);
+        }
+    }
+    return d;
+}
+
+// OMG: omega stays in its global (L2-resident) slot instead of shared memory,
+// for tiles whose omega + ordinal image exceed shared memory (r >~ 110).
+template <bool CIRCLE, bool OMG>
 __global__ void __launch_bounds__(512) k2_select(Geom g, SelParams p,
                                                  const uint16_t* __restrict__ omega_in) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nwarps = blockDim.x >> 5;
     const int N = g.N, Npad = g.Npad, Sw = g.Sw, r = g.r;
-    const int Tw = g.Tw, Th = g.Th, G = p.G, K = p.K;
+    const int Tw = g.Tw, Th = g.Th, G = p.G;
     const TileCoord tc = tile_coord(g, g.tile_begin + blockIdx.x);
 
-    uint16_t* om = reinterpret_cast<uint16_t*>(smem);
-    uint8_t* Iq = reinterpret_cast<uint8_t*>(om + Npad);
-    int* ktab = reinterpret_cast<int*>(Iq + ((N + 15) & ~15));
+    const uint16_t* om_g = omega_in + (long long)blockIdx.x * (Npad + 2 * OMEGA_SLOT_PAD) + OMEGA_SLOT_PAD;
+    uint16_t* om_s = reinterpret_cast<uint16_t*>(smem) + OMEGA_PAD;
+    const uint16_t* om = OMG ? om_g : om_s;
+    uint16_t* I = OMG ? reinterpret_cast<uint16_t*>(smem) : om_s + Npad + OMEGA_PAD;
+    int* ktab = reinterpret_cast<int*>(I + ((N + 7) & ~7));
     const int ktab_n = 2 * p.ncols + 2 * p.nrows + 2 * r + 1;
-    uint16_t* shist = reinterpret_cast<uint16_t*>(ktab + ((ktab_n + 3) & ~3));
-    const int nhist = min(nwarps, G * K);
-    int* st_m = reinterpret_cast<int*>(shist + nhist * 1024);
-    int* st_p = st_m + G * Tw;
-    int* st_c = st_p + G * Tw;
-    int* deltas = st_c + G * Tw;
+    int* st_P = ktab + ((ktab_n + 3) & ~3);
+    int* st_C = st_P + G * Tw;
+    int* deltas = st_C + G * Tw;                   // max(G*Tw, Th) entries
+    int* hist = deltas + max(G * Tw, Th);          // 32 bins
+    int* seedP = hist + 32;                        // G
+    int* seedC = seedP + G;                        // G
 
     const int2* vtab = reinterpret_cast<const int2*>(ktab);
     const int2* htab = reinterpret_cast<const int2*>(ktab + 2 * p.ncols);
-    Ctx c{&g, &p, om, Iq, ktab + 2 * p.ncols + 2 * p.nrows, N, Sw, r};
+    const Ctx c{&g, &p, om, I, ktab + 2 * p.ncols + 2 * p.nrows, N, Sw, r};
 
-    // ---- 0. stage omega (swizzled) and build Iq -------------------------
+    // ---- 0. stage omega and build the ordinal image -----------------------
     {
-        const uint4* src = reinterpret_cast<const uint4*>(omega_in + (long long)blockIdx.x * Npad);
-        uint4* dst = reinterpret_cast<uint4*>(om);
+        const uint4* src = reinterpret_cast<const uint4*>(om_g);
+        uint4* dst = reinterpret_cast<uint4*>(om_s);
         for (int i = tid; i < (Npad >> 3); i += blockDim.x) {
-            uint4 v = src[i];
-            const int s = i >> 3;
-            dst[(s << 3) | ((i & 7) ^ (s & 7))] = v;
-            uint32_t w[4] = {v.x, v.y, v.z, v.w};
+            const uint4 v = src[i];
+            if (!OMG) dst[i] = v;
+            const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
             for (int q = 0; q < 8; q++) {
                 const int rank = (i << 3) + q;
                 if (rank < N) {
-                    const uint32_t e = (q & 1) ? (w[q >> 1] >> 16) : (w[q >> 1] & 0xffff);
-                    int qv = (rank >> p.qs) - p.qb;
-                    qv = qv < 0 ? 0 : (qv > 255 ? 255 : qv);
-                    Iq[(int)(e >> 8) * Sw + (int)(e & 0xff)] = (uint8_t)qv;
+                    const uint32_t e = (q & 1) ? (w[q >> 1] >> 16) : (w[q >> 1] & 0xffffu);
+                    I[(int)(e >> 8) * Sw + (int)(e & 0xffu)] = (uint16_t)rank;
                 }
             }
         }
+        if (!OMG && tid < OMEGA_PAD) {
+            om_s[-OMEGA_PAD + tid] = OMEGA_SENTINEL;
+            om_s[Npad + tid] = OMEGA_SENTINEL;
+        }
         for (int i = tid; i < ktab_n; i += blockDim.x) ktab[i] = __ldg(p.ktab + i);
+        if (tid < 32) hist[tid] = 0;
     }
     __syncthreads();
 
-    const int R = Th / G;  // rows per group; seed row at local R/2
-    auto blk_lo = [&](int k) { return (k * Tw) / K; };
-    auto seed_col = [&](int k) { return (blk_lo(k) + blk_lo(k + 1)) >> 1; };
+    const int R = Th / G;                 // rows per group; seed row at local R/2
+    const int g0 = G >> 1;                // group of the direct seed
+    const int cs = Tw >> 1;               // seed column
+    auto seed_row = [&](int gi) { return gi * R + (R >> 1); };
 
-    // ---- 1. direct seeds (one warp each) ----------------------------------
-    for (int sd = wid; sd < G * K; sd += nwarps) {
-        const int gi = sd / K, ki = sd % K;
-        const int row = gi * R + (R >> 1), col = seed_col(ki);
-        const int cx = col + r, cy = row + r;
-        const int tgt = target_at(g, p, tc, row, col);
-        uint16_t* h = shist + (wid % nhist) * 1024;
-        for (int i = lane; i < 1024; i += 32) h[i] = 0;
-        __syncwarp();
-        const uint8_t* Ic = Iq + cy * Sw + cx;
-        for (int k = 0; k < p.nrows; k++) {
+    // ---- A. direct seed: 32-bin rank histogram split over all warps -------
+    const int sh = max(0, 32 - __clz(max(N - 1, 1)) - 5);  // 32 bins of 2^sh ranks cover [0, N)
+    {
+        const int cx = cs + r, cy = seed_row(g0) + r;
+        const uint16_t* Ic = I + cy * Sw + cx;
+        unsigned lm[5];
+#pragma unroll
+        for (int b = 0; b < 5; b++) lm[b] = ((lane >> b) & 1) ? 0u : FULLM;
+        int cntb = 0;
+        for (int k = wid; k < p.nrows; k += nwarps) {
             const int2 hp = htab[k];  // (dy*Sw + xhi, dy*Sw + xlo)
-            for (int o = hp.y + lane; o < hp.x; o += 32) h[((Ic[o] >> 3) << 5) + lane]++;
+            for (int o0 = hp.y; o0 < hp.x; o0 += 32) {
+                const int o = o0 + lane;
+                const bool ok = o < hp.x;
+                const unsigned b = ok ? (unsigned)(Ic[o] >> sh) : 0u;
+                unsigned m = __ballot_sync(FULLM, ok);
+#pragma unroll
+                for (int bit = 0; bit < 5; bit++) m &= ~(__ballot_sync(FULLM, (b >> bit) & 1u) ^ ~lm[bit]);
+                cntb += __popc(m);
+            }
         }
-        __syncwarp();
-        int tot = 0;
-        for (int b = 0; b < 32; b++) {
-            int v = __reduce_add_sync(FULLM, (unsigned)h[(b << 5) + lane]);
-            if (lane == b) tot = v;
-        }
+        if (cntb) atomicAdd(&hist[lane], cntb);
+    }
+    __syncthreads();
+    if (wid == 0) {
+        const int row = seed_row(g0);
+        const int tgt = target_at(g, p, tc, row, cs);
+        const int tot = hist[lane];
         int cum = tot;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            int v = __shfl_up_sync(FULLM, cum, o);
+            const int v = __shfl_up_sync(FULLM, cum, o);
             if (lane >= o) cum += v;
         }
         const int B = __ffs(__ballot_sync(FULLM, cum > tgt)) - 1;
-        int pq, cnt;
-        if (B == 0) {
-            pq = 8;
-            cnt = __shfl_sync(FULLM, cum, 0);
-        } else {
-            pq = 8 * B;
-            cnt = __shfl_sync(FULLM, cum - tot, B);
-        }
-        int piv = (pq + p.qb) << p.qs;
-        const int m = refine_warp<CIRCLE>(c, cx, cy, piv, cnt, tgt);
-        if (m < 0 && lane == 0) atomicOr(p.status, 1);
+        const int cnt = __shfl_sync(FULLM, cum - tot, B);
+        const int m = refine_warp<CIRCLE>(c, cs + r, row + r, B << sh, cnt, tgt);
         if (lane == 0) {
-            st_m[gi * Tw + col] = m < 0 ? 0 : m;
-            st_p[gi * Tw + col] = piv;
-            st_c[gi * Tw + col] = cnt;
+            if (m < 0) atomicOr(p.status, 1);
+            seedP[g0] = max(m, 0);
+            seedC[g0] = tgt;
         }
     }
     __syncthreads();
 
-    // ---- 2. seed rows: horizontal slide deltas at the seed pivot ----------
-    for (int u = tid; u < G * Tw; u += blockDim.x) {
-        const int gi = u / Tw, j = u % Tw;
-        int ki = 0;
-        while (ki + 1 < K && j >= blk_lo(ki + 1)) ki++;
-        const int sc = seed_col(ki);
-        if (j + 1 < blk_lo(ki + 1) && j + 1 < Tw) {
-            const int row = gi * R + (R >> 1);
-            const int pq = (st_p[gi * Tw + sc] >> p.qs) - p.qb;
-            const uint8_t* Ic = Iq + (row + r) * Sw + (j + r);
-            int d = 0;
-            for (int k = 0; k < p.nrows; k++) {
-                const int2 hp = htab[k];
-                d += (Ic[hp.x] < pq) - (Ic[hp.y] < pq);
+    // ---- B. other seed rows: vertical deltas at the direct seed's pivot ----
+    const int ytop = seed_row(0), ybot = seed_row(G - 1);
+    if (G > 1) {
+        const int P0 = seedP[g0];
+        for (int y = ytop + tid; y < ybot; y += blockDim.x) {  // step y -> y+1, column cs
+            const uint16_t* Ib = I + (y + r) * Sw + cs + r;
+            deltas[y] = slide_delta(Ib, vtab, p.ncols, P0, false);
+        }
+        __syncthreads();
+        for (int gi = wid; gi < G; gi += nwarps) {
+            if (gi == g0) continue;
+            const int y0 = seed_row(g0), y1 = seed_row(gi);
+            int part = 0;
+            if (y1 > y0) {
+                for (int y = y0 + lane; y < y1; y += 32) part += deltas[y];
+            } else {
+                for (int y = y1 + lane; y < y0; y += 32) part -= deltas[y];
             }
-            deltas[u] = d;
+            const int cnt = seedC[g0] + (int)__reduce_add_sync(FULLM, (unsigned)part);
+            const int tgt = target_at(g, p, tc, y1, cs);
+            const int m = refine_warp<CIRCLE>(c, cs + r, y1 + r, P0, cnt, tgt);
+            if (lane == 0) {
+                if (m < 0) atomicOr(p.status, 1);
+                seedP[gi] = max(m, 0);
+                seedC[gi] = tgt;
+            }
+        }
+        __syncthreads();
+    }
+
+    // ---- C. seed rows: horizontal deltas at the row pivot, then refine ----
+    for (int u = tid; u < G * Tw; u += blockDim.x) {
+        const int gi = u / Tw, j = u % Tw;
+        if (j + 1 < Tw) {  // step j -> j+1
+            const uint16_t* Ib = I + (seed_row(gi) + r) * Sw + j + r;
+            deltas[u] = slide_delta(Ib, htab, p.nrows, seedP[gi], false);
         }
     }
     __syncthreads();
     for (int u = tid; u < G * Tw; u += blockDim.x) {
-        const int gi = u / Tw, j = u % Tw;
-        int ki = 0;
-        while (ki + 1 < K && j >= blk_lo(ki + 1)) ki++;
-        const int sc = seed_col(ki);
-        if (j == sc) continue;
-        int piv = st_p[gi * Tw + sc], cnt = st_c[gi * Tw + sc];
-        if (j > sc) {
-            for (int i = sc; i < j; i++) cnt += deltas[gi * Tw + i];
+        const int gi = u / Tw, j = u % Tw, row = seed_row(gi);
+        const int P = seedP[gi];
+        int cnt = seedC[gi];
+        if (j > cs) {
+            for (int i = cs; i < j; i++) cnt += deltas[gi * Tw + i];
         } else {
-            for (int i = j; i < sc; i++) cnt -= deltas[gi * Tw + i];
+            for (int i = j; i < cs; i++) cnt -= deltas[gi * Tw + i];
         }
-        const int row = gi * R + (R >> 1);
-        const int m = refine_thread<CIRCLE>(c, j + r, row + r, piv, cnt, target_at(g, p, tc, row, j));
-        if (m < 0) atomicOr(p.status, 1);
-        st_m[u] = m < 0 ? 0 : m;
-        st_p[u] = piv;
-        st_c[u] = cnt;
+        const int tgt = target_at(g, p, tc, row, j);
+        int m = (j == cs) ? P : refine_thread<CIRCLE>(c, j + r, row + r, P, cnt, tgt);
+        if (m < 0) {
+            atomicOr(p.status, 1);
+            m = 0;
+        }
+        st_P[u] = m;
+        st_C[u] = tgt;
     }
     __syncthreads();
 
-    // ---- 3. vertical sweeps --------------------------------------------------
+    // ---- D. vertical sweeps --------------------------------------------------
     for (int u = tid; u < G * Tw * 2; u += blockDim.x) {
-        const int j = u % Tw, rest = u / Tw, gi = rest >> 1, down = (rest & 1) == 0;
-        const int row0 = gi * R + (R >> 1);
+        const int j = u % Tw, rest = u / Tw, gi = rest >> 1;
+        const bool down = (rest & 1) == 0;
+        const int row0 = seed_row(gi);
         const int rend = (gi == G - 1) ? Th : (gi + 1) * R;  // exclusive
-        int m = st_m[gi * Tw + j], piv = st_p[gi * Tw + j], cnt = st_c[gi * Tw + j];
+        int P = st_P[gi * Tw + j], cnt = st_C[gi * Tw + j];
+        if (down) write_out(c, tc, P, row0, j);
         const int cx = j + r;
-        if (down) write_out(c, tc, m, row0, j);
-        int row = row0;
         const int nsteps = down ? (rend - 1 - row0) : (row0 - gi * R);
+        int row = row0;
         for (int step = 0; step < nsteps; step++) {
-            const int pq = (piv >> p.qs) - p.qb;
-            int d = 0;
             if (down) {
-                const uint8_t* Ib = Iq + (row + r) * Sw + cx;
-                for (int k = 0; k < p.ncols; k++) {
-                    const int2 o = vtab[k];
-                    d += (Ib[o.x] < pq) - (Ib[o.y] < pq);
-                }
+                cnt += slide_delta(I + (row + r) * Sw + cx, vtab, p.ncols, P, false);
                 row++;
             } else {
-                const uint8_t* Ib = Iq + (row + r - 1) * Sw + cx;
-                for (int k = 0; k < p.ncols; k++) {
-                    const int2 o = vtab[k];
-                    d += (Ib[o.y] < pq) - (Ib[o.x] < pq);
-                }
+                cnt += slide_delta(I + (row + r - 1) * Sw + cx, vtab, p.ncols, P, true);
                 row--;
             }
-            cnt += d;
-            m = refine_thread<CIRCLE>(c, cx, row + r, piv, cnt, target_at(g, p, tc, row, j));
+            const int tgt = target_at(g, p, tc, row, j);
+            const int m = refine_thread<CIRCLE>(c, cx, row + r, P, cnt, tgt);
             if (m < 0) {
                 atomicOr(p.status, 1);
                 break;
             }
             write_out(c, tc, m, row, j);
+            P = m;
+            cnt = tgt;
         }
     }
 }
 
-template __global__ void k2_select<true>(Geom, SelParams, const uint16_t*);
-template __global__ void k2_select<false>(Geom, SelParams, const uint16_t*);
+template __global__ void k2_select<true, false>(Geom, SelParams, const uint16_t*);
+template __global__ void k2_select<false, false>(Geom, SelParams, const uint16_t*);
+template __global__ void k2_select<true, true>(Geom, SelParams, const uint16_t*);
+template __global__ void k2_select<false, true>(Geom, SelParams, const uint16_t*);
 
-size_t k2_smem_bytes(int N, int Npad, int ncols, int nrows, int r, int G, int K, int Tw, int nwarps) {
+size_t k2_smem_bytes(int N, int Npad, int ncols, int nrows, int r, int G, int Tw, int Th, bool omg) {
     const int ktab_n = 2 * ncols + 2 * nrows + 2 * r + 1;
-    const int nhist = nwarps < G * K ? nwarps : G * K;
-    return 2 * (size_t)Npad + (size_t)((N + 15) & ~15) + 4 * (size_t)((ktab_n + 3) & ~3) +
-           2048 * (size_t)nhist + 4 * (size_t)(4 * G * Tw);
+    const int gt = G * Tw;
+    return (omg ? 0 : 2 * (size_t)(Npad + 2 * OMEGA_PAD)) + 2 * (size_t)((N + 7) & ~7) +
+           4 * (size_t)((ktab_n + 3) & ~3) + 4 * (size_t)(2 * gt + (gt > Th ? gt : Th) + 32 + 2 * G);
 }
 
 }  // namespace imf

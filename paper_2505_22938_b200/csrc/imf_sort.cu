@@ -128,11 +128,21 @@ __device__ __forceinline__ uint16_t pack_pos(int i, int Sw, float invS) {
 }
 
 // Copy the finished omega (smem, N entries) to its global slot, 16 B at a time.
+// Global omega slot of a tile: OMEGA_SLOT_PAD sentinel entries on both sides
+// of Npad ranks, so scans may step a few ranks past either end.
+__device__ __forceinline__ uint16_t* omega_slot(const Geom& g, uint16_t* base) {
+    return base + (long long)blockIdx.x * (g.Npad + 2 * OMEGA_SLOT_PAD) + OMEGA_SLOT_PAD;
+}
+
 __device__ __forceinline__ void store_omega(const Geom& g, const uint16_t* om_s, uint16_t* om_g) {
     const int n16 = g.Npad >> 3;  // uint4 count
     const uint4* s = reinterpret_cast<const uint4*>(om_s);
     uint4* d = reinterpret_cast<uint4*>(om_g);
     for (int i = threadIdx.x; i < n16; i += blockDim.x) d[i] = s[i];
+    if (threadIdx.x < OMEGA_SLOT_PAD) {
+        om_g[-OMEGA_SLOT_PAD + (int)threadIdx.x] = 0xffffu;
+        om_g[g.Npad + threadIdx.x] = 0xffffu;
+    }
 }
 
 template <int DT, bool GMEM>
@@ -150,7 +160,7 @@ __global__ void __launch_bounds__(512) k1_sort(Geom g, uint16_t* __restrict__ om
     uint16_t* om = reinterpret_cast<uint16_t*>(cnt + (DT == DT_U8 ? 0 : 256 * nw));
     unsigned char* big = GMEM ? gscratch + blockIdx.x * gscratch_stride
                               : reinterpret_cast<unsigned char*>(om + g.Npad);
-    uint16_t* om_g = omega_out + (long long)blockIdx.x * g.Npad;
+    uint16_t* om_g = omega_slot(g, omega_out);
 
     if (DT == DT_U8) {
         auto digit = [&](int i) {
@@ -200,9 +210,125 @@ __global__ void __launch_bounds__(512) k1_sort(Geom g, uint16_t* __restrict__ om
         auto e3 = [&](int k, int dst) { om[dst] = pack_pos(posA[k], Sw, invS); };
         stable_pass(N, cnt, d3, e3);
     }
-    for (int i = N + threadIdx.x; i < g.Npad; i += blockDim.x) om[i] = 0;
+    for (int i = N + threadIdx.x; i < g.Npad; i += blockDim.x) om[i] = 0xffffu;
     __syncthreads();
     store_omega(g, om, om_g);
+}
+
+// Direct counting sort for 8/16-bit tiles (ordinal.py:62-79 _rank_by_bucket,
+// the paper's 16-bit bucket sort): one 2^bits-bin histogram
+// of u16 counters packed two per 32-bit word in shared memory (65536 bins =
+// 128 KB for u16), shared atomics for the histogram and for the scatter
+// (ties unordered -- output-neutral, see above).  Input tile rows are read
+// straight from global memory twice (L2-resident), with the clamped column
+// offsets of every lane precomputed once.  Requires N <= 65535 (S <= 255).
+template <int DT>
+__global__ void __launch_bounds__(512) k1_count(Geom g, uint16_t* __restrict__ omega_out) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    constexpr int NB = DT == DT_U8 ? 256 : 65536;
+    constexpr int NW = NB / 2;  // histogram words
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+    const TileCoord tc = tile_coord(g, g.tile_begin + blockIdx.x);
+    const int S = g.Sw, Sh = g.Sh;
+    uint32_t* hw = reinterpret_cast<uint32_t*>(smem);
+    uint16_t* om = reinterpret_cast<uint16_t*>(hw + NW);
+    {
+        uint4* h4 = reinterpret_cast<uint4*>(hw);
+        for (int i = tid; i < NW / 4; i += blockDim.x) h4[i] = make_uint4(0, 0, 0, 0);
+    }
+    // clamped column offsets of this lane's columns x = lane + 32k
+    long long xo[8];
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+        int x = tc.ox0 + lane + 32 * k - g.r + g.vshift;
+        x = x < 0 ? 0 : (x >= g.W ? g.W - 1 : x);
+        xo[k] = (long long)x * g.s_x;
+    }
+    const int nk = (S + 31) >> 5;
+    __syncthreads();
+    auto row_ptr = [&](int y) {
+        int yy = tc.oy0 + y - g.r + g.vshift;
+        yy = yy < 0 ? 0 : (yy >= g.H ? g.H - 1 : yy);
+        return tc.src + (long long)yy * g.s_y * (DT == DT_U8 ? 1 : 2);
+    };
+    for (int y = wid; y < Sh; y += nw) {
+        const char* rp = row_ptr(y);
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+            if (k < nk && lane + 32 * k < S) {
+                uint32_t v = DT == DT_U8 ? (uint32_t)__ldg((const uint8_t*)rp + xo[k])
+                                         : (uint32_t)__ldg((const uint16_t*)rp + xo[k]);
+                atomicAdd(&hw[v >> 1], 1u << ((v & 1) << 4));
+            }
+        }
+    }
+    __syncthreads();
+    {   // exclusive scan over NB 16-bit counters (two per word).  Warp w owns the
+        // contiguous word range [w*per, (w+1)*per); lanes stride by one word so
+        // every shared access is bank-conflict free.
+        __shared__ uint32_t wt[32];
+        const int per = NW / nw;  // NW and nw are powers of two (<= 16 warps)
+        const uint32_t* wbase = hw + wid * per;
+        uint32_t sum = 0;
+        for (int i = lane; i < per; i += 32) {
+            const uint32_t w = wbase[i];
+            sum += (w & 0xffffu) + (w >> 16);
+        }
+        sum = __reduce_add_sync(0xffffffffu, sum);
+        if (lane == 0) wt[wid] = sum;
+        __syncthreads();
+        if (wid == 0) {
+            uint32_t v = lane < nw ? wt[lane] : 0, x = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                uint32_t t = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += t;
+            }
+            if (lane < nw) wt[lane] = x - v;
+        }
+        __syncthreads();
+        uint32_t carry = wt[wid];
+        uint32_t* wb = hw + wid * per;
+        for (int i0 = 0; i0 < per; i0 += 32) {
+            const bool ok = i0 + lane < per;
+            const uint32_t w = ok ? wb[i0 + lane] : 0u;
+            const uint32_t lo = w & 0xffffu, tot = lo + (w >> 16);
+            uint32_t incl = tot;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += t;
+            }
+            const uint32_t ex = carry + incl - tot;
+            if (ok) wb[i0 + lane] = ex | ((ex + lo) << 16);
+            carry += __shfl_sync(0xffffffffu, incl, 31);
+        }
+    }
+    __syncthreads();
+    for (int y = wid; y < Sh; y += nw) {
+        const char* rp = row_ptr(y);
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+            const int x = lane + 32 * k;
+            if (k < nk && x < S) {
+                uint32_t v = DT == DT_U8 ? (uint32_t)__ldg((const uint8_t*)rp + xo[k])
+                                         : (uint32_t)__ldg((const uint16_t*)rp + xo[k]);
+                const uint32_t sh = (v & 1) << 4;
+                const uint32_t old = atomicAdd(&hw[v >> 1], 1u << sh);
+                om[(old >> sh) & 0xffffu] = (uint16_t)(x | (y << 8));
+            }
+        }
+    }
+    for (int i = g.N + tid; i < g.Npad; i += blockDim.x) om[i] = 0xffffu;
+    __syncthreads();
+    store_omega(g, om, omega_slot(g, omega_out));
+}
+
+template __global__ void k1_count<DT_U8>(Geom, uint16_t*);
+template __global__ void k1_count<DT_U16>(Geom, uint16_t*);
+
+size_t k1_count_smem_bytes(int dtype, int Npad) {
+    return (dtype == DT_U8 ? 128 * 4 : 32768 * 4) + 2 * (size_t)Npad;
 }
 
 template __global__ void k1_sort<DT_U8, false>(Geom, uint16_t*, unsigned char*, long long);

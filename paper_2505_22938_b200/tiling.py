@@ -194,6 +194,11 @@ class _Workspace:
 _WS = _Workspace()
 
 
+def workspace_for(device):
+    """The cached device workspace (holds the status word of the last call)."""
+    return _WS.get(device, 1)
+
+
 def _kernel_struct(kernel):
     keep = [np.ascontiguousarray(a, dtype=np.int32) for a in
             (kernel.row_dy, kernel.row_xlo, kernel.row_xhi, kernel.col_dx,
@@ -221,7 +226,7 @@ def _image_struct(t, dt_code, batched: bool, has_c: bool):
 
 
 def run_device(src, params: FilterParams, out=None, *, batched: bool = False, stream=None,
-               check: bool = True, kernel=None):
+               check: bool = True, kernel=None, profile: bool = False):
     """Filter a CUDA tensor ([B,] H, W[, C]) into a new (or given) CUDA tensor.
 
     Host prologue (validation, kernel, targets) is the caller's job except for
@@ -248,6 +253,8 @@ def run_device(src, params: FilterParams, out=None, *, batched: bool = False, st
     simg = _image_struct(src, dt_code, batched, has_c)
     dimg = _image_struct(out, dt_code, batched, has_c)
     opt = _lib.ImfOptions(1 if valid else 0, int(params.tile_size or 0), 0, 0)
+    if profile:
+        opt.reserved[0] = 1  # per-kernel CUDA-event timing (synchronizes)
     need = L.imf_workspace_size(ctypes.byref(simg), ctypes.byref(ks), ctypes.byref(opt))
     if need == 0:
         raise ValueError("unsupported filter geometry for the CUDA engine")

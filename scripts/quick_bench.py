@@ -1,34 +1,50 @@
-"""Quick device-resident timing of one config (development aid)."""
-import sys, os, time, json
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests", "golden"))
+"""Quick device-resident timing of BASELINE configs (development aid).
+
+    python scripts/quick_bench.py [c1 c2 c3 c4 c5]   (env IMF_TILE / IMF_SEED_ROWS / IMF_SEEDS tune)
+"""
+import ctypes, json, os, sys
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT); sys.path.insert(0, os.path.join(ROOT, "tests", "golden"))
 import numpy as np, torch
 import cases as C
-from paper_2505_22938_b200 import FilterParams, ShapeSpec, filter_batch
+from paper_2505_22938_b200 import FilterParams, ShapeSpec, _lib, make_kernel
+from paper_2505_22938_b200.tiling import run_device
 
-def run(name, img, spec, reps=5):
+def run(name, img, spec, reps=5, gold=None):
     t = torch.from_numpy(img).cuda().unsqueeze(0)
     params = FilterParams(shape=ShapeSpec(*spec))
-    out = filter_batch(t, params)
-    torch.cuda.synchronize()
+    k = make_kernel(params.shape)
+    out = run_device(t, params, batched=True)
+    ok = None if gold is None else C.digest(out[0].cpu().numpy()) == gold
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-    ts = []
+    L = _lib.lib(); ts = []; k1 = []; k2 = []
     for _ in range(reps):
         flush.zero_()
         e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(); filter_batch(t, params, out=out, check=False); e1.record(); torch.cuda.synchronize()
-        ts.append(e0.elapsed_time(e1))
+        e0.record(); run_device(t, params, out=out, batched=True, check=False, kernel=k, profile=True); e1.record()
+        torch.cuda.synchronize(); ts.append(e0.elapsed_time(e1))
+        a, b = ctypes.c_float(), ctypes.c_float(); tl = ctypes.c_int32(); qs = ctypes.c_int32()
+        L.imf_profile_last(ctypes.byref(a), ctypes.byref(b), None, None, ctypes.byref(tl), ctypes.byref(qs))
+        k1.append(a.value); k2.append(b.value)
     ms = float(np.median(ts))
     h, w = img.shape[:2]; c = img.shape[2] if img.ndim == 3 else 1
-    print(json.dumps({"cfg": name, "ms": round(ms, 3), "MP/s": round(h*w/1e3/ms, 1), "chMP/s": round(h*w*c/1e3/ms, 1)}), flush=True)
-    return out
+    W = 4 * len(k.col_dx) + 384
+    print(json.dumps({"cfg": name, "ms": round(ms, 3), "k1_ms": round(float(np.median(k1)), 3),
+                      "k2_ms": round(float(np.median(k2)), 3), "MP/s": round(h*w/1e3/ms, 1),
+                      "chMP/s": round(h*w*c/1e3/ms, 1), "tile": tl.value, "qs": qs.value,
+                      "frac_nominal18.6": round(h*w*c/1e3/ms*1e6*W/18.6e12, 3), "parity": ok,
+                      "env": {k_: os.environ.get(k_) for k_ in ("IMF_TILE", "IMF_SEED_ROWS", "IMF_SEEDS") if os.environ.get(k_)}}), flush=True)
 
 which = sys.argv[1:] or ["c1", "c2", "c3", "c4"]
-if "c1" in which: run("c1", C.baseline_input("c1"), ("circle", 8, 0, 0.0))
-if "c2" in which: run("c2", C.baseline_input("c2"), ("circle", 48, 0, 0.0))
+gold = json.load(open(os.path.join(ROOT, "tests", "golden", "golden.json")))["baseline"]
+if "c1" in which: run("c1", C.baseline_input("c1"), ("circle", 8, 0, 0.0), gold=gold["c1"])
+if "c2" in which: run("c2", C.baseline_input("c2"), ("circle", 48, 0, 0.0), gold=gold["c2"])
 if "c3" in which:
     img = C.baseline_input("c3")
-    for r in (2, 8, 32, 48, 64, 100): run(f"c3 r{r}", img, ("circle", r, 0, 0.0), reps=3)
+    for r in (2, 8, 16, 32, 48, 64, 100): run(f"c3 r{r}", img, ("circle", r, 0, 0.0), reps=3, gold=gold[f"c3/r{r}"])
 if "c4" in which:
     img = C.baseline_input("c4")
-    for s in C.C4_SHAPES: run(f"c4 {s}", img, s, reps=3)
+    for s in C.C4_SHAPES: run(f"c4 {s[0]}{s[2]}", img, s, reps=3, gold=gold["c4/" + json.dumps(list(s))])
+if "c5" in which:
+    g5 = json.load(open(os.path.join(ROOT, "tests", "golden", "golden_c5.json")))
+    run("c5 img0", C.baseline_input("c5", 0), ("circle", 64, 0, 0.0), reps=3, gold=g5.get("0"))
