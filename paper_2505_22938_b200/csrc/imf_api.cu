@@ -33,7 +33,8 @@ static int cuda_fail(cudaError_t e, const char* where) {
 namespace {
 
 constexpr size_t kSmemMax = 227 * 1024 - 1024;  // B200 opt-in 232448 B minus static smem headroom
-constexpr int kK1Threads = 512;
+constexpr int kK1Threads = 1024;      // k1_count (latency-bound: more warps)
+constexpr int kK1SortThreads = 512;   // k1_sort (per-warp digit counters)
 constexpr size_t kStatusBytes = 256;
 constexpr size_t kOmegaScratchTarget = 96ull << 20;  // stays mostly L2-resident
 
@@ -119,8 +120,8 @@ int make_plan(const imf_image* src, const imf_kernel* k, const imf_options* opt,
     g.tiles_y = (out_h + g.Th - 1) / g.Th;
     p.total_tiles = (long long)g.tiles_x * g.tiles_y * g.C * g.B;
 
-    p.k1_threads = kK1Threads;
     p.k1_count = g.dtype != DT_F32 && k1_count_smem_bytes(g.dtype, g.Npad) <= kSmemMax;
+    p.k1_threads = p.k1_count ? kK1Threads : kK1SortThreads;
     p.k1_gmem = !p.k1_count && k1_smem_bytes(g.dtype, g.Npad, p.k1_threads / 32, false) > kSmemMax;
     p.k1_smem = p.k1_count ? k1_count_smem_bytes(g.dtype, g.Npad)
                            : k1_smem_bytes(g.dtype, g.Npad, p.k1_threads / 32, p.k1_gmem);
@@ -139,6 +140,19 @@ int make_plan(const imf_image* src, const imf_kernel* k, const imf_options* opt,
     p.ws_k1g = (size_t)chunk * p.k1_gs_per_tile;
     p.ws_total = kStatusBytes + p.ws_ktab + p.ws_omega + p.ws_k1g;
     return IMF_OK;
+}
+
+void build_ktab_struct(const imf_kernel* k, int Sw, KTab& t) {
+    memset(&t, 0, sizeof(t));
+    const int r = k->radius;
+    // byte offsets into the 16-bit ordinal image
+    for (int i = 0; i < k->ncols; i++)
+        t.v[i] = make_int2(2 * ((k->col_ybot[i] + 1) * Sw + k->col_dx[i]),
+                           2 * (k->col_ytop[i] * Sw + k->col_dx[i]));
+    for (int i = 0; i < k->nrows; i++) {
+        t.h[i] = make_int2(2 * (k->row_dy[i] * Sw + k->row_xhi[i]), 2 * (k->row_dy[i] * Sw + k->row_xlo[i]));
+        t.span[k->row_dy[i] + r] = (k->row_xlo[i] & 0xffff) | ((k->row_xhi[i] - k->row_xlo[i]) << 16);
+    }
 }
 
 void build_ktab(const imf_kernel* k, int Sw, std::vector<int>& t) {
@@ -247,6 +261,8 @@ int imf_filter(const imf_image* src, imf_image* dst, const imf_kernel* kernel, i
 
     std::vector<int> ktab;
     build_ktab(kernel, p.g.Sw, ktab);
+    static thread_local KTab kt;
+    build_ktab_struct(kernel, p.g.Sw, kt);
     if (cudaError_t e = cudaMemsetAsync(status, 0, sizeof(int), s)) return cuda_fail(e, "status memset");
     if (cudaError_t e = cudaMemcpyAsync(ktab_d, ktab.data(), ktab.size() * 4, cudaMemcpyHostToDevice, s))
         return cuda_fail(e, "kernel table upload");
@@ -289,13 +305,13 @@ int imf_filter(const imf_image* src, imf_image* dst, const imf_kernel* kernel, i
         launch_k1(p, g, nb, omega, k1g, s);
         if (prof) cudaEventRecord(e1, s);
         if (sp.circle && !p.omg)
-            k2_select<true, false><<<nb, p.k2_threads, p.k2_smem, s>>>(g, sp, omega);
+            k2_select<true, false><<<nb, p.k2_threads, p.k2_smem, s>>>(g, sp, kt, omega);
         else if (!p.omg)
-            k2_select<false, false><<<nb, p.k2_threads, p.k2_smem, s>>>(g, sp, omega);
+            k2_select<false, false><<<nb, p.k2_threads, p.k2_smem, s>>>(g, sp, kt, omega);
         else if (sp.circle)
-            k2_select<true, true><<<nb, p.k2_threads, p.k2_smem, s>>>(g, sp, omega);
+            k2_select<true, true><<<nb, p.k2_threads, p.k2_smem, s>>>(g, sp, kt, omega);
         else
-            k2_select<false, true><<<nb, p.k2_threads, p.k2_smem, s>>>(g, sp, omega);
+            k2_select<false, true><<<nb, p.k2_threads, p.k2_smem, s>>>(g, sp, kt, omega);
         if (prof) {
             cudaEventRecord(e2, s);
             ev.push_back(e0);

@@ -37,6 +37,16 @@ struct Geom {
     long long tile_begin;          // first tile of this launch (chunking)
 };
 
+// Kernel offset tables, passed by value as a __grid_constant__ kernel parameter
+// (constant bank): every thread of a warp reads the same entry in the same
+// iteration, so the tables are uniform-datapath loads, not shared-memory traffic.
+constexpr int KTAB_MAX = 249;  // 2*124 + 1 rows / columns
+struct KTab {
+    int2 v[KTAB_MAX];    // per kernel column: ((ybot+1)*Sw + dx, ytop*Sw + dx)  (down-slide enter, exit)
+    int2 h[KTAB_MAX];    // per kernel row:    (dy*Sw + xhi, dy*Sw + xlo)          (right-slide enter, exit)
+    int span[KTAB_MAX];  // per dy + r: (xlo & 0xffff) | (xhi - xlo) << 16
+};
+
 struct TileCoord {
     int b, c, ty, tx;
     int oy0, ox0;                  // output origin of the tile

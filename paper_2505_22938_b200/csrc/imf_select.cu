@@ -82,24 +82,18 @@ __device__ __forceinline__ uint32_t test8(const Ctx& c, int v, int cx, int cy) {
 // walk leaves [0, N) (inconsistent state: core.py:31-36 ScanDefectError).
 template <bool CIRCLE>
 __device__ int refine_thread(const Ctx& c, int cx, int cy, int P, int cnt, int t) {
-    if (cnt <= t) {
-        int need = t - cnt;  // members to skip at ranks >= P
-        for (int v = P; v < c.N; v += 8) {
-            const uint32_t m = test8<CIRCLE>(c, v, cx, cy);
-            const int pc = __popc(m);
-            if (need < pc) return v + (int)__fns(m, 0, need + 1);
-            need -= pc;
-        }
-        return -1;
-    }
-    int need = cnt - t - 1;  // members to skip below P, counting downward
-    for (int v = P - 8; v > -8; v -= 8) {
+    // One loop for both directions, so lanes of a warp walking up and lanes
+    // walking down share iterations instead of serializing two loops.
+    const bool up = cnt <= t;
+    int need = up ? t - cnt : cnt - t - 1;  // members to skip (from P outward)
+    const int step = up ? 8 : -8;
+    for (int v = up ? P : P - 8;; v += step) {
+        if (up ? v >= c.N : v <= -8) return -1;
         const uint32_t m = test8<CIRCLE>(c, v, cx, cy);
         const int pc = __popc(m);
-        if (need < pc) return v + (int)__fns(m, 0, pc - need);
+        if (need < pc) return v + (int)__fns(m, 0, up ? need + 1 : pc - need);
         need -= pc;
     }
-    return -1;
 }
 
 // Warp-collaborative refine: all lanes hold the same window;
@@ -155,30 +149,40 @@ __device__ __forceinline__ void write_out(const Ctx& c, const TileCoord& tc, int
     }
 }
 
-// Count change of a slide, from two offset tables: + [I[b+e] < P] - [I[b+x] < P].
-__device__ __forceinline__ int slide_delta(const uint16_t* __restrict__ Ib,
-                                           const int2* __restrict__ tab, int n, int P, bool swap) {
-    int d = 0;
-    if (!swap) {
-#pragma unroll 4
-        for (int k = 0; k < n; k++) {
-            const int2 o = tab[k];
-            d += ((int)Ib[o.x] < P) - ((int)Ib[o.y] < P);
-        }
-    } else {
-#pragma unroll 4
-        for (int k = 0; k < n; k++) {
-            const int2 o = tab[k];
-            d += ((int)Ib[o.y] < P) - ((int)Ib[o.x] < P);
-        }
-    }
-    return d;
+// acc += (a < P) for a, P in [0, 2^16): the sign bit of a - P (IADD + LEA.HI).
+__device__ __forceinline__ void acc_lt(unsigned& acc, unsigned a, unsigned P) {
+    asm("{\n\t.reg .u32 t;\n\tsub.u32 t, %1, %2;\n\tshr.u32 t, t, 31;\n\tadd.u32 %0, %0, t;\n\t}"
+        : "+r"(acc) : "r"(a), "r"(P));
 }
 
-// OMG: omega stays in its global (L2-resident) slot instead of shared memory,
-// for tiles whose omega + ordinal image exceed shared memory (r >~ 110).
+// Count change of a slide, from a BYTE-offset table in the constant bank
+// (__grid_constant__ kernel parameter): + #[I[b+e] < P] - #[I[b+x] < P].
+__device__ __forceinline__ int slide_delta(const unsigned char* __restrict__ Ib, const int2* tab,
+                                           int n, int P, bool swap) {
+    unsigned ein = 0, eout = 0;
+#pragma unroll 4
+    for (int k = 0; k < n; k++) {
+        const int2 o = tab[k];
+        acc_lt(ein, *reinterpret_cast<const uint16_t*>(Ib + o.x), (unsigned)P);
+        acc_lt(eout, *reinterpret_cast<const uint16_t*>(Ib + o.y), (unsigned)P);
+    }
+    return swap ? (int)eout - (int)ein : (int)ein - (int)eout;
+}
+
+// Warp-collaborative slide delta: lanes split the n table entries.
+__device__ __forceinline__ int slide_delta_warp(const unsigned char* __restrict__ Ib, const int2* tab,
+                                                int n, int P, int lane) {
+    unsigned ein = 0, eout = 0;
+    for (int k = lane; k < n; k += 32) {
+        const int2 o = tab[k];
+        acc_lt(ein, *reinterpret_cast<const uint16_t*>(Ib + o.x), (unsigned)P);
+        acc_lt(eout, *reinterpret_cast<const uint16_t*>(Ib + o.y), (unsigned)P);
+    }
+    return (int)__reduce_add_sync(FULLM, ein) - (int)__reduce_add_sync(FULLM, eout);
+}
+
 template <bool CIRCLE, bool OMG>
-__global__ void __launch_bounds__(512) k2_select(Geom g, SelParams p,
+__global__ void __launch_bounds__(512) k2_select(Geom g, SelParams p, const __grid_constant__ KTab kt,
                                                  const uint16_t* __restrict__ omega_in) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nwarps = blockDim.x >> 5;
@@ -190,18 +194,21 @@ __global__ void __launch_bounds__(512) k2_select(Geom g, SelParams p,
     uint16_t* om_s = reinterpret_cast<uint16_t*>(smem) + OMEGA_PAD;
     const uint16_t* om = OMG ? om_g : om_s;
     uint16_t* I = OMG ? reinterpret_cast<uint16_t*>(smem) : om_s + Npad + OMEGA_PAD;
-    int* ktab = reinterpret_cast<int*>(I + ((N + 7) & ~7));
-    const int ktab_n = 2 * p.ncols + 2 * p.nrows + 2 * r + 1;
-    int* st_P = ktab + ((ktab_n + 3) & ~3);
+    int* st_P = reinterpret_cast<int*>(I + ((N + 7) & ~7));
     int* st_C = st_P + G * Tw;
     int* deltas = st_C + G * Tw;                   // max(G*Tw, Th) entries
     int* hist = deltas + max(G * Tw, Th);          // 32 bins
     int* seedP = hist + 32;                        // G
     int* seedC = seedP + G;                        // G
+    // shared copies of the offset tables for lane-divergent indexing (the
+    // constant bank serializes divergent addresses; uniform loops use kt.*)
+    int2* vtab_s = reinterpret_cast<int2*>((reinterpret_cast<uintptr_t>(seedC + G) + 7) & ~uintptr_t(7));
+    int2* htab_s = vtab_s + p.ncols;
+    int* span_s = reinterpret_cast<int*>(htab_s + p.nrows);
 
-    const int2* vtab = reinterpret_cast<const int2*>(ktab);
-    const int2* htab = reinterpret_cast<const int2*>(ktab + 2 * p.ncols);
-    const Ctx c{&g, &p, om, I, ktab + 2 * p.ncols + 2 * p.nrows, N, Sw, r};
+    const int2* vtab = kt.v;
+    const int2* htab = kt.h;
+    const Ctx c{&g, &p, om, I, span_s, N, Sw, r};
 
     // ---- 0. stage omega and build the ordinal image -----------------------
     {
@@ -224,8 +231,10 @@ __global__ void __launch_bounds__(512) k2_select(Geom g, SelParams p,
             om_s[-OMEGA_PAD + tid] = OMEGA_SENTINEL;
             om_s[Npad + tid] = OMEGA_SENTINEL;
         }
-        for (int i = tid; i < ktab_n; i += blockDim.x) ktab[i] = __ldg(p.ktab + i);
         if (tid < 32) hist[tid] = 0;
+        for (int i = tid; i < p.ncols; i += blockDim.x) vtab_s[i] = kt.v[i];
+        for (int i = tid; i < p.nrows; i += blockDim.x) htab_s[i] = kt.h[i];
+        for (int i = tid; i < 2 * r + 1; i += blockDim.x) span_s[i] = kt.span[i];
     }
     __syncthreads();
 
@@ -244,10 +253,11 @@ __global__ void __launch_bounds__(512) k2_select(Geom g, SelParams p,
         for (int b = 0; b < 5; b++) lm[b] = ((lane >> b) & 1) ? 0u : FULLM;
         int cntb = 0;
         for (int k = wid; k < p.nrows; k += nwarps) {
-            const int2 hp = htab[k];  // (dy*Sw + xhi, dy*Sw + xlo)
-            for (int o0 = hp.y; o0 < hp.x; o0 += 32) {
+            const int2 hp = htab[k];  // byte offsets (2*(dy*Sw + xhi), 2*(dy*Sw + xlo))
+            const int hx = hp.x >> 1;
+            for (int o0 = hp.y >> 1; o0 < hx; o0 += 32) {
                 const int o = o0 + lane;
-                const bool ok = o < hp.x;
+                const bool ok = o < hx;
                 const unsigned b = ok ? (unsigned)(Ic[o] >> sh) : 0u;
                 unsigned m = __ballot_sync(FULLM, ok);
 #pragma unroll
@@ -280,12 +290,14 @@ __global__ void __launch_bounds__(512) k2_select(Geom g, SelParams p,
     __syncthreads();
 
     // ---- B. other seed rows: vertical deltas at the direct seed's pivot ----
+    const unsigned char* Ib0 = reinterpret_cast<const unsigned char*>(I);
+    const int rowB = 2 * Sw;  // bytes per ordinal-image row
     const int ytop = seed_row(0), ybot = seed_row(G - 1);
     if (G > 1) {
         const int P0 = seedP[g0];
-        for (int y = ytop + tid; y < ybot; y += blockDim.x) {  // step y -> y+1, column cs
-            const uint16_t* Ib = I + (y + r) * Sw + cs + r;
-            deltas[y] = slide_delta(Ib, vtab, p.ncols, P0, false);
+        for (int y = ytop + wid; y < ybot; y += nwarps) {  // step y -> y+1 at column cs, one warp each
+            const int d = slide_delta_warp(Ib0 + (y + r) * rowB + 2 * (cs + r), vtab_s, p.ncols, P0, lane);
+            if (lane == 0) deltas[y] = d;
         }
         __syncthreads();
         for (int gi = wid; gi < G; gi += nwarps) {
@@ -310,11 +322,12 @@ __global__ void __launch_bounds__(512) k2_select(Geom g, SelParams p,
     }
 
     // ---- C. seed rows: horizontal deltas at the row pivot, then refine ----
-    for (int u = tid; u < G * Tw; u += blockDim.x) {
+    for (int u = wid; u < G * Tw; u += nwarps) {  // step j -> j+1 of seed row gi, one warp each
         const int gi = u / Tw, j = u % Tw;
-        if (j + 1 < Tw) {  // step j -> j+1
-            const uint16_t* Ib = I + (seed_row(gi) + r) * Sw + j + r;
-            deltas[u] = slide_delta(Ib, htab, p.nrows, seedP[gi], false);
+        if (j + 1 < Tw) {
+            const int d = slide_delta_warp(Ib0 + (seed_row(gi) + r) * rowB + 2 * (j + r), htab_s,
+                                           p.nrows, seedP[gi], lane);
+            if (lane == 0) deltas[u] = d;
         }
     }
     __syncthreads();
@@ -347,14 +360,15 @@ __global__ void __launch_bounds__(512) k2_select(Geom g, SelParams p,
         int P = st_P[gi * Tw + j], cnt = st_C[gi * Tw + j];
         if (down) write_out(c, tc, P, row0, j);
         const int cx = j + r;
+        const unsigned char* Ic = Ib0 + 2 * cx;
         const int nsteps = down ? (rend - 1 - row0) : (row0 - gi * R);
         int row = row0;
         for (int step = 0; step < nsteps; step++) {
             if (down) {
-                cnt += slide_delta(I + (row + r) * Sw + cx, vtab, p.ncols, P, false);
+                cnt += slide_delta(Ic + (row + r) * rowB, vtab, p.ncols, P, false);
                 row++;
             } else {
-                cnt += slide_delta(I + (row + r - 1) * Sw + cx, vtab, p.ncols, P, true);
+                cnt += slide_delta(Ic + (row + r - 1) * rowB, vtab, p.ncols, P, true);
                 row--;
             }
             const int tgt = target_at(g, p, tc, row, j);
@@ -370,16 +384,16 @@ __global__ void __launch_bounds__(512) k2_select(Geom g, SelParams p,
     }
 }
 
-template __global__ void k2_select<true, false>(Geom, SelParams, const uint16_t*);
-template __global__ void k2_select<false, false>(Geom, SelParams, const uint16_t*);
-template __global__ void k2_select<true, true>(Geom, SelParams, const uint16_t*);
-template __global__ void k2_select<false, true>(Geom, SelParams, const uint16_t*);
+template __global__ void k2_select<true, false>(Geom, SelParams, const __grid_constant__ KTab, const uint16_t*);
+template __global__ void k2_select<false, false>(Geom, SelParams, const __grid_constant__ KTab, const uint16_t*);
+template __global__ void k2_select<true, true>(Geom, SelParams, const __grid_constant__ KTab, const uint16_t*);
+template __global__ void k2_select<false, true>(Geom, SelParams, const __grid_constant__ KTab, const uint16_t*);
 
 size_t k2_smem_bytes(int N, int Npad, int ncols, int nrows, int r, int G, int Tw, int Th, bool omg) {
-    const int ktab_n = 2 * ncols + 2 * nrows + 2 * r + 1;
     const int gt = G * Tw;
+    const size_t tabs = 8 * (size_t)(ncols + nrows) + 4 * (size_t)(2 * r + 1) + 8;
     return (omg ? 0 : 2 * (size_t)(Npad + 2 * OMEGA_PAD)) + 2 * (size_t)((N + 7) & ~7) +
-           4 * (size_t)((ktab_n + 3) & ~3) + 4 * (size_t)(2 * gt + (gt > Th ? gt : Th) + 32 + 2 * G);
+           4 * (size_t)(2 * gt + (gt > Th ? gt : Th) + 32 + 2 * G + 2) + tabs;
 }
 
 }  // namespace imf

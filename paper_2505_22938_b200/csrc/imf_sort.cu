@@ -146,7 +146,7 @@ __device__ __forceinline__ void store_omega(const Geom& g, const uint16_t* om_s,
 }
 
 template <int DT, bool GMEM>
-__global__ void __launch_bounds__(512) k1_sort(Geom g, uint16_t* __restrict__ omega_out,
+__global__ void __launch_bounds__(1024) k1_sort(Geom g, uint16_t* __restrict__ omega_out,
                                                unsigned char* __restrict__ gscratch,
                                                long long gscratch_stride) {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -223,7 +223,7 @@ __global__ void __launch_bounds__(512) k1_sort(Geom g, uint16_t* __restrict__ om
 // straight from global memory twice (L2-resident), with the clamped column
 // offsets of every lane precomputed once.  Requires N <= 65535 (S <= 255).
 template <int DT>
-__global__ void __launch_bounds__(512) k1_count(Geom g, uint16_t* __restrict__ omega_out) {
+__global__ void __launch_bounds__(1024) k1_count(Geom g, uint16_t* __restrict__ omega_out) {
     extern __shared__ __align__(16) unsigned char smem[];
     constexpr int NB = DT == DT_U8 ? 256 : 65536;
     constexpr int NW = NB / 2;  // histogram words
