@@ -40,7 +40,7 @@ constexpr size_t kOmegaScratchTarget = 96ull << 20;  // stays mostly L2-resident
 
 struct Plan {
     Geom g;
-    int G, k2_threads, k1_threads;
+    int G, k2_threads, k1_threads, paired;
     bool k1_gmem, k1_count, omg;
     size_t k1_smem, k2_smem, k1_gs_per_tile;
     long long total_tiles, chunk_tiles;
@@ -77,12 +77,14 @@ int make_plan(const imf_image* src, const imf_kernel* k, const imf_options* opt,
     const int Tmax = std::max(1, std::min(opt->tile_size > 0 ? opt->tile_size : env_int("IMF_TILE", 64),
                                           255 - 2 * r));
     const int G0 = opt->seed_rows > 0 ? opt->seed_rows : env_int("IMF_SEED_ROWS", 4);
+    const int paired = env_int("IMF_PAIRED", 0);
     double best = -1.0;
     for (int T = Tmax; T >= 1; T--) {
         const int S = T + 2 * r;
         const int N = S * S, Npad = (N + 63) & ~63;
         const int G = std::max(1, std::min(G0, T));
-        const int thr = std::min(((T * G * 2 + 31) / 32) * 32, 512);
+        const int thr = std::min(((T * G * (paired ? 1 : 2) + 31) / 32) * 32, 512);
+        if (paired && T * G > 512) continue;
         for (int omg = 0; omg < 2; omg++) {
             const size_t k2s = k2_smem_bytes(N, Npad, k->ncols, k->nrows, r, G, T, T, omg != 0);
             if (k2s > kSmemMax) continue;
@@ -94,6 +96,7 @@ int make_plan(const imf_image* src, const imf_kernel* k, const imf_options* opt,
                 p.g.N = N;
                 p.g.Npad = Npad;
                 p.G = G;
+                p.paired = paired;
                 p.k2_threads = thr;
                 p.k2_smem = k2s;
                 p.omg = omg != 0;
@@ -284,6 +287,7 @@ int imf_filter(const imf_image* src, imf_image* dst, const imf_kernel* kernel, i
     sp.target = target;
     sp.tmap = target_map;
     sp.G = p.G;
+    sp.paired = p.paired;
     sp.ktab = ktab_d;
     sp.status = status;
 

@@ -60,6 +60,7 @@ struct SelParams {
     int target;          // scalar target rank (tiling.py:176-177 / kernels.py:191-192)
     const int* tmap;     // per-pixel target ranks [out_h*out_w] or nullptr
     int G;               // seed rows per tile
+    int paired;          // 1: one thread slides a window down and one up (phase D)
     const int* ktab;     // [ncols pairs (VE,VX)][nrows pairs (HP,HM)][2r+1 spans]
     int* status;         // device status word (1 = scan defect)
 };

@@ -215,6 +215,100 @@ __global__ void __launch_bounds__(1024) k1_sort(Geom g, uint16_t* __restrict__ o
     store_omega(g, om, om_g);
 }
 
+// Exclusive scan, in place, of the 2*NW 16-bit counters packed two per word
+// in hw[0..NW).  Warp w owns words [w*NW/nw, (w+1)*NW/nw); lanes stride by one
+// word, so every shared access is bank-conflict free.  Ends with the counters
+// replaced by their exclusive prefix (no trailing barrier).
+__device__ __forceinline__ void hist16_exclusive_scan(uint32_t* hw, const int NW) {
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+    __shared__ uint32_t wt[32];
+    const int per = NW / nw;  // words per warp (NW and nw are powers of two)
+    if (per >= 128) {
+        // 16-byte chunks: lane l of the warp handles chunk i*32 + l of the warp's
+        // range (conflict-free), 8 counters per lane per step.
+        uint4* wb = reinterpret_cast<uint4*>(hw + wid * per);
+        const int nch = per >> 2;  // chunks per warp, multiple of 32
+        uint32_t sum = 0;
+        for (int i = lane; i < nch; i += 32) {
+            const uint4 q = wb[i];
+            sum += (q.x & 0xffffu) + (q.x >> 16) + (q.y & 0xffffu) + (q.y >> 16) +
+                   (q.z & 0xffffu) + (q.z >> 16) + (q.w & 0xffffu) + (q.w >> 16);
+        }
+        sum = __reduce_add_sync(0xffffffffu, sum);
+        if (lane == 0) wt[wid] = sum;
+        __syncthreads();
+        if (wid == 0) {
+            uint32_t v = lane < nw ? wt[lane] : 0, x = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                uint32_t t = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += t;
+            }
+            if (lane < nw) wt[lane] = x - v;
+        }
+        __syncthreads();
+        uint32_t carry = wt[wid];
+        for (int i0 = 0; i0 < nch; i0 += 32) {
+            uint4 q = wb[i0 + lane];
+            const uint32_t c0 = q.x & 0xffffu, c1 = q.x >> 16, c2 = q.y & 0xffffu, c3 = q.y >> 16;
+            const uint32_t c4 = q.z & 0xffffu, c5 = q.z >> 16, c6 = q.w & 0xffffu, c7 = q.w >> 16;
+            const uint32_t tot = c0 + c1 + c2 + c3 + c4 + c5 + c6 + c7;
+            uint32_t incl = tot;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += t;
+            }
+            uint32_t e = carry + incl - tot;
+            const uint32_t e1 = e + c0, e2 = e1 + c1, e3 = e2 + c2, e4 = e3 + c3;
+            const uint32_t e5 = e4 + c4, e6 = e5 + c5, e7 = e6 + c6;
+            q.x = e | (e1 << 16);
+            q.y = e2 | (e3 << 16);
+            q.z = e4 | (e5 << 16);
+            q.w = e6 | (e7 << 16);
+            wb[i0 + lane] = q;
+            carry += __shfl_sync(0xffffffffu, incl, 31);
+        }
+        return;
+    }
+    // small histograms (u8: 128 words): one word per lane per step
+    const uint32_t* wbase = hw + wid * per;
+    uint32_t sum = 0;
+    for (int i = lane; i < per; i += 32) {
+        const uint32_t w = wbase[i];
+        sum += (w & 0xffffu) + (w >> 16);
+    }
+    sum = __reduce_add_sync(0xffffffffu, sum);
+    if (lane == 0) wt[wid] = sum;
+    __syncthreads();
+    if (wid == 0) {
+        uint32_t v = lane < nw ? wt[lane] : 0, x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t t = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += t;
+        }
+        if (lane < nw) wt[lane] = x - v;
+    }
+    __syncthreads();
+    uint32_t carry = wt[wid];
+    uint32_t* wb = hw + wid * per;
+    for (int i0 = 0; i0 < per; i0 += 32) {
+        const bool ok = i0 + lane < per;
+        const uint32_t w = ok ? wb[i0 + lane] : 0u;
+        const uint32_t lo = w & 0xffffu, tot = lo + (w >> 16);
+        uint32_t incl = tot;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        const uint32_t ex = carry + incl - tot;
+        if (ok) wb[i0 + lane] = ex | ((ex + lo) << 16);
+        carry += __shfl_sync(0xffffffffu, incl, 31);
+    }
+}
+
 // Direct counting sort for 8/16-bit tiles (ordinal.py:62-79 _rank_by_bucket,
 // the paper's 16-bit bucket sort): one 2^bits-bin histogram
 // of u16 counters packed two per 32-bit word in shared memory (65536 bins =
@@ -263,47 +357,7 @@ __global__ void __launch_bounds__(1024) k1_count(Geom g, uint16_t* __restrict__ 
         }
     }
     __syncthreads();
-    {   // exclusive scan over NB 16-bit counters (two per word).  Warp w owns the
-        // contiguous word range [w*per, (w+1)*per); lanes stride by one word so
-        // every shared access is bank-conflict free.
-        __shared__ uint32_t wt[32];
-        const int per = NW / nw;  // NW and nw are powers of two (<= 16 warps)
-        const uint32_t* wbase = hw + wid * per;
-        uint32_t sum = 0;
-        for (int i = lane; i < per; i += 32) {
-            const uint32_t w = wbase[i];
-            sum += (w & 0xffffu) + (w >> 16);
-        }
-        sum = __reduce_add_sync(0xffffffffu, sum);
-        if (lane == 0) wt[wid] = sum;
-        __syncthreads();
-        if (wid == 0) {
-            uint32_t v = lane < nw ? wt[lane] : 0, x = v;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                uint32_t t = __shfl_up_sync(0xffffffffu, x, o);
-                if (lane >= o) x += t;
-            }
-            if (lane < nw) wt[lane] = x - v;
-        }
-        __syncthreads();
-        uint32_t carry = wt[wid];
-        uint32_t* wb = hw + wid * per;
-        for (int i0 = 0; i0 < per; i0 += 32) {
-            const bool ok = i0 + lane < per;
-            const uint32_t w = ok ? wb[i0 + lane] : 0u;
-            const uint32_t lo = w & 0xffffu, tot = lo + (w >> 16);
-            uint32_t incl = tot;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += t;
-            }
-            const uint32_t ex = carry + incl - tot;
-            if (ok) wb[i0 + lane] = ex | ((ex + lo) << 16);
-            carry += __shfl_sync(0xffffffffu, incl, 31);
-        }
-    }
+    hist16_exclusive_scan(hw, NW);
     __syncthreads();
     for (int y = wid; y < Sh; y += nw) {
         const char* rp = row_ptr(y);
