@@ -313,9 +313,8 @@ __global__ void __launch_bounds__(512) k2_select(Geom g, SelParams p, const __gr
     const int ytop = seed_row(0), ybot = seed_row(G - 1);
     if (G > 1) {
         const int P0 = seedP[g0];
-        for (int y = ytop + wid; y < ybot; y += nwarps) {  // step y -> y+1 at column cs, one warp each
-            const int d = slide_delta_warp(Ib0 + (y + r) * rowB + 2 * (cs + r), vtab_s, p.ncols, P0, lane);
-            if (lane == 0) deltas[y] = d;
+        for (int y = ytop + tid; y < ybot; y += blockDim.x) {  // step y -> y+1 at column cs
+            deltas[y] = slide_delta(Ib0 + (y + r) * rowB + 2 * (cs + r), vtab, p.ncols, P0, false);
         }
         __syncthreads();
         for (int gi = wid; gi < G; gi += nwarps) {
@@ -340,17 +339,15 @@ __global__ void __launch_bounds__(512) k2_select(Geom g, SelParams p, const __gr
     }
 
     // ---- C. seed rows: horizontal deltas at the row pivot, then refine ----
-    for (int u = wid; u < G * Tw; u += nwarps) {  // step j -> j+1 of seed row gi, one warp each
-        const int gi = u / Tw, j = u % Tw;
-        if (j + 1 < Tw) {
-            const int d = slide_delta_warp(Ib0 + (seed_row(gi) + r) * rowB + 2 * (j + r), htab_s,
-                                           p.nrows, seedP[gi], lane);
-            if (lane == 0) deltas[u] = d;
-        }
+    for (int u = tid; u < G * Tw; u += blockDim.x) {  // step j -> j+1 of seed row gi
+        const int gi = u / Tw, j = u - gi * Tw;
+        if (j + 1 < Tw)
+            deltas[u] = slide_delta(Ib0 + (seed_row(gi) + r) * rowB + 2 * (j + r), htab, p.nrows,
+                                    seedP[gi], false);
     }
     __syncthreads();
     for (int u = tid; u < G * Tw; u += blockDim.x) {
-        const int gi = u / Tw, j = u % Tw, row = seed_row(gi);
+        const int gi = u / Tw, j = u - gi * Tw, row = seed_row(gi);
         const int P = seedP[gi];
         int cnt = seedC[gi];
         if (j > cs) {
