@@ -42,6 +42,7 @@ struct Plan {
     Geom g;
     int G, k2_threads, k1_threads, paired;
     bool k1_gmem, k1_count, omg;
+    bool pair;  // K2 fast path (imf_pair.cu): two windows per thread, 15-bit ranks
     size_t k1_smem, k2_smem, k1_gs_per_tile;
     long long total_tiles, chunk_tiles;
     size_t ws_ktab, ws_omega, ws_k1g, ws_total;
@@ -79,7 +80,35 @@ int make_plan(const imf_image* src, const imf_kernel* k, const imf_options* opt,
     const int G0 = opt->seed_rows > 0 ? opt->seed_rows : env_int("IMF_SEED_ROWS", 4);
     const int paired = env_int("IMF_PAIRED", 0);
     double best = -1.0;
-    for (int T = Tmax; T >= 1; T--) {
+    // K2 fast path: tile ranks < 2^15 (S <= 181), even T, and T + r <= 128 for
+    // the packed circle test.  Largest such tile.
+    if (env_int("IMF_PAIR", 1)) {
+        int T = std::min(Tmax, 181 - 2 * r);
+        if (k->shape_code == IMF_SHAPE_CIRCLE) T = std::min(T, 128 - r);
+        T &= ~1;
+        if (T >= 2) {
+            const int S = T + 2 * r, N = S * S, Npad = (N + 63) & ~63;
+            int G = std::max(1, std::min(opt->seed_rows > 0 ? opt->seed_rows : env_int("IMF_SEED_ROWS", 8), T));
+            const int quad = env_int("IMF_QUAD", 1);
+            const int tpg = quad ? T / 2 : T;  // threads per seed-row group
+            while (G > 1 && ((G * tpg + 31) & ~31) > 512) G--;
+            const size_t ks = k2_pair_smem_bytes(N, Npad, r, G, T);
+            if (N <= 32768 && ((G * tpg + 31) & ~31) <= 512 && ks <= kSmemMax && k->ncols <= PT_MAX && k->nrows <= PT_MAX) {
+                best = 1.0;
+                p.pair = true;
+                p.g.Tw = p.g.Th = T;
+                p.g.Sw = p.g.Sh = S;
+                p.g.N = N;
+                p.g.Npad = Npad;
+                p.G = G;
+                p.k2_threads = std::max((G * tpg + 31) & ~31, 64);  // whole warps (phase A/B ballots)
+                p.paired = quad;
+                p.k2_smem = ks;
+                p.omg = false;
+            }
+        }
+    }
+    for (int T = Tmax; T >= 1 && !p.pair; T--) {
         const int S = T + 2 * r;
         const int N = S * S, Npad = (N + 63) & ~63;
         const int G = std::max(1, std::min(G0, T));
@@ -204,6 +233,8 @@ cudaError_t set_attrs() {
     if (!e) e = allow_smem(k2_select<false, false>, optin);
     if (!e) e = allow_smem(k2_select<true, true>, optin);
     if (!e) e = allow_smem(k2_select<false, true>, optin);
+    if (!e) e = allow_smem(k2_pair<true>, optin);
+    if (!e) e = allow_smem(k2_pair<false>, optin);
     if (!e) g_attr_done = true;
     return e;
 }
@@ -291,6 +322,24 @@ int imf_filter(const imf_image* src, imf_image* dst, const imf_kernel* kernel, i
     sp.ktab = ktab_d;
     sp.status = status;
 
+    static thread_local PairTab ptab;
+    PairParams pp;
+    memset(&pp, 0, sizeof(pp));
+    if (p.pair) {
+        const int r = kernel->radius;
+        if (!build_pair_tab(kernel->row_dy, kernel->row_xlo, kernel->row_xhi, kernel->nrows, kernel->col_dx,
+                            kernel->col_ytop, kernel->col_ybot, kernel->ncols, r, p.g.Sw, ptab, pp))
+            return IMF_ERR_UNSUPPORTED;
+        pp.circle = kernel->shape_code == IMF_SHAPE_CIRCLE && p.g.Tw + r <= 128;
+        pp.R2p1 = r * (r + 1) + 1;
+        pp.target = target;
+        pp.tmap = target_map;
+        pp.G = p.G;
+        pp.quad = p.paired;
+        pp.span = ktab_d + 2 * kernel->ncols + 2 * kernel->nrows;
+        pp.status = status;
+    }
+
     // Optional per-kernel timing (opt->reserved[0] & 1): CUDA events recorded on
     // `stream` around every launch; the call then synchronizes and leaves the
     // sums in imf_profile_last().  Used by bench.py for the roofline figure.
@@ -308,7 +357,12 @@ int imf_filter(const imf_image* src, imf_image* dst, const imf_kernel* kernel, i
         }
         launch_k1(p, g, nb, omega, k1g, s);
         if (prof) cudaEventRecord(e1, s);
-        if (sp.circle && !p.omg)
+        if (p.pair) {
+            if (pp.circle)
+                k2_pair<true><<<nb, p.k2_threads, p.k2_smem, s>>>(g, pp, ptab, omega);
+            else
+                k2_pair<false><<<nb, p.k2_threads, p.k2_smem, s>>>(g, pp, ptab, omega);
+        } else if (sp.circle && !p.omg)
             k2_select<true, false><<<nb, p.k2_threads, p.k2_smem, s>>>(g, sp, kt, omega);
         else if (!p.omg)
             k2_select<false, false><<<nb, p.k2_threads, p.k2_smem, s>>>(g, sp, kt, omega);
@@ -339,7 +393,7 @@ int imf_filter(const imf_image* src, imf_image* dst, const imf_kernel* kernel, i
         for (cudaEvent_t e : ev) cudaEventDestroy(e);
         g_prof.tiles = p.total_tiles;
         g_prof.tile = p.g.Tw;
-        g_prof.qs = p.omg ? 1 : 0;
+        g_prof.qs = p.pair ? 2 : (p.omg ? 1 : 0);
         g_prof.chunk = p.chunk_tiles;
     }
     return IMF_OK;

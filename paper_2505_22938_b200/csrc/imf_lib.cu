@@ -2,5 +2,6 @@
 // host launch stubs must live in the same TU without -rdc).
 #include "imf_sort.cu"
 #include "imf_select.cu"
+#include "imf_pair.cu"
 #include "imf_api.cu"
 #include "imf_peak.cu"

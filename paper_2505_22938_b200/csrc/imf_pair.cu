@@ -1,0 +1,808 @@
+// imf_pair.cu -- K2 fast path: per-output-pixel rank selection with two
+// windows per thread and packed 15-bit rank compares (sm_100a).
+//
+// Same algorithm and phases as k2_select (imf_select.cu: direct seed, seed-row
+// centres, seed rows, vertical sweeps -- core.py:47-60, :63-84, :87-146), with
+// the two inner loops re-laid-out for the B200 SM:
+//
+// * Slides (core.py:63-84, 2 tests per kernel column/row per window).  A
+//   thread owns the windows of two horizontally adjacent output pixels.  Their
+//   entering / exiting pixels are horizontally adjacent too, so ONE 32-bit
+//   shared load returns both windows' ranks (I[o], I[o+1]).  With tile ranks
+//   below 2^15 (N <= 32768) the two "rank >= pivot" tests are one add:
+//       d = (I[o+1] << 16 | I[o]) + ((0x8000 - P_B) << 16 | (0x8000 - P_A))
+//   leaves [I >= P] in bits 15 and 31 (no carry crosses the halves), and
+//   acc += (d & 0x80008000) >> 15 (LOP3 + LEA.HI) counts both.  Offsets come
+//   from the constant bank and the load uses the [R + UR] form, so a kernel
+//   column costs 2 LDS + 6 integer ops for 4 tests (reference: 4 tests = 8 ops).
+//   Offsets whose pixel pair is not 4-byte aligned read the two enclosing words
+//   and PRMT the middle halves.
+// * Refine (core.py:87-146, ordinal.py:175-199).  Eight ranks per step from one
+//   LDS.128 of omega.  Circle membership 4(dx^2+dy^2) <= (2r+1)^2 (kernels.py:
+//   70-71) is evaluated on packed bytes: omega entry x | y << 8 plus a per-window
+//   constant gives (dx+128, dy+128) bytes for two ranks at once, XOR 0x80
+//   makes them signed, and IDP.4A squares-and-adds them against -(r(r+1)+1);
+//   the sign bit is the membership bit (funnel-shifted into the step mask).
+//   Requires |dx|, |dy| <= 127 over the tile: T + r <= 128.  Square / polygon
+//   kernels use the span table (kernels.py:127-182) per rank.
+//
+// Layout (shared memory): omega (rank -> x | y << 8, 8 sentinel entries each
+// side, 16-byte aligned so rank 8k starts a 16-byte chunk), then the ordinal
+// image I (u16 rank per input-tile pixel, row stride Sw), then per-window state.
+#include "imf_common.cuh"
+
+namespace imf {
+
+constexpr int PT_MAX = 184;  // >= S for N <= 32768 (S <= 181), rounded to 8
+
+// Byte offsets into I relative to a window pair's base 2*(row*Sw + 2q), in
+// the constant bank.  Every list holds its 4-byte-aligned entries first; the
+// rest ("odd") store the offset of the aligned word BEFORE the pixel pair.
+struct PairTab {
+    int2 v[PT_MAX];  // per kernel column: (enter, exit) of a down slide
+    int he[PT_MAX];  // per kernel row: pixel entering on a right slide
+    int hx[PT_MAX];  // per kernel row: pixel exiting on a right slide
+};
+
+struct PairParams {
+    int circle;      // 1: packed circle test (requires T + r <= 128)
+    int R2p1;        // r(r+1) + 1
+    int nv, nv_even;
+    int nh, nhe_even, nhx_even;
+    int target;
+    const int* tmap;
+    int G;
+    int quad;         // phase D with four windows per thread
+    const int* span;  // 2r+1 packed (xlo & 0xffff) | width << 16, device copy
+    int* status;
+};
+
+__device__ __forceinline__ uint32_t lds32(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+    uint4 q;
+    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(q.x), "=r"(q.y), "=r"(q.z), "=r"(q.w)
+                 : "r"(a));
+    return q;
+}
+
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t s) {
+    uint32_t r;
+    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(s));
+    return r;
+}
+
+// acc += (d & 0x80008000) >> 15: counts [I >= P] of both halves (LOP3 + LEA.HI).
+__device__ __forceinline__ void acc_ge2(uint32_t& acc, uint32_t d) {
+    asm("{\n\t.reg .u32 t;\n\tand.b32 t, %1, 0x80008000;\n\tshr.u32 t, t, 15;\n\tadd.u32 %0, %0, t;\n\t}"
+        : "+r"(acc)
+        : "r"(d));
+}
+
+// Packed pivot constant: halves (0x8000 - PA, 0x8000 - PB).
+__device__ __forceinline__ uint32_t pivot_k(int PA, int PB) {
+    return (uint32_t)(0x8000 - PA) | ((uint32_t)(0x8000 - PB) << 16);
+}
+
+// Packed counts of [I >= P] over the vertical list at window-pair base `b`
+// (two accumulators per list so the LEA.HI chains interleave).
+__device__ __forceinline__ void vcount(uint32_t b, const int2* __restrict__ v, int ne, int n, uint32_t K,
+                                       uint32_t& ge_in, uint32_t& ge_out) {
+    uint32_t ai0 = 0, ao0 = 0, ai1 = 0, ao1 = 0;
+    int k = 0;
+#pragma unroll 2
+    for (; k + 1 < ne; k += 2) {
+        const int2 o0 = v[k], o1 = v[k + 1];
+        acc_ge2(ai0, lds32(b + o0.x) + K);
+        acc_ge2(ao0, lds32(b + o0.y) + K);
+        acc_ge2(ai1, lds32(b + o1.x) + K);
+        acc_ge2(ao1, lds32(b + o1.y) + K);
+    }
+    if (k < ne) {
+        const int2 o = v[k];
+        acc_ge2(ai0, lds32(b + o.x) + K);
+        acc_ge2(ao0, lds32(b + o.y) + K);
+    }
+#pragma unroll 2
+    for (k = ne; k < n; k++) {
+        const int2 o = v[k];
+        acc_ge2(ai1, prmt(lds32(b + o.x), lds32(b + o.x + 4), 0x5432) + K);
+        acc_ge2(ao1, prmt(lds32(b + o.y), lds32(b + o.y + 4), 0x5432) + K);
+    }
+    ge_in = ai0 + ai1;
+    ge_out = ao0 + ao1;
+}
+
+// vcount for a down slide at base bd (pivots Kd) and an up slide at base bu
+// (pivots Ku) through the same column list: four independent accumulators,
+// one constant-bank offset fetch per column for both.
+__device__ __forceinline__ void vcount_du(uint32_t bd, uint32_t bu, const int2* __restrict__ v, int ne, int n,
+                                          uint32_t Kd, uint32_t Ku, uint32_t& d_in, uint32_t& d_out,
+                                          uint32_t& u_in, uint32_t& u_out) {
+    uint32_t di = 0, dx = 0, ui = 0, ux = 0;
+#pragma unroll 2
+    for (int k = 0; k < ne; k++) {
+        const int2 o = v[k];
+        acc_ge2(di, lds32(bd + o.x) + Kd);
+        acc_ge2(dx, lds32(bd + o.y) + Kd);
+        acc_ge2(ui, lds32(bu + o.x) + Ku);
+        acc_ge2(ux, lds32(bu + o.y) + Ku);
+    }
+#pragma unroll 2
+    for (int k = ne; k < n; k++) {
+        const int2 o = v[k];
+        acc_ge2(di, prmt(lds32(bd + o.x), lds32(bd + o.x + 4), 0x5432) + Kd);
+        acc_ge2(dx, prmt(lds32(bd + o.y), lds32(bd + o.y + 4), 0x5432) + Kd);
+        acc_ge2(ui, prmt(lds32(bu + o.x), lds32(bu + o.x + 4), 0x5432) + Ku);
+        acc_ge2(ux, prmt(lds32(bu + o.y), lds32(bu + o.y + 4), 0x5432) + Ku);
+    }
+    d_in = di;
+    d_out = dx;
+    u_in = ui;
+    u_out = ux;
+}
+
+// Packed count of [I >= P] over one horizontal list.
+__device__ __forceinline__ uint32_t hcount(uint32_t b, const int* __restrict__ h, int ne, int n, uint32_t K) {
+    uint32_t a = 0;
+#pragma unroll 4
+    for (int k = 0; k < ne; k++) acc_ge2(a, lds32(b + h[k]) + K);
+#pragma unroll 2
+    for (int k = ne; k < n; k++) acc_ge2(a, prmt(lds32(b + h[k]), lds32(b + h[k] + 4), 0x5432) + K);
+    return a;
+}
+
+// Per-half difference lo(a) - lo(b), hi(a) - hi(b).
+__device__ __forceinline__ void half_diff(uint32_t a, uint32_t b, int& lo, int& hi) {
+    lo = (int)(a & 0xffffu) - (int)(b & 0xffffu);
+    hi = (int)(a >> 16) - (int)(b >> 16);
+}
+
+// Index of the k-th (0-based) set bit of an 8-bit mask.
+__device__ __forceinline__ int nth_bit8(uint32_t m, int k) {
+    int pos = 0;
+    int c = __popc(m & 0xfu);
+    if (k >= c) { k -= c; m >>= 4; pos = 4; }
+    c = __popc(m & 0x3u);
+    if (k >= c) { k -= c; m >>= 2; pos += 2; }
+    if (k >= (int)(m & 1u)) pos += 1;
+    return pos;
+}
+
+struct PairCtx {
+    uint32_t om_a;        // shared address of omega rank 0
+    const uint16_t* om;   // generic pointer to omega rank 0
+    const int* span;      // shared span table (2r+1)
+    int N, r, R2p1;
+};
+
+// Membership bits of ranks v0..v0+7 (bit i = rank v0+i) of the window at (cx, cy).
+template <bool CIRCLE>
+__device__ __forceinline__ uint32_t test8(const PairCtx& c, int v0, uint32_t Kc, int cx, int cy) {
+    const uint4 q = lds128(c.om_a + 2 * v0);
+    const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+    uint32_t m = 0;
+    if (CIRCLE) {
+#pragma unroll
+        for (int i = 3; i >= 0; i--) {
+            const int b = (int)((w[i] + Kc) ^ 0x80808080u);
+            const int slo = __dp4a(b, b & 0xffff, -c.R2p1);
+            const int shi = __dp4a(b, (int)((uint32_t)b & 0xffff0000u), -c.R2p1);
+            m = __funnelshift_l((uint32_t)shi, m, 1);
+            m = __funnelshift_l((uint32_t)slo, m, 1);
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < 8; i++) {
+            const uint32_t e = (i & 1) ? (w[i >> 1] >> 16) : (w[i >> 1] & 0xffffu);
+            const int dy = (int)(e >> 8) - cy + c.r;
+            bool in = false;
+            if ((unsigned)dy <= (unsigned)(2 * c.r)) {
+                const int sp = c.span[dy];
+                in = (unsigned)((int)(e & 0xffu) - cx - (int)(short)(sp & 0xffff)) < (unsigned)(sp >> 16);
+            }
+            m |= (in ? 1u : 0u) << i;
+        }
+    }
+    return m;
+}
+
+// t-th smallest rank of the window at (cx, cy) from the exact state (P, cnt):
+// walk omega from P toward the target 8 ranks per step (core.py:87-146 with an
+// exact pivot).  -1 if the walk leaves [0, N) (core.py:31-36).
+template <bool CIRCLE>
+__device__ int refine8(const PairCtx& c, int cx, int cy, int P, int cnt, int t) {
+    const bool up = cnt <= t;
+    int need = up ? t - cnt : cnt - t - 1;
+    int v0;
+    uint32_t mask;
+    if (up) {
+        v0 = P & ~7;
+        mask = (0xffu << (P - v0)) & 0xffu;
+    } else {
+        if (P <= 0) return -1;
+        v0 = (P - 1) & ~7;
+        mask = (1u << (P - v0)) - 1u;
+    }
+    const int step = up ? 8 : -8;
+    const uint32_t Kc = (uint32_t)((128 - cx) + ((128 - cy) << 8)) * 0x10001u;
+    for (;;) {
+        if (v0 < 0 || v0 >= c.N) return -1;
+        uint32_t m = test8<CIRCLE>(c, v0, Kc, cx, cy) & mask;
+        if (v0 + 8 > c.N) m &= (1u << (c.N - v0)) - 1u;
+        const int pc = __popc(m);
+        if (need < pc) return v0 + nth_bit8(m, up ? need : pc - 1 - need);
+        need -= pc;
+        v0 += step;
+        mask = 0xffu;
+    }
+}
+
+// Both windows of a pair (columns cx and cx+1, same row) in ONE loop: a lane
+// moves on to window B as soon as A is solved, so a warp iterates
+// max(steps_A + steps_B) instead of max(steps_A) + max(steps_B).
+template <bool CIRCLE>
+__device__ __forceinline__ void refine8x2(const PairCtx& c, int cx, int cy, int PA, int cntA, int tA, int PB,
+                                          int cntB, int tB, int& mA, int& mB) {
+    bool up;
+    int need, v0, step, P = PA, cnt = cntA, t = tA, w = 0;
+    uint32_t mask, Kc;
+    auto init = [&]() {
+        up = cnt <= t;
+        need = up ? t - cnt : cnt - t - 1;
+        if (up) {
+            v0 = P & ~7;
+            mask = (0xffu << (P - v0)) & 0xffu;
+        } else {
+            v0 = (P - 1) & ~7;  // P == 0: v0 = -8, reported as a defect below
+            mask = (P > 0) ? (1u << (P - v0)) - 1u : 0xffu;
+        }
+        step = up ? 8 : -8;
+        Kc = (uint32_t)((128 - cx) + ((128 - cy) << 8)) * 0x10001u;
+    };
+    init();
+    mA = -1;
+    mB = -1;
+    for (;;) {
+        int res = -2;
+        if (v0 < 0 || v0 >= c.N) {
+            res = -1;
+        } else {
+            uint32_t m = test8<CIRCLE>(c, v0, Kc, cx, cy) & mask;
+            if (v0 + 8 > c.N) m &= (1u << (c.N - v0)) - 1u;
+            const int pc = __popc(m);
+            if (need < pc) {
+                res = v0 + nth_bit8(m, up ? need : pc - 1 - need);
+            } else {
+                need -= pc;
+                v0 += step;
+                mask = 0xffu;
+            }
+        }
+        if (res != -2) {
+            if (w == 0) {
+                mA = res;
+                w = 1;
+                cx += 1;
+                P = PB;
+                cnt = cntB;
+                t = tB;
+                init();
+            } else {
+                mB = res;
+                return;
+            }
+        }
+    }
+}
+
+// Four windows (a down pair at row cyd and an up pair at row cyu, columns cx
+// and cx+1) in one loop, tasks [w0, w1) of {0: down A, 1: down B, 2: up A,
+// 3: up B}: a warp iterates max over lanes of the SUM of the four walks.
+template <bool CIRCLE>
+__device__ __forceinline__ void refine8x4(const PairCtx& c, int cx0, int cyd, int cyu, const int (&P4)[4],
+                                          const int (&C4)[4], const int (&T4)[4], int w0, int w1, int (&M4)[4]) {
+    bool up;
+    int need, v0, step, w = w0, cx = 0, cy = 0;
+    uint32_t mask, Kc;
+    auto init = [&]() {
+        const int P = (w & 2) ? ((w & 1) ? P4[3] : P4[2]) : ((w & 1) ? P4[1] : P4[0]);
+        const int cnt = (w & 2) ? ((w & 1) ? C4[3] : C4[2]) : ((w & 1) ? C4[1] : C4[0]);
+        const int t = (w & 2) ? ((w & 1) ? T4[3] : T4[2]) : ((w & 1) ? T4[1] : T4[0]);
+        cx = cx0 + (w & 1);
+        cy = (w & 2) ? cyu : cyd;
+        up = cnt <= t;
+        need = up ? t - cnt : cnt - t - 1;
+        if (up) {
+            v0 = P & ~7;
+            mask = (0xffu << (P - v0)) & 0xffu;
+        } else {
+            v0 = (P - 1) & ~7;  // P == 0: v0 = -8, reported as a defect below
+            mask = (P > 0) ? (1u << (P - v0)) - 1u : 0xffu;
+        }
+        step = up ? 8 : -8;
+        Kc = (uint32_t)((128 - cx) + ((128 - cy) << 8)) * 0x10001u;
+    };
+    M4[0] = M4[1] = M4[2] = M4[3] = 0;
+    if (w0 >= w1) return;
+    init();
+    for (;;) {
+        int res = -2;
+        if (v0 < 0 || v0 >= c.N) {
+            res = -1;
+        } else {
+            uint32_t m = test8<CIRCLE>(c, v0, Kc, cx, cy) & mask;
+            if (v0 + 8 > c.N) m &= (1u << (c.N - v0)) - 1u;
+            const int pc = __popc(m);
+            if (need < pc) {
+                res = v0 + nth_bit8(m, up ? need : pc - 1 - need);
+            } else {
+                need -= pc;
+                v0 += step;
+                mask = 0xffu;
+            }
+        }
+        if (res != -2) {
+            if (w == 0) M4[0] = res;
+            else if (w == 1) M4[1] = res;
+            else if (w == 2) M4[2] = res;
+            else M4[3] = res;
+            if (++w >= w1) return;
+            init();
+        }
+    }
+}
+
+// Gather C[m] (the input value at omega[m]'s position, core.py:366) and the
+// flat destination index; the store is issued later so the L2 latency of the
+// gather overlaps the next slide.
+struct Pend {
+    uint32_t v;
+    long long d;
+    bool ok;
+};
+
+__device__ __forceinline__ Pend gather_out(const Geom& g, const TileCoord& tc, const uint16_t* om, int m, int row,
+                                           int col) {
+    Pend o;
+    const int oy = tc.oy0 + row, ox = tc.ox0 + col;
+    o.ok = oy < g.out_h && ox < g.out_w;
+    o.d = tc.b * g.d_b + (long long)oy * g.d_y + (long long)ox * g.d_x + tc.c * g.d_c;
+    o.v = 0;
+    if (o.ok) {
+        const uint32_t e = om[m];
+        const long long so = src_offset(g, tc, (int)(e >> 8), (int)(e & 0xff));
+        if (g.dtype == DT_U8)
+            o.v = __ldg((const uint8_t*)tc.src + so);
+        else if (g.dtype == DT_U16)
+            o.v = __ldg((const uint16_t*)tc.src + so);
+        else
+            o.v = __ldg((const uint32_t*)tc.src + so);
+    }
+    return o;
+}
+
+__device__ __forceinline__ void store_out(const Geom& g, const Pend& o) {
+    if (!o.ok) return;
+    if (g.dtype == DT_U8)
+        ((uint8_t*)g.dst)[o.d] = (uint8_t)o.v;
+    else if (g.dtype == DT_U16)
+        ((uint16_t*)g.dst)[o.d] = (uint16_t)o.v;
+    else
+        ((uint32_t*)g.dst)[o.d] = o.v;
+}
+
+__device__ __forceinline__ int target_at2(const Geom& g, const PairParams& p, const TileCoord& tc, int row,
+                                          int col) {
+    if (!p.tmap) return p.target;
+    const int y = min(tc.oy0 + row, g.out_h - 1), x = min(tc.ox0 + col, g.out_w - 1);
+    return __ldg(p.tmap + (long long)y * g.out_w + x);
+}
+
+// Output = C[m]: the input value at omega[m]'s position (core.py:366).
+__device__ __forceinline__ void write_out2(const Geom& g, const TileCoord& tc, const uint16_t* om, int m,
+                                           int row, int col) {
+    const int oy = tc.oy0 + row, ox = tc.ox0 + col;
+    if (oy >= g.out_h || ox >= g.out_w) return;
+    const uint32_t e = om[m];
+    const long long so = src_offset(g, tc, (int)(e >> 8), (int)(e & 0xff));
+    const long long d = tc.b * g.d_b + (long long)oy * g.d_y + (long long)ox * g.d_x + tc.c * g.d_c;
+    if (g.dtype == DT_U8) {
+        ((uint8_t*)g.dst)[d] = __ldg((const uint8_t*)tc.src + so);
+    } else if (g.dtype == DT_U16) {
+        ((uint16_t*)g.dst)[d] = __ldg((const uint16_t*)tc.src + so);
+    } else {
+        ((uint32_t*)g.dst)[d] = __ldg((const uint32_t*)tc.src + so);
+    }
+}
+
+// Warp-collaborative refine for the few seed windows (lane l tests ranks
+// v0+2l, v0+2l+1 of each 64-rank block), generic membership.
+template <bool CIRCLE>
+__device__ int refine_warp2(const PairCtx& c, int cx, int cy, int P, int cnt, int t) {
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = lanemask_lt();
+    const bool up = cnt <= t;
+    int need = up ? t - cnt : cnt - t - 1;
+    const int R2 = c.R2p1 - 1;
+    auto inside = [&](int v) -> bool {
+        if (v < 0 || v >= c.N) return false;
+        const uint32_t e = c.om[v];
+        const int dx = (int)(e & 0xffu) - cx, dyr = (int)(e >> 8) - cy;
+        if (CIRCLE) return dx * dx + dyr * dyr <= R2;
+        const int dy = dyr + c.r;
+        if ((unsigned)dy > (unsigned)(2 * c.r)) return false;
+        const int sp = c.span[dy];
+        return (unsigned)(dx - (int)(short)(sp & 0xffff)) < (unsigned)(sp >> 16);
+    };
+    for (int v0 = up ? P : P - 64;; v0 += up ? 64 : -64) {
+        if (up ? v0 >= c.N : v0 + 64 <= 0) return -1;
+        const int v = v0 + 2 * lane;
+        const bool i0 = inside(v), i1 = inside(v + 1);
+        const unsigned b0 = __ballot_sync(0xffffffffu, i0), b1 = __ballot_sync(0xffffffffu, i1);
+        const int pc = __popc(b0) + __popc(b1);
+        if (need < pc) {
+            const int k = up ? need : pc - 1 - need;
+            const int pre = __popc(b0 & lt) + __popc(b1 & lt);
+            const bool h0 = i0 && pre == k;
+            const bool h1 = i1 && pre + (i0 ? 1 : 0) == k;
+            const unsigned hb = __ballot_sync(0xffffffffu, h0 || h1);
+            const int L = __ffs(hb) - 1;
+            const int off = __shfl_sync(0xffffffffu, h0 ? 0 : 1, L);
+            return v0 + 2 * L + off;
+        }
+        need -= pc;
+    }
+}
+
+template <bool CIRCLE>
+__global__ void __launch_bounds__(512) k2_pair(Geom g, PairParams p, const __grid_constant__ PairTab kt,
+                                               const uint16_t* __restrict__ omega_in) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nwarps = blockDim.x >> 5;
+    const int N = g.N, Npad = g.Npad, Sw = g.Sw, r = g.r;
+    const int T = g.Tw, G = p.G, TH = T >> 1;
+    const TileCoord tc = tile_coord(g, g.tile_begin + blockIdx.x);
+
+    const uint16_t* om_g = omega_in + (long long)blockIdx.x * (Npad + 2 * OMEGA_SLOT_PAD) + OMEGA_SLOT_PAD;
+    uint16_t* om = reinterpret_cast<uint16_t*>(smem) + 8;  // 8 sentinels before rank 0
+    uint16_t* I = om + Npad + 8;                               // 16-byte aligned (Npad % 64 == 0)
+    const int Ipad = (N + 15) & ~7;
+    int* st_P = reinterpret_cast<int*>(I + Ipad);
+    int* st_C = st_P + G * T;
+    int* deltas = st_C + G * T;                // max(G*T, T) entries
+    int* hist = deltas + max(G * T, T);        // 32 bins
+    int* seedP = hist + 32;                    // G
+    int* seedC = seedP + G;                    // G
+    int* span_s = seedC + G;                   // 2r+1
+
+    // ---- 0. stage omega, build the ordinal image --------------------------
+    {
+        const uint4* src = reinterpret_cast<const uint4*>(om_g);
+        uint4* dst = reinterpret_cast<uint4*>(om);
+        for (int i = tid; i < (Npad >> 3); i += blockDim.x) {
+            const uint4 v = src[i];
+            dst[i] = v;
+            const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int q = 0; q < 8; q++) {
+                const int rank = (i << 3) + q;
+                if (rank < N) {
+                    const uint32_t e = (q & 1) ? (w[q >> 1] >> 16) : (w[q >> 1] & 0xffffu);
+                    I[(int)(e >> 8) * Sw + (int)(e & 0xffu)] = (uint16_t)rank;
+                }
+            }
+        }
+        if (tid < 8) {
+            om[-8 + tid] = 0;
+            om[Npad + tid] = 0;
+        }
+        for (int i = N + tid; i < Ipad; i += blockDim.x) I[i] = 0;
+        if (tid < 32) hist[tid] = 0;
+        for (int i = tid; i < 2 * r + 1; i += blockDim.x) span_s[i] = __ldg(p.span + i);
+    }
+    __syncthreads();
+
+    const uint32_t I_a = (uint32_t)__cvta_generic_to_shared(I);
+    const PairCtx c{(uint32_t)__cvta_generic_to_shared(om), om, span_s, N, r, p.R2p1};
+    const int R = T / G;
+    const int g0 = G >> 1;
+    const int cs = (T >> 1) & ~1;  // seed column (even: a pair base)
+    auto seed_row = [&](int gi) { return gi * R + (R >> 1); };
+
+    // ---- A. direct seed: 32-bin rank histogram over the window ------------
+    const int sh = max(0, 32 - __clz(max(N - 1, 1)) - 5);
+    {
+        const int cx = cs + r, cy = seed_row(g0) + r;
+        unsigned lm[5];
+#pragma unroll
+        for (int b = 0; b < 5; b++) lm[b] = ((lane >> b) & 1) ? 0u : 0xffffffffu;
+        int cntb = 0;
+        for (int dy = wid; dy <= 2 * r; dy += nwarps) {
+            const int sp = span_s[dy];
+            const int w = sp >> 16;
+            if (w <= 0) continue;
+            const uint16_t* row = I + (cy - r + dy) * Sw + cx + (int)(short)(sp & 0xffff);
+            for (int o0 = 0; o0 < w; o0 += 32) {
+                const int o = o0 + lane;
+                const bool ok = o < w;
+                const unsigned b = ok ? (unsigned)(row[o] >> sh) : 0u;
+                unsigned m = __ballot_sync(0xffffffffu, ok);
+#pragma unroll
+                for (int bit = 0; bit < 5; bit++)
+                    m &= ~(__ballot_sync(0xffffffffu, (b >> bit) & 1u) ^ ~lm[bit]);
+                cntb += __popc(m);
+            }
+        }
+        if (cntb) atomicAdd(&hist[lane], cntb);
+    }
+    __syncthreads();
+    if (wid == 0) {
+        const int row = seed_row(g0);
+        const int tgt = target_at2(g, p, tc, row, cs);
+        const int tot = hist[lane];
+        int cum = tot;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, cum, o);
+            if (lane >= o) cum += v;
+        }
+        const int B = __ffs(__ballot_sync(0xffffffffu, cum > tgt)) - 1;
+        const int cnt = __shfl_sync(0xffffffffu, cum - tot, B);
+        const int m = refine_warp2<CIRCLE>(c, cs + r, row + r, B << sh, cnt, tgt);
+        if (lane == 0) {
+            if (m < 0) atomicOr(p.status, 1);
+            seedP[g0] = max(m, 0);
+            seedC[g0] = tgt;
+        }
+    }
+    __syncthreads();
+
+    // ---- B. other seed rows' centre windows: vertical deltas at column cs --
+    const int ytop = seed_row(0), ybot = seed_row(G - 1);
+    if (G > 1) {
+        const int P0 = seedP[g0];
+        const uint32_t K0 = pivot_k(P0, P0);
+        for (int y = ytop + tid; y < ybot; y += blockDim.x) {  // step y -> y+1 at column cs
+            uint32_t gi_, go_;
+            vcount(I_a + 2 * (y * Sw + cs), kt.v, p.nv_even, p.nv, K0, gi_, go_);
+            deltas[y] = (int)(go_ & 0xffffu) - (int)(gi_ & 0xffffu);
+        }
+        __syncthreads();
+        for (int gi = wid; gi < G; gi += nwarps) {
+            if (gi == g0) continue;
+            const int y0 = seed_row(g0), y1 = seed_row(gi);
+            int part = 0;
+            if (y1 > y0) {
+                for (int y = y0 + lane; y < y1; y += 32) part += deltas[y];
+            } else {
+                for (int y = y1 + lane; y < y0; y += 32) part -= deltas[y];
+            }
+            const int cnt = seedC[g0] + (int)__reduce_add_sync(0xffffffffu, (unsigned)part);
+            const int tgt = target_at2(g, p, tc, y1, cs);
+            const int m = refine_warp2<CIRCLE>(c, cs + r, y1 + r, P0, cnt, tgt);
+            if (lane == 0) {
+                if (m < 0) atomicOr(p.status, 1);
+                seedP[gi] = max(m, 0);
+                seedC[gi] = tgt;
+            }
+        }
+        __syncthreads();
+    }
+
+    // ---- C. seed rows: horizontal deltas (pairs of steps) at the row pivot --
+    for (int u = tid; u < G * TH; u += blockDim.x) {  // steps 2q -> 2q+1, 2q+1 -> 2q+2 of row gi
+        const int gi = u / TH, q = u - gi * TH;
+        const int P = seedP[gi];
+        const uint32_t K = pivot_k(P, P);
+        const uint32_t b = I_a + 2 * (seed_row(gi) * Sw + 2 * q);
+        const uint32_t ge_in = hcount(b, kt.he, p.nhe_even, p.nh, K);
+        const uint32_t ge_out = hcount(b, kt.hx, p.nhx_even, p.nh, K);
+        int d0, d1;
+        half_diff(ge_out, ge_in, d0, d1);
+        deltas[gi * T + 2 * q] = d0;
+        deltas[gi * T + 2 * q + 1] = d1;
+    }
+    __syncthreads();
+    for (int u = tid; u < G * T; u += blockDim.x) {
+        const int gi = u / T, j = u - gi * T, row = seed_row(gi);
+        const int P = seedP[gi];
+        int cnt = seedC[gi];
+        if (j > cs) {
+            for (int i = cs; i < j; i++) cnt += deltas[gi * T + i];
+        } else {
+            for (int i = j; i < cs; i++) cnt -= deltas[gi * T + i];
+        }
+        const int tgt = target_at2(g, p, tc, row, j);
+        int m = (j == cs) ? P : refine8<CIRCLE>(c, j + r, row + r, P, cnt, tgt);
+        if (m < 0) {
+            atomicOr(p.status, 1);
+            m = 0;
+        }
+        st_P[u] = m;
+        st_C[u] = tgt;
+    }
+    __syncthreads();
+
+    // ---- D'. vertical sweeps, four windows per thread: thread = (group,
+    // column pair) slides its down pair and its up pair in lockstep (shared
+    // offset fetches, four independent accumulation chains) and refines all
+    // four in one loop.
+    if (p.quad) {
+        for (int u = tid; u < G * TH; u += blockDim.x) {
+            const int q = u % TH, gi = u / TH;
+            const int row0 = seed_row(gi);
+            const int rend = (gi == G - 1) ? T : (gi + 1) * R;
+            const int nd = rend - 1 - row0, nu = row0 - gi * R;
+            const int j0 = 2 * q;
+            int P4[4], C4[4], T4[4], M4[4];
+            P4[0] = P4[2] = st_P[gi * T + j0];
+            P4[1] = P4[3] = st_P[gi * T + j0 + 1];
+            C4[0] = C4[2] = st_C[gi * T + j0];
+            C4[1] = C4[3] = st_C[gi * T + j0 + 1];
+            Pend w4[4];
+            w4[0] = gather_out(g, tc, om, P4[0], row0, j0);
+            w4[1] = gather_out(g, tc, om, P4[1], row0, j0 + 1);
+            w4[2].ok = w4[3].ok = false;
+            int rd = row0, ru = row0;
+            const int ns = max(nd, nu);
+            for (int s = 0; s < ns; s++) {
+                const bool dd = s < nd, du = s < nu;
+                uint32_t d_in = 0, d_out = 0, u_in = 0, u_out = 0;
+                const uint32_t Kd = pivot_k(P4[0], P4[1]), Ku = pivot_k(P4[2], P4[3]);
+                if (dd && du) {
+                    vcount_du(I_a + 2 * (rd * Sw + j0), I_a + 2 * ((ru - 1) * Sw + j0), kt.v, p.nv_even, p.nv, Kd,
+                              Ku, d_in, d_out, u_in, u_out);
+                } else if (dd) {
+                    vcount(I_a + 2 * (rd * Sw + j0), kt.v, p.nv_even, p.nv, Kd, d_in, d_out);
+                } else {
+                    vcount(I_a + 2 * ((ru - 1) * Sw + j0), kt.v, p.nv_even, p.nv, Ku, u_in, u_out);
+                }
+#pragma unroll
+                for (int i = 0; i < 4; i++) store_out(g, w4[i]);
+                int dA, dB;
+                if (dd) {
+                    half_diff(d_out, d_in, dA, dB);
+                    C4[0] += dA;
+                    C4[1] += dB;
+                    rd++;
+                }
+                if (du) {
+                    half_diff(u_in, u_out, dA, dB);
+                    C4[2] += dA;
+                    C4[3] += dB;
+                    ru--;
+                }
+                T4[0] = target_at2(g, p, tc, rd, j0);
+                T4[1] = target_at2(g, p, tc, rd, j0 + 1);
+                T4[2] = target_at2(g, p, tc, ru, j0);
+                T4[3] = target_at2(g, p, tc, ru, j0 + 1);
+                refine8x4<CIRCLE>(c, j0 + r, rd + r, ru + r, P4, C4, T4, dd ? 0 : 2, du ? 4 : 2, M4);
+                if ((M4[0] | M4[1] | M4[2] | M4[3]) < 0) atomicOr(p.status, 1);
+#pragma unroll
+                for (int i = 0; i < 4; i++) {
+                    const bool act = (i < 2) ? dd : du;
+                    w4[i].ok = false;
+                    if (act) {
+                        const int m = max(M4[i], 0);
+                        w4[i] = gather_out(g, tc, om, m, (i < 2) ? rd : ru, j0 + (i & 1));
+                        P4[i] = m;
+                        C4[i] = T4[i];
+                    }
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < 4; i++) store_out(g, w4[i]);
+        }
+        return;
+    }
+
+    // ---- D. vertical sweeps: thread = (direction, group, column pair) ------
+    for (int u = tid; u < 2 * G * TH; u += blockDim.x) {
+        const int q = u % TH, rest = u / TH, gi = rest % G;
+        const bool down = rest < G;
+        const int row0 = seed_row(gi);
+        const int rend = (gi == G - 1) ? T : (gi + 1) * R;  // exclusive
+        const int j0 = 2 * q, j1 = j0 + 1;
+        int PA = st_P[gi * T + j0], cA = st_C[gi * T + j0];
+        int PB = st_P[gi * T + j1], cB = st_C[gi * T + j1];
+        Pend wa{0, 0, false}, wb{0, 0, false};
+        if (down) {
+            wa = gather_out(g, tc, om, PA, row0, j0);
+            wb = gather_out(g, tc, om, PB, row0, j1);
+        }
+        const int nsteps = down ? (rend - 1 - row0) : (row0 - gi * R);
+        int row = row0;
+        for (int s = 0; s < nsteps; s++) {
+            const uint32_t K = pivot_k(PA, PB);
+            uint32_t ge_in, ge_out;
+            int dA, dB;
+            if (down) {
+                vcount(I_a + 2 * (row * Sw + j0), kt.v, p.nv_even, p.nv, K, ge_in, ge_out);
+                half_diff(ge_out, ge_in, dA, dB);
+                row++;
+            } else {
+                vcount(I_a + 2 * ((row - 1) * Sw + j0), kt.v, p.nv_even, p.nv, K, ge_in, ge_out);
+                half_diff(ge_in, ge_out, dA, dB);
+                row--;
+            }
+            store_out(g, wa);
+            store_out(g, wb);
+            cA += dA;
+            cB += dB;
+            const int tA = target_at2(g, p, tc, row, j0);
+            const int tB = target_at2(g, p, tc, row, j1);
+            int mA, mB;
+            refine8x2<CIRCLE>(c, j0 + r, row + r, PA, cA, tA, PB, cB, tB, mA, mB);
+            if ((mA | mB) < 0) {
+                atomicOr(p.status, 1);
+                mA = max(mA, 0);
+                mB = max(mB, 0);
+            }
+            wa = gather_out(g, tc, om, mA, row, j0);
+            wb = gather_out(g, tc, om, mB, row, j1);
+            PA = mA;
+            cA = tA;
+            PB = mB;
+            cB = tB;
+        }
+        store_out(g, wa);
+        store_out(g, wb);
+    }
+}
+
+template __global__ void k2_pair<true>(Geom, PairParams, const __grid_constant__ PairTab, const uint16_t*);
+template __global__ void k2_pair<false>(Geom, PairParams, const __grid_constant__ PairTab, const uint16_t*);
+
+size_t k2_pair_smem_bytes(int N, int Npad, int r, int G, int T) {
+    const int Ipad = (N + 15) & ~7;
+    const int gt = G * T;
+    return 2 * (size_t)(Npad + 16) + 2 * (size_t)Ipad +
+           4 * (size_t)(2 * gt + (gt > T ? gt : T) + 32 + 2 * G + 2 * r + 1) + 16;
+}
+
+// Host: build the pair tables for input-tile row stride Sw.  Returns false if
+// an offset list would overflow PT_MAX.
+bool build_pair_tab(const int* row_dy, const int* row_xlo, const int* row_xhi, int nrows, const int* col_dx,
+                    const int* col_ytop, const int* col_ybot, int ncols, int r, int Sw, PairTab& t,
+                    PairParams& p) {
+    if (ncols > PT_MAX || nrows > PT_MAX) return false;
+    memset(&t, 0, sizeof(t));
+    // element offset of a pixel relative to the pair base (row*Sw + 2q): (r + dy)*Sw + r + dx
+    auto put_v = [&](int k, int e, int x, bool odd) {
+        t.v[k] = odd ? make_int2(2 * (e - 1), 2 * (x - 1)) : make_int2(2 * e, 2 * x);
+    };
+    int k = 0;
+    for (int pass = 0; pass < 2; pass++) {
+        for (int i = 0; i < ncols; i++) {
+            const int e = (r + col_ybot[i] + 1) * Sw + r + col_dx[i];
+            const int x = (r + col_ytop[i]) * Sw + r + col_dx[i];
+            const bool odd = (e & 1) != 0;  // e and x share the parity of r + dx (Sw even)
+            if (odd == (pass == 1)) put_v(k++, e, x, odd);
+        }
+        if (pass == 0) p.nv_even = k;
+    }
+    p.nv = ncols;
+    auto fill_h = [&](int* dst, bool hi, int& ne) {
+        int kk = 0;
+        for (int pass = 0; pass < 2; pass++) {
+            for (int i = 0; i < nrows; i++) {
+                const int o = (r + row_dy[i]) * Sw + r + (hi ? row_xhi[i] : row_xlo[i]);
+                const bool odd = (o & 1) != 0;
+                if (odd == (pass == 1)) dst[kk++] = odd ? 2 * (o - 1) : 2 * o;
+            }
+            if (pass == 0) ne = kk;
+        }
+    };
+    fill_h(t.he, true, p.nhe_even);
+    fill_h(t.hx, false, p.nhx_even);
+    p.nh = nrows;
+    return true;
+}
+
+}  // namespace imf
