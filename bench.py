@@ -292,10 +292,12 @@ def run_ours(args):
     # ---- end-to-end through the public call with host buffers ---------------
     e2e = None
     if not args.no_e2e:
+        from paper_2505_22938_b200.tiling import run_host
+
         def e2e_step():
-            src.copy_(host_pin, non_blocking=True)
-            run_device(src, params, out=out, batched=True, check=False, kernel=kernel)
-            out_pin.copy_(out, non_blocking=True)
+            # public C-ABI host entry (imf_filter_host): pinned host in -> pinned host out,
+            # row stripes pipelined over upload / filter / download streams
+            run_host(host_pin, params, out=out_pin, batched=True, kernel=kernel)
         for _ in range(args.warmup):
             e2e_step()
         barrier()

@@ -82,8 +82,14 @@ typedef struct imf_options {
     int32_t tile_size;     /* output tile side; 0 = auto.  Output-neutral (tiling.py:110-119) */
     int32_t seed_rows;     /* seed rows per tile; 0 = auto (tuning knob, output-neutral) */
     int32_t seeds_per_row; /* direct seeds per seed row; 0 = auto */
-    int32_t reserved[4];
+    int32_t flags;         /* IMF_FLAG_* */
+    int32_t row_begin;     /* output stripe [row_begin, row_end) of every plane; */
+    int32_t row_end;       /*   row_end == 0 = all output rows (SURVEY 8(b) sketch) */
+    int32_t reserved;
 } imf_options;
+
+#define IMF_FLAG_PROFILE 1      /* per-kernel CUDA-event timing, see imf_profile_last */
+#define IMF_FLAG_KEEP_STATUS 2  /* do not clear the workspace status word (stripe 2..n of one job) */
 
 /* Bytes of device workspace imf_filter needs for this problem. */
 size_t imf_workspace_size(const imf_image* src, const imf_kernel* kernel, const imf_options* opt);
@@ -107,9 +113,12 @@ int imf_workspace_status(void* workspace, void* stream);
 
 /*
  * Synchronous host-memory variant for FFI callers (cgo / JNI / ctypes): copies
- * src to the current device, filters, copies the result back to dst.  Device
- * buffers come from the stream-ordered pool (cudaMallocAsync).  Host buffers
- * should be pinned for full copy bandwidth.
+ * src to the current device, filters, copies the result back to dst.  Images
+ * whose rows are outermost within each plane group (HW, HWC, NHWC) are
+ * pipelined in output-row stripes: the upload of stripe i+1, the filter of
+ * stripe i and the download of stripe i-1 run concurrently (three streams,
+ * event-ordered).  Device buffers come from the stream-ordered pool
+ * (cudaMallocAsync).  Host buffers should be pinned for full copy bandwidth.
  */
 int imf_filter_host(const imf_image* src, imf_image* dst, const imf_kernel* kernel, int32_t target,
                     const int32_t* target_map, int32_t tmin, int32_t tmax, const imf_options* opt,
@@ -121,7 +130,7 @@ const char* imf_last_error(void);       /* detail of the last IMF_ERR_CUDA on th
 uint64_t imf_launch_count(void);        /* kernels launched by this process (diagnostic) */
 
 /* Per-kernel device time of the last imf_filter on this thread that ran with
- * opt->reserved[0] & 1 (events on its stream; that call synchronizes). */
+ * opt->flags & IMF_FLAG_PROFILE (events on its stream; that call synchronizes). */
 int imf_profile_last(float* sort_ms, float* select_ms, int32_t* launches, int64_t* tiles,
                      int32_t* tile_side, int32_t* qshift);
 

@@ -49,7 +49,10 @@ class ImfImage(ctypes.Structure):
 class ImfOptions(ctypes.Structure):
     _fields_ = [("boundary", ctypes.c_int32), ("tile_size", ctypes.c_int32),
                 ("seed_rows", ctypes.c_int32), ("seeds_per_row", ctypes.c_int32),
-                ("reserved", ctypes.c_int32 * 4)]
+                ("flags", ctypes.c_int32), ("row_begin", ctypes.c_int32),
+                ("row_end", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+
+IMF_FLAG_PROFILE = 1
 
 
 _lock = threading.Lock()

@@ -42,6 +42,7 @@ struct Plan {
     Geom g;
     int G, k2_threads, k1_threads, paired;
     bool k1_gmem, k1_count, omg;
+    int full_out_h;
     bool pair;  // K2 fast path (imf_pair.cu): two windows per thread, 15-bit ranks
     size_t k1_smem, k2_smem, k1_gs_per_tile;
     long long total_tiles, chunk_tiles;
@@ -72,6 +73,9 @@ int make_plan(const imf_image* src, const imf_kernel* k, const imf_options* opt,
     const int valid = opt->boundary == IMF_BOUNDARY_VALID;
     const int out_h = valid ? H - 2 * r : H, out_w = valid ? W - 2 * r : W;
     if (out_h < 1 || out_w < 1) return IMF_ERR_INVALID;
+    const int row0 = opt->row_end > 0 ? opt->row_begin : 0;
+    const int row1 = opt->row_end > 0 ? opt->row_end : out_h;
+    if (row0 < 0 || row1 > out_h || row0 >= row1) return IMF_ERR_INVALID;
 
     Plan& p = *pl;
     memset(&p, 0, sizeof(p));
@@ -89,7 +93,7 @@ int make_plan(const imf_image* src, const imf_kernel* k, const imf_options* opt,
         if (T >= 2) {
             const int S = T + 2 * r, N = S * S, Npad = (N + 63) & ~63;
             int G = std::max(1, std::min(opt->seed_rows > 0 ? opt->seed_rows : env_int("IMF_SEED_ROWS", 8), T));
-            const int quad = env_int("IMF_QUAD", 1);
+            const int quad = env_int("IMF_QUAD", 0);
             const int tpg = quad ? T / 2 : T;  // threads per seed-row group
             while (G > 1 && ((G * tpg + 31) & ~31) > 512) G--;
             const size_t ks = k2_pair_smem_bytes(N, Npad, r, G, T);
@@ -144,12 +148,14 @@ int make_plan(const imf_image* src, const imf_kernel* k, const imf_options* opt,
     g.s_y = src->stride_y;
     g.s_x = src->stride_x;
     g.s_c = src->stride_c;
-    g.out_h = out_h;
+    g.out_h = row1;
+    g.oy_base = row0;
     g.out_w = out_w;
     g.vshift = valid ? r : 0;
     g.r = r;
     g.tiles_x = (out_w + g.Tw - 1) / g.Tw;
-    g.tiles_y = (out_h + g.Th - 1) / g.Th;
+    g.tiles_y = (row1 - row0 + g.Th - 1) / g.Th;
+    p.full_out_h = out_h;
     p.total_tiles = (long long)g.tiles_x * g.tiles_y * g.C * g.B;
 
     p.k1_count = g.dtype != DT_F32 && k1_count_smem_bytes(g.dtype, g.Npad) <= kSmemMax;
@@ -282,7 +288,7 @@ int imf_filter(const imf_image* src, imf_image* dst, const imf_kernel* kernel, i
     Plan p;
     int st = make_plan(src, kernel, opt, &p);
     if (st) return st;
-    if (dst->height != p.g.out_h || dst->width != p.g.out_w) return IMF_ERR_INVALID;
+    if (dst->height != p.full_out_h || dst->width != p.g.out_w) return IMF_ERR_INVALID;
     if (!workspace || workspace_bytes < p.ws_total) return IMF_ERR_WORKSPACE;
     cudaStream_t s = (cudaStream_t)stream;
     if (cudaError_t e = set_attrs()) return cuda_fail(e, "cudaFuncSetAttribute");
@@ -293,13 +299,10 @@ int imf_filter(const imf_image* src, imf_image* dst, const imf_kernel* kernel, i
     uint16_t* omega = (uint16_t*)(ws + kStatusBytes + p.ws_ktab);
     unsigned char* k1g = ws + kStatusBytes + p.ws_ktab + p.ws_omega;
 
-    std::vector<int> ktab;
-    build_ktab(kernel, p.g.Sw, ktab);
     static thread_local KTab kt;
     build_ktab_struct(kernel, p.g.Sw, kt);
-    if (cudaError_t e = cudaMemsetAsync(status, 0, sizeof(int), s)) return cuda_fail(e, "status memset");
-    if (cudaError_t e = cudaMemcpyAsync(ktab_d, ktab.data(), ktab.size() * 4, cudaMemcpyHostToDevice, s))
-        return cuda_fail(e, "kernel table upload");
+    if (!(opt->flags & IMF_FLAG_KEEP_STATUS))
+        if (cudaError_t e = cudaMemsetAsync(status, 0, sizeof(int), s)) return cuda_fail(e, "status memset");
 
     Geom g = p.g;
     g.src = src->data;
@@ -336,14 +339,13 @@ int imf_filter(const imf_image* src, imf_image* dst, const imf_kernel* kernel, i
         pp.tmap = target_map;
         pp.G = p.G;
         pp.quad = p.paired;
-        pp.span = ktab_d + 2 * kernel->ncols + 2 * kernel->nrows;
         pp.status = status;
     }
 
     // Optional per-kernel timing (opt->reserved[0] & 1): CUDA events recorded on
     // `stream` around every launch; the call then synchronizes and leaves the
     // sums in imf_profile_last().  Used by bench.py for the roofline figure.
-    const bool prof = (opt->reserved[0] & 1) != 0;
+    const bool prof = (opt->flags & IMF_FLAG_PROFILE) != 0;
     std::vector<cudaEvent_t> ev;
     for (long long t0 = 0; t0 < p.total_tiles; t0 += p.chunk_tiles) {
         const int nb = (int)std::min(p.chunk_tiles, p.total_tiles - t0);
@@ -428,39 +430,146 @@ static size_t extent_bytes(const imf_image* im) {
     return (size_t)(last + 1) * dtype_size(im->dtype);
 }
 
+// Rows are outermost within an image (HW / HWC / NHWC): rows [a, b) of image
+// bi are the contiguous element range [bi*s_b + a*s_y, bi*s_b + b*s_y).
+static bool rows_outermost(const imf_image* im) {
+    const long long row = (long long)(im->width - 1) * im->stride_x + (long long)(im->channels - 1) * im->stride_c + 1;
+    return im->stride_x >= 0 && im->stride_c >= 0 && im->stride_y >= row &&
+           (im->batch == 1 || im->stride_b >= (long long)im->height * im->stride_y);
+}
+
+namespace {
+struct HostStreams {
+    cudaStream_t up = nullptr, down = nullptr;
+    int dev = -1;
+};
+thread_local HostStreams g_hs;
+}  // namespace
+
 int imf_filter_host(const imf_image* src, imf_image* dst, const imf_kernel* kernel, int32_t target,
                     const int32_t* target_map, int32_t tmin, int32_t tmax, const imf_options* opt,
                     void* stream) {
-    if (!src || !dst || !kernel || !opt) return IMF_ERR_INVALID;
+    if (!src || !dst || !kernel || !opt || !src->data || !dst->data) return IMF_ERR_INVALID;
     cudaStream_t s = (cudaStream_t)stream;
     if (!target_map) tmin = tmax = target;
     Plan p;
     int st = make_plan(src, kernel, opt, &p);
     if (st) return st;
+    const int dsz = dtype_size(src->dtype);
     const size_t sb = extent_bytes(src), db = extent_bytes(dst);
-    const size_t tb = target_map ? (size_t)p.g.out_h * p.g.out_w * 4 : 0;
+    const size_t tb = target_map ? (size_t)p.full_out_h * p.g.out_w * 4 : 0;
+    int dev = 0;
+    if (cudaGetDevice(&dev)) return IMF_ERR_CUDA;
+    if (g_hs.dev != dev) {
+        if (g_hs.up) cudaStreamDestroy(g_hs.up);
+        if (g_hs.down) cudaStreamDestroy(g_hs.down);
+        if (cudaStreamCreateWithFlags(&g_hs.up, cudaStreamNonBlocking) ||
+            cudaStreamCreateWithFlags(&g_hs.down, cudaStreamNonBlocking))
+            return cuda_fail(cudaGetLastError(), "stream create");
+        // keep freed pool memory cached across calls (default threshold 0 returns
+        // it to the driver at every synchronization)
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t thr = 4ull << 30;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+        g_hs.dev = dev;
+    }
     void *dsrc = nullptr, *ddst = nullptr, *dws = nullptr, *dtm = nullptr;
+    std::vector<cudaEvent_t> evs;
+    auto event = [&]() {
+        cudaEvent_t e = nullptr;
+        cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+        evs.push_back(e);
+        return e;
+    };
     int rc = IMF_OK;
-    if (cudaMallocAsync(&dsrc, sb, s) || cudaMallocAsync(&ddst, db, s) ||
-        cudaMallocAsync(&dws, p.ws_total, s) || (tb && cudaMallocAsync(&dtm, tb, s))) {
-        rc = IMF_ERR_CUDA;
-    }
-    if (!rc && cudaMemcpyAsync(dsrc, src->data, sb, cudaMemcpyHostToDevice, s)) rc = IMF_ERR_CUDA;
-    if (!rc && tb && cudaMemcpyAsync(dtm, target_map, tb, cudaMemcpyHostToDevice, s)) rc = IMF_ERR_CUDA;
+    if (cudaMallocAsync(&dsrc, sb, s) || cudaMallocAsync(&ddst, db, s) || cudaMallocAsync(&dws, p.ws_total, s) ||
+        (tb && cudaMallocAsync(&dtm, tb, s)))
+        rc = cuda_fail(cudaGetLastError(), "cudaMallocAsync");
+    if (!rc && tb && cudaMemcpyAsync(dtm, target_map, tb, cudaMemcpyHostToDevice, s))
+        rc = cuda_fail(cudaGetLastError(), "target map upload");
+    cudaEvent_t e_alloc = event();
+    if (!rc) cudaEventRecord(e_alloc, s);
+    imf_image ds = *src, dd = *dst;
+    ds.data = dsrc;
+    dd.data = ddst;
+    const int r = kernel->radius, vshift = opt->boundary == IMF_BOUNDARY_VALID ? r : 0;
+    const int H = src->height, OH = p.full_out_h;
+    const bool pipe = rows_outermost(src) && rows_outermost(dst) && OH > 2 * p.g.Th;
+    // stripes of whole tile rows, about eight per image
+    const int tiles_y = (OH + p.g.Th - 1) / p.g.Th;
+    const int stripe = pipe ? p.g.Th * std::max(1, (tiles_y + 7) / 8) : OH;
     if (!rc) {
-        imf_image ds = *src, dd = *dst;
-        ds.data = dsrc;
-        dd.data = ddst;
-        rc = imf_filter(&ds, &dd, kernel, target, (const int32_t*)dtm, tmin, tmax, opt, dws, p.ws_total,
-                        stream);
+        cudaStreamWaitEvent(g_hs.up, e_alloc, 0);
+        for (int bi = 0; bi < src->batch && !rc; bi++) {
+            const long long sbase = (long long)bi * src->stride_b, dbase = (long long)bi * dst->stride_b;
+            int up_hi = 0;  // input rows [0, up_hi) of image bi are uploaded
+            for (int y0 = 0; y0 < OH && !rc; y0 += stripe) {
+                const int y1 = std::min(OH, y0 + stripe);
+                if (pipe) {
+                    const int need = std::min(H, y1 - 1 + r + vshift + 1);
+                    if (need > up_hi) {
+                        const size_t off = (size_t)(sbase + (long long)up_hi * src->stride_y) * dsz;
+                        const size_t len = (size_t)((long long)(need - up_hi) * src->stride_y) * dsz;
+                        const size_t cap = sb - off;
+                        if (cudaMemcpyAsync((char*)dsrc + off, (const char*)src->data + off, std::min(len, cap),
+                                            cudaMemcpyHostToDevice, g_hs.up))
+                            rc = cuda_fail(cudaGetLastError(), "stripe upload");
+                        up_hi = need;
+                    }
+                } else if (bi == 0 && y0 == 0) {
+                    if (cudaMemcpyAsync(dsrc, src->data, sb, cudaMemcpyHostToDevice, g_hs.up))
+                        rc = cuda_fail(cudaGetLastError(), "upload");
+                }
+                cudaEvent_t e_up = event();
+                cudaEventRecord(e_up, g_hs.up);
+                cudaStreamWaitEvent(s, e_up, 0);
+                imf_options o = *opt;
+                o.flags &= ~IMF_FLAG_PROFILE;
+                if (bi > 0 || y0 > 0) o.flags |= IMF_FLAG_KEEP_STATUS;  // defects of earlier stripes persist
+                o.row_begin = y0;
+                o.row_end = y1;
+                imf_image dsi = ds, ddi = dd;
+                if (pipe) {  // one image of the batch per launch sequence
+                    dsi.data = (char*)dsrc + (size_t)sbase * dsz;
+                    ddi.data = (char*)ddst + (size_t)dbase * dsz;
+                    dsi.batch = ddi.batch = 1;
+                } else {
+                    o.row_begin = o.row_end = 0;
+                }
+                if (!rc)
+                    rc = imf_filter(&dsi, &ddi, kernel, target, (const int32_t*)dtm, tmin, tmax, &o, dws,
+                                    p.ws_total, s);
+                cudaEvent_t e_done = event();
+                cudaEventRecord(e_done, s);
+                cudaStreamWaitEvent(g_hs.down, e_done, 0);
+                if (!rc) {
+                    if (pipe) {
+                        const size_t off = (size_t)(dbase + (long long)y0 * dst->stride_y) * dsz;
+                        const size_t len = std::min((size_t)((long long)(y1 - y0) * dst->stride_y) * dsz, db - off);
+                        if (cudaMemcpyAsync((char*)dst->data + off, (char*)ddst + off, len, cudaMemcpyDeviceToHost,
+                                            g_hs.down))
+                            rc = cuda_fail(cudaGetLastError(), "stripe download");
+                    } else if (cudaMemcpyAsync(dst->data, ddst, db, cudaMemcpyDeviceToHost, g_hs.down)) {
+                        rc = cuda_fail(cudaGetLastError(), "download");
+                    }
+                }
+                if (!pipe) break;
+            }
+            if (!pipe) break;
+        }
     }
-    if (!rc && cudaMemcpyAsync(dst->data, ddst, db, cudaMemcpyDeviceToHost, s)) rc = IMF_ERR_CUDA;
-    if (!rc) rc = imf_workspace_status(dws, stream);
+    cudaEvent_t e_end = event();
+    cudaEventRecord(e_end, g_hs.down);
+    cudaStreamWaitEvent(s, e_end, 0);
+    if (!rc) rc = imf_workspace_status(dws, stream);  // synchronizes s
     if (dsrc) cudaFreeAsync(dsrc, s);
     if (ddst) cudaFreeAsync(ddst, s);
     if (dws) cudaFreeAsync(dws, s);
     if (dtm) cudaFreeAsync(dtm, s);
     cudaStreamSynchronize(s);
+    for (cudaEvent_t e : evs) cudaEventDestroy(e);
     return rc;
 }
 

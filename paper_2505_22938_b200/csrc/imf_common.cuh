@@ -29,7 +29,8 @@ struct Geom {
     int B, H, W, C;
     long long s_b, s_y, s_x, s_c;  // source strides, elements
     long long d_b, d_y, d_x, d_c;  // destination strides, elements
-    int out_h, out_w;
+    int out_h, out_w;              // out_h: exclusive end of the output rows this launch writes
+    int oy_base;                   // first output row of this launch (row stripe)
     int vshift;                    // r in valid mode, 0 in replicate mode
     int r;
     int Tw, Th, Sw, Sh, N, Npad;   // Npad: N rounded up to a multiple of 64
@@ -71,7 +72,7 @@ __device__ __forceinline__ TileCoord tile_coord(const Geom& g, long long t) {
     tc.ty = (int)(t % g.tiles_y); t /= g.tiles_y;
     tc.c = (int)(t % g.C); t /= g.C;
     tc.b = (int)t;
-    tc.oy0 = tc.ty * g.Th;
+    tc.oy0 = g.oy_base + tc.ty * g.Th;
     tc.ox0 = tc.tx * g.Tw;
     int esz = g.dtype == DT_U8 ? 1 : (g.dtype == DT_U16 ? 2 : 4);
     tc.src = (const char*)g.src + (tc.b * g.s_b + tc.c * g.s_c) * esz;

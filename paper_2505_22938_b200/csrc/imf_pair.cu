@@ -42,6 +42,7 @@ struct PairTab {
     int2 v[PT_MAX];  // per kernel column: (enter, exit) of a down slide
     int he[PT_MAX];  // per kernel row: pixel entering on a right slide
     int hx[PT_MAX];  // per kernel row: pixel exiting on a right slide
+    int span[PT_MAX];  // per dy + r: (xlo & 0xffff) | width << 16 (kernels.py:127-182 rows)
 };
 
 struct PairParams {
@@ -53,7 +54,6 @@ struct PairParams {
     const int* tmap;
     int G;
     int quad;         // phase D with four windows per thread
-    const int* span;  // 2r+1 packed (xlo & 0xffff) | width << 16, device copy
     int* status;
 };
 
@@ -504,7 +504,7 @@ __global__ void __launch_bounds__(512) k2_pair(Geom g, PairParams p, const __gri
         }
         for (int i = N + tid; i < Ipad; i += blockDim.x) I[i] = 0;
         if (tid < 32) hist[tid] = 0;
-        for (int i = tid; i < 2 * r + 1; i += blockDim.x) span_s[i] = __ldg(p.span + i);
+        for (int i = tid; i < 2 * r + 1; i += blockDim.x) span_s[i] = kt.span[i];
     }
     __syncthreads();
 
@@ -771,7 +771,7 @@ size_t k2_pair_smem_bytes(int N, int Npad, int r, int G, int T) {
 bool build_pair_tab(const int* row_dy, const int* row_xlo, const int* row_xhi, int nrows, const int* col_dx,
                     const int* col_ytop, const int* col_ybot, int ncols, int r, int Sw, PairTab& t,
                     PairParams& p) {
-    if (ncols > PT_MAX || nrows > PT_MAX) return false;
+    if (ncols > PT_MAX || nrows > PT_MAX || 2 * r + 1 > PT_MAX) return false;
     memset(&t, 0, sizeof(t));
     // element offset of a pixel relative to the pair base (row*Sw + 2q): (r + dy)*Sw + r + dx
     auto put_v = [&](int k, int e, int x, bool odd) {
@@ -802,6 +802,8 @@ bool build_pair_tab(const int* row_dy, const int* row_xlo, const int* row_xhi, i
     fill_h(t.he, true, p.nhe_even);
     fill_h(t.hx, false, p.nhx_even);
     p.nh = nrows;
+    for (int i = 0; i < nrows; i++)
+        t.span[row_dy[i] + r] = (row_xlo[i] & 0xffff) | ((row_xhi[i] - row_xlo[i]) << 16);
     return true;
 }
 

@@ -152,8 +152,11 @@ def _check_dtype(dt):
         raise ValueError(f"unsupported image dtype {dt}; use uint8, uint16, or float32")
 
 
-def _target_spec(area: int, percentile, out_shape, device):
-    """(scalar target, device target map or None, tmin, tmax) -- tiling.py:165-177."""
+def _target_spec(area: int, percentile, out_shape, device, host: bool = False):
+    """(scalar target, target map or None, tmin, tmax) -- tiling.py:165-177.
+
+    The map is an int32 CUDA tensor on `device`, or a contiguous int32 numpy
+    array when `host` is set (for imf_filter_host)."""
     if np.isscalar(percentile) or np.ndim(percentile) == 0:
         t = target_rank(area, float(percentile))
         return t, None, t, t
@@ -168,6 +171,8 @@ def _target_spec(area: int, percentile, out_shape, device):
     if pmap.min() < 0.0 or pmap.max() > 1.0:
         raise ValueError("percentile map values must lie in [0, 1]")
     targets = np.clip(np.floor(pmap * (area - 1) + 0.5).astype(np.int64), 0, area - 1)
+    if host:
+        return 0, np.ascontiguousarray(targets, dtype=np.int32), int(targets.min()), int(targets.max())
     torch = _torch()
     tmap = torch.from_numpy(targets.astype(np.int32)).to(device)
     return 0, tmap, int(targets.min()), int(targets.max())
@@ -254,7 +259,7 @@ def run_device(src, params: FilterParams, out=None, *, batched: bool = False, st
     dimg = _image_struct(out, dt_code, batched, has_c)
     opt = _lib.ImfOptions(1 if valid else 0, int(params.tile_size or 0), 0, 0)
     if profile:
-        opt.reserved[0] = 1  # per-kernel CUDA-event timing (synchronizes)
+        opt.flags = _lib.IMF_FLAG_PROFILE  # per-kernel CUDA-event timing (synchronizes)
     need = L.imf_workspace_size(ctypes.byref(simg), ctypes.byref(ks), ctypes.byref(opt))
     if need == 0:
         raise ValueError("unsupported filter geometry for the CUDA engine")
@@ -329,10 +334,73 @@ def filter_image(image, params: FilterParams):
     if is_t and image.is_cuda:
         return run_device(image, params, kernel=kernel)
     if is_t:
-        src = image.to("cuda", non_blocking=False)
-        return run_device(src, params, kernel=kernel).cpu()
-    src = torch.from_numpy(np.ascontiguousarray(image)).to("cuda")
-    return run_device(src, params, kernel=kernel).cpu().numpy()
+        return torch.from_numpy(run_host(image.numpy(), params, kernel=kernel))
+    return run_host(image, params, kernel=kernel)
+
+
+def _host_image_struct(a: np.ndarray, dt_code: int, batched: bool):
+    """imf_image for a host array of shape ([B,] H, W[, C]) (strides in elements)."""
+    it = a.itemsize
+    shape, strides = list(a.shape), [st // it for st in a.strides]
+    has_c = a.ndim == (4 if batched else 3)
+    if not has_c:
+        shape.append(1)
+        strides.append(0)
+    if not batched:
+        shape.insert(0, 1)
+        strides.insert(0, 0)
+    b, h, w, c = shape
+    sb, sy, sx, sc = strides
+    return _lib.ImfImage(a.ctypes.data, dt_code, b, h, w, c, sb, sy, sx, sc)
+
+
+def run_host(image, params: FilterParams, out=None, *, batched: bool = False, kernel=None,
+             stream=None) -> np.ndarray:
+    """Filter a HOST array through the C-ABI host entry point (imf_filter_host).
+
+    The extension uploads, filters and downloads in output-row stripes on
+    three streams, so the copies of one stripe overlap the filter of another
+    (include/isomedian_b200.h).  `image` may be a numpy array or a CPU torch
+    tensor (pinned memory gives full copy bandwidth); the result is a numpy
+    array (or `out`, a host array/tensor of the output shape, filled in place).
+    """
+    torch = _torch()
+    L = _lib.lib()
+    a = image.numpy() if _is_tensor(image) else image
+    if a.dtype.byteorder not in ("=", "|") or any(st % a.itemsize for st in a.strides) or \
+            any(st < 0 for st in a.strides):
+        a = np.ascontiguousarray(a)
+    dt_code = _DTYPES[a.dtype]
+    kernel = kernel or make_kernel(params.shape)
+    r = params.shape.radius
+    valid = params.boundary == "valid"
+    hy = 1 if batched else 0
+    h, w = a.shape[hy], a.shape[hy + 1]
+    out_h, out_w = (h - 2 * r, w - 2 * r) if valid else (h, w)
+    if out is None:
+        oshape = list(a.shape)
+        oshape[hy], oshape[hy + 1] = out_h, out_w
+        o = np.empty(oshape, dtype=a.dtype)
+    else:
+        o = out.numpy() if _is_tensor(out) else out
+    target, tmap, tmin, tmax = _target_spec(kernel.area, params.percentile, (out_h, out_w), None,
+                                            host=True)
+    ks, keep = _kernel_struct(kernel)
+    simg = _host_image_struct(a, dt_code, batched)
+    dimg = _host_image_struct(o, dt_code, batched)
+    opt = _lib.ImfOptions(1 if valid else 0, int(params.tile_size or 0), 0, 0)
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    st = L.imf_filter_host(ctypes.byref(simg), ctypes.byref(dimg), ctypes.byref(ks), target,
+                           None if tmap is None else tmap.ctypes.data, tmin, tmax,
+                           ctypes.byref(opt), ctypes.c_void_p(stream.cuda_stream))
+    del keep
+    if st == _lib.IMF_ERR_DEFECT:
+        raise ScanDefectError("segment scan exhausted while solving tile; "
+                              "pivot/count state was inconsistent")
+    if st != _lib.IMF_OK:
+        raise RuntimeError(f"imf_filter_host failed: {_lib.strerror(st)}")
+    return out if out is not None else o
 
 
 def filter_batch(images, params: FilterParams, out=None, *, check: bool = True, stream=None):
