@@ -86,27 +86,36 @@ int make_plan(const imf_image* src, const imf_kernel* k, const imf_options* opt,
     double best = -1.0;
     // K2 fast path: tile ranks < 2^15 (S <= 181), even T, and T + r <= 128 for
     // the packed circle test.  Largest such tile.
-    if (env_int("IMF_PAIR", 1)) {
-        int T = std::min(Tmax, 181 - 2 * r);
-        if (k->shape_code == IMF_SHAPE_CIRCLE) T = std::min(T, 128 - r);
-        T &= ~1;
-        if (T >= 2) {
-            const int S = T + 2 * r, N = S * S, Npad = (N + 63) & ~63;
-            int G = std::max(1, std::min(opt->seed_rows > 0 ? opt->seed_rows : env_int("IMF_SEED_ROWS", 8), T));
-            const int quad = env_int("IMF_QUAD", 0);
-            const int tpg = quad ? T / 2 : T;  // threads per seed-row group
+    if (env_int("IMF_PAIR", 1) && (k->shape_code == IMF_SHAPE_CIRCLE || env_int("IMF_PAIR_ANY", 0))) {
+        // columns: even, <= Tmax, packed circle test needs Tw + r <= 128; rows: the
+        // tallest tile keeping N = Sw * Sh <= 32768 (ranks < 2^15), at most Tw
+        int Tw = std::min(Tmax, 255 - 2 * r);
+        if (k->shape_code == IMF_SHAPE_CIRCLE) Tw = std::min(Tw, 128 - r);
+        Tw &= ~1;
+        const int Sw = Tw + 2 * r;
+        int Th = std::min(Tw, 32768 / std::max(Sw, 1) - 2 * r);
+        if (k->shape_code == IMF_SHAPE_CIRCLE) Th = std::min(Th, 128 - r);
+        // rectangular tiles (Th < Tw) measured slower than the generic path
+        // (short sweeps, more seed rows per output row): square tiles only
+        if (Tw >= 2 && Th >= (env_int("IMF_PAIR_RECT", 0) ? std::max(2, Tw / 4) : Tw)) {
+            const int Sh = Th + 2 * r;
+            const int N = Sw * Sh, Npad = (N + 63) & ~63;
+            int G = std::max(1, std::min(opt->seed_rows > 0 ? opt->seed_rows : env_int("IMF_SEED_ROWS", 8), Th));
+            const int tpg = Tw;  // threads per seed-row group: (direction, column pair)
             while (G > 1 && ((G * tpg + 31) & ~31) > 512) G--;
-            const size_t ks = k2_pair_smem_bytes(N, Npad, r, G, T);
-            if (N <= 32768 && ((G * tpg + 31) & ~31) <= 512 && ks <= kSmemMax && k->ncols <= PT_MAX && k->nrows <= PT_MAX) {
+            const size_t ks = k2_pair_smem_bytes(N, Npad, r, G, Tw, Th);
+            if (N <= 32768 && ((G * tpg + 31) & ~31) <= 512 && ks <= kSmemMax && k->ncols <= PT_MAX &&
+                k->nrows <= PT_MAX) {
                 best = 1.0;
                 p.pair = true;
-                p.g.Tw = p.g.Th = T;
-                p.g.Sw = p.g.Sh = S;
+                p.g.Tw = Tw;
+                p.g.Th = Th;
+                p.g.Sw = Sw;
+                p.g.Sh = Sh;
                 p.g.N = N;
                 p.g.Npad = Npad;
                 p.G = G;
                 p.k2_threads = std::max((G * tpg + 31) & ~31, 64);  // whole warps (phase A/B ballots)
-                p.paired = quad;
                 p.k2_smem = ks;
                 p.omg = false;
             }
@@ -235,6 +244,16 @@ cudaError_t set_attrs() {
     if (!e) e = allow_smem(k1_sort<DT_F32, true>, optin);
     if (!e) e = allow_smem(k1_count<DT_U8>, optin);
     if (!e) e = allow_smem(k1_count<DT_U16>, optin);
+#define IMF_K1R_ATTR(DT)                                                          \
+    if (!e) e = allow_smem(k1_count_reg<DT, 1>, optin);                          \
+    if (!e) e = allow_smem(k1_count_reg<DT, 2>, optin);                          \
+    if (!e) e = allow_smem(k1_count_reg<DT, 3>, optin);                          \
+    if (!e) e = allow_smem(k1_count_reg<DT, 4>, optin);                          \
+    if (!e) e = allow_smem(k1_count_reg<DT, 5>, optin);                          \
+    if (!e) e = allow_smem(k1_count_reg<DT, 6>, optin);
+    IMF_K1R_ATTR(DT_U8)
+    IMF_K1R_ATTR(DT_U16)
+#undef IMF_K1R_ATTR
     if (!e) e = allow_smem(k2_select<true, false>, optin);
     if (!e) e = allow_smem(k2_select<false, false>, optin);
     if (!e) e = allow_smem(k2_select<true, true>, optin);
@@ -250,6 +269,25 @@ void launch_k1(const Plan& p, const Geom& g, int nblocks, uint16_t* omega, unsig
     const dim3 grid(nblocks), block(p.k1_threads);
     const long long gs = (long long)p.k1_gs_per_tile;
     if (p.k1_count) {
+        const int nk = (g.Sw + 31) >> 5;
+        if (nk <= 6 && env_int("IMF_K1REG", 1)) {
+#define IMF_K1R_LAUNCH(DT)                                                                       \
+    switch (nk) {                                                                                \
+        case 1: k1_count_reg<DT, 1><<<grid, block, p.k1_smem, s>>>(g, omega); break;             \
+        case 2: k1_count_reg<DT, 2><<<grid, block, p.k1_smem, s>>>(g, omega); break;             \
+        case 3: k1_count_reg<DT, 3><<<grid, block, p.k1_smem, s>>>(g, omega); break;             \
+        case 4: k1_count_reg<DT, 4><<<grid, block, p.k1_smem, s>>>(g, omega); break;             \
+        case 5: k1_count_reg<DT, 5><<<grid, block, p.k1_smem, s>>>(g, omega); break;             \
+        default: k1_count_reg<DT, 6><<<grid, block, p.k1_smem, s>>>(g, omega); break;            \
+    }
+            if (g.dtype == DT_U8) {
+                IMF_K1R_LAUNCH(DT_U8)
+            } else {
+                IMF_K1R_LAUNCH(DT_U16)
+            }
+#undef IMF_K1R_LAUNCH
+            return;
+        }
         if (g.dtype == DT_U8)
             k1_count<DT_U8><<<grid, block, p.k1_smem, s>>>(g, omega);
         else
@@ -338,7 +376,6 @@ int imf_filter(const imf_image* src, imf_image* dst, const imf_kernel* kernel, i
         pp.target = target;
         pp.tmap = target_map;
         pp.G = p.G;
-        pp.quad = p.paired;
         pp.status = status;
     }
 

@@ -53,7 +53,6 @@ struct PairParams {
     int target;
     const int* tmap;
     int G;
-    int quad;         // phase D with four windows per thread
     int* status;
 };
 
@@ -116,35 +115,6 @@ __device__ __forceinline__ void vcount(uint32_t b, const int2* __restrict__ v, i
     }
     ge_in = ai0 + ai1;
     ge_out = ao0 + ao1;
-}
-
-// vcount for a down slide at base bd (pivots Kd) and an up slide at base bu
-// (pivots Ku) through the same column list: four independent accumulators,
-// one constant-bank offset fetch per column for both.
-__device__ __forceinline__ void vcount_du(uint32_t bd, uint32_t bu, const int2* __restrict__ v, int ne, int n,
-                                          uint32_t Kd, uint32_t Ku, uint32_t& d_in, uint32_t& d_out,
-                                          uint32_t& u_in, uint32_t& u_out) {
-    uint32_t di = 0, dx = 0, ui = 0, ux = 0;
-#pragma unroll 2
-    for (int k = 0; k < ne; k++) {
-        const int2 o = v[k];
-        acc_ge2(di, lds32(bd + o.x) + Kd);
-        acc_ge2(dx, lds32(bd + o.y) + Kd);
-        acc_ge2(ui, lds32(bu + o.x) + Ku);
-        acc_ge2(ux, lds32(bu + o.y) + Ku);
-    }
-#pragma unroll 2
-    for (int k = ne; k < n; k++) {
-        const int2 o = v[k];
-        acc_ge2(di, prmt(lds32(bd + o.x), lds32(bd + o.x + 4), 0x5432) + Kd);
-        acc_ge2(dx, prmt(lds32(bd + o.y), lds32(bd + o.y + 4), 0x5432) + Kd);
-        acc_ge2(ui, prmt(lds32(bu + o.x), lds32(bu + o.x + 4), 0x5432) + Ku);
-        acc_ge2(ux, prmt(lds32(bu + o.y), lds32(bu + o.y + 4), 0x5432) + Ku);
-    }
-    d_in = di;
-    d_out = dx;
-    u_in = ui;
-    u_out = ux;
 }
 
 // Packed count of [I >= P] over one horizontal list.
@@ -244,13 +214,17 @@ __device__ int refine8(const PairCtx& c, int cx, int cy, int P, int cnt, int t) 
 }
 
 // Both windows of a pair (columns cx and cx+1, same row) in ONE loop: a lane
-// moves on to window B as soon as A is solved, so a warp iterates
-// max(steps_A + steps_B) instead of max(steps_A) + max(steps_B).
+// moves on to window B as soon as A's answer block is found, so a warp
+// iterates max(steps_A + steps_B) instead of max(steps_A) + max(steps_B).  The
+// loop only locates the 8-rank block holding each answer; the bit search runs
+// once after it (inside the loop it would cost every iteration issue slots
+// whenever any lane of the warp resolves).
 template <bool CIRCLE>
 __device__ __forceinline__ void refine8x2(const PairCtx& c, int cx, int cy, int PA, int cntA, int tA, int PB,
                                           int cntB, int tB, int& mA, int& mB) {
     bool up;
-    int need, v0, step, P = PA, cnt = cntA, t = tA, w = 0;
+    int need, v0, step, P = PA, cnt = cntA, t = tA;
+    bool second = false;
     uint32_t mask, Kc;
     auto init = [&]() {
         up = cnt <= t;
@@ -266,96 +240,52 @@ __device__ __forceinline__ void refine8x2(const PairCtx& c, int cx, int cy, int 
         Kc = (uint32_t)((128 - cx) + ((128 - cy) << 8)) * 0x10001u;
     };
     init();
-    mA = -1;
-    mB = -1;
+    int baseA = -1, kA = 0, baseB = -1, kB = 0;
+    uint32_t mskA = 0, mskB = 0;
     for (;;) {
-        int res = -2;
-        if (v0 < 0 || v0 >= c.N) {
-            res = -1;
-        } else {
-            uint32_t m = test8<CIRCLE>(c, v0, Kc, cx, cy) & mask;
-            if (v0 + 8 > c.N) m &= (1u << (c.N - v0)) - 1u;
-            const int pc = __popc(m);
-            if (need < pc) {
-                res = v0 + nth_bit8(m, up ? need : pc - 1 - need);
-            } else {
-                need -= pc;
-                v0 += step;
-                mask = 0xffu;
+        if (v0 < 0 || v0 >= c.N) {  // inconsistent state (core.py:31-36)
+            if (!second) {
+                baseA = -1;
+                second = true;
+                cx += 1;
+                P = PB;
+                cnt = cntB;
+                t = tB;
+                init();
+                continue;
             }
+            baseB = -1;
+            break;
         }
-        if (res != -2) {
-            if (w == 0) {
-                mA = res;
-                w = 1;
+        uint32_t m = test8<CIRCLE>(c, v0, Kc, cx, cy) & mask;
+        if (v0 + 8 > c.N) m &= (1u << (c.N - v0)) - 1u;
+        const int pc = __popc(m);
+        if (need < pc) {
+            const int k = up ? need : pc - 1 - need;
+            if (!second) {
+                baseA = v0;
+                mskA = m;
+                kA = k;
+                second = true;
                 cx += 1;
                 P = PB;
                 cnt = cntB;
                 t = tB;
                 init();
             } else {
-                mB = res;
-                return;
+                baseB = v0;
+                mskB = m;
+                kB = k;
+                break;
             }
+        } else {
+            need -= pc;
+            v0 += step;
+            mask = 0xffu;
         }
     }
-}
-
-// Four windows (a down pair at row cyd and an up pair at row cyu, columns cx
-// and cx+1) in one loop, tasks [w0, w1) of {0: down A, 1: down B, 2: up A,
-// 3: up B}: a warp iterates max over lanes of the SUM of the four walks.
-template <bool CIRCLE>
-__device__ __forceinline__ void refine8x4(const PairCtx& c, int cx0, int cyd, int cyu, const int (&P4)[4],
-                                          const int (&C4)[4], const int (&T4)[4], int w0, int w1, int (&M4)[4]) {
-    bool up;
-    int need, v0, step, w = w0, cx = 0, cy = 0;
-    uint32_t mask, Kc;
-    auto init = [&]() {
-        const int P = (w & 2) ? ((w & 1) ? P4[3] : P4[2]) : ((w & 1) ? P4[1] : P4[0]);
-        const int cnt = (w & 2) ? ((w & 1) ? C4[3] : C4[2]) : ((w & 1) ? C4[1] : C4[0]);
-        const int t = (w & 2) ? ((w & 1) ? T4[3] : T4[2]) : ((w & 1) ? T4[1] : T4[0]);
-        cx = cx0 + (w & 1);
-        cy = (w & 2) ? cyu : cyd;
-        up = cnt <= t;
-        need = up ? t - cnt : cnt - t - 1;
-        if (up) {
-            v0 = P & ~7;
-            mask = (0xffu << (P - v0)) & 0xffu;
-        } else {
-            v0 = (P - 1) & ~7;  // P == 0: v0 = -8, reported as a defect below
-            mask = (P > 0) ? (1u << (P - v0)) - 1u : 0xffu;
-        }
-        step = up ? 8 : -8;
-        Kc = (uint32_t)((128 - cx) + ((128 - cy) << 8)) * 0x10001u;
-    };
-    M4[0] = M4[1] = M4[2] = M4[3] = 0;
-    if (w0 >= w1) return;
-    init();
-    for (;;) {
-        int res = -2;
-        if (v0 < 0 || v0 >= c.N) {
-            res = -1;
-        } else {
-            uint32_t m = test8<CIRCLE>(c, v0, Kc, cx, cy) & mask;
-            if (v0 + 8 > c.N) m &= (1u << (c.N - v0)) - 1u;
-            const int pc = __popc(m);
-            if (need < pc) {
-                res = v0 + nth_bit8(m, up ? need : pc - 1 - need);
-            } else {
-                need -= pc;
-                v0 += step;
-                mask = 0xffu;
-            }
-        }
-        if (res != -2) {
-            if (w == 0) M4[0] = res;
-            else if (w == 1) M4[1] = res;
-            else if (w == 2) M4[2] = res;
-            else M4[3] = res;
-            if (++w >= w1) return;
-            init();
-        }
-    }
+    mA = baseA < 0 ? -1 : baseA + nth_bit8(mskA, kA);
+    mB = baseB < 0 ? -1 : baseB + nth_bit8(mskB, kB);
 }
 
 // Gather C[m] (the input value at omega[m]'s position, core.py:366) and the
@@ -404,23 +334,6 @@ __device__ __forceinline__ int target_at2(const Geom& g, const PairParams& p, co
     return __ldg(p.tmap + (long long)y * g.out_w + x);
 }
 
-// Output = C[m]: the input value at omega[m]'s position (core.py:366).
-__device__ __forceinline__ void write_out2(const Geom& g, const TileCoord& tc, const uint16_t* om, int m,
-                                           int row, int col) {
-    const int oy = tc.oy0 + row, ox = tc.ox0 + col;
-    if (oy >= g.out_h || ox >= g.out_w) return;
-    const uint32_t e = om[m];
-    const long long so = src_offset(g, tc, (int)(e >> 8), (int)(e & 0xff));
-    const long long d = tc.b * g.d_b + (long long)oy * g.d_y + (long long)ox * g.d_x + tc.c * g.d_c;
-    if (g.dtype == DT_U8) {
-        ((uint8_t*)g.dst)[d] = __ldg((const uint8_t*)tc.src + so);
-    } else if (g.dtype == DT_U16) {
-        ((uint16_t*)g.dst)[d] = __ldg((const uint16_t*)tc.src + so);
-    } else {
-        ((uint32_t*)g.dst)[d] = __ldg((const uint32_t*)tc.src + so);
-    }
-}
-
 // Warp-collaborative refine for the few seed windows (lane l tests ranks
 // v0+2l, v0+2l+1 of each 64-rank block), generic membership.
 template <bool CIRCLE>
@@ -466,7 +379,7 @@ __global__ void __launch_bounds__(512) k2_pair(Geom g, PairParams p, const __gri
     extern __shared__ __align__(16) unsigned char smem[];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nwarps = blockDim.x >> 5;
     const int N = g.N, Npad = g.Npad, Sw = g.Sw, r = g.r;
-    const int T = g.Tw, G = p.G, TH = T >> 1;
+    const int T = g.Tw, TY = g.Th, G = p.G, TH = T >> 1;  // T: tile columns, TY: tile rows
     const TileCoord tc = tile_coord(g, g.tile_begin + blockIdx.x);
 
     const uint16_t* om_g = omega_in + (long long)blockIdx.x * (Npad + 2 * OMEGA_SLOT_PAD) + OMEGA_SLOT_PAD;
@@ -475,8 +388,8 @@ __global__ void __launch_bounds__(512) k2_pair(Geom g, PairParams p, const __gri
     const int Ipad = (N + 15) & ~7;
     int* st_P = reinterpret_cast<int*>(I + Ipad);
     int* st_C = st_P + G * T;
-    int* deltas = st_C + G * T;                // max(G*T, T) entries
-    int* hist = deltas + max(G * T, T);        // 32 bins
+    int* deltas = st_C + G * T;                // max(G*T, TY) entries
+    int* hist = deltas + max(G * T, TY);       // 32 bins
     int* seedP = hist + 32;                    // G
     int* seedC = seedP + G;                    // G
     int* span_s = seedC + G;                   // 2r+1
@@ -510,7 +423,7 @@ __global__ void __launch_bounds__(512) k2_pair(Geom g, PairParams p, const __gri
 
     const uint32_t I_a = (uint32_t)__cvta_generic_to_shared(I);
     const PairCtx c{(uint32_t)__cvta_generic_to_shared(om), om, span_s, N, r, p.R2p1};
-    const int R = T / G;
+    const int R = TY / G;
     const int g0 = G >> 1;
     const int cs = (T >> 1) & ~1;  // seed column (even: a pair base)
     auto seed_row = [&](int gi) { return gi * R + (R >> 1); };
@@ -629,85 +542,12 @@ __global__ void __launch_bounds__(512) k2_pair(Geom g, PairParams p, const __gri
     }
     __syncthreads();
 
-    // ---- D'. vertical sweeps, four windows per thread: thread = (group,
-    // column pair) slides its down pair and its up pair in lockstep (shared
-    // offset fetches, four independent accumulation chains) and refines all
-    // four in one loop.
-    if (p.quad) {
-        for (int u = tid; u < G * TH; u += blockDim.x) {
-            const int q = u % TH, gi = u / TH;
-            const int row0 = seed_row(gi);
-            const int rend = (gi == G - 1) ? T : (gi + 1) * R;
-            const int nd = rend - 1 - row0, nu = row0 - gi * R;
-            const int j0 = 2 * q;
-            int P4[4], C4[4], T4[4], M4[4];
-            P4[0] = P4[2] = st_P[gi * T + j0];
-            P4[1] = P4[3] = st_P[gi * T + j0 + 1];
-            C4[0] = C4[2] = st_C[gi * T + j0];
-            C4[1] = C4[3] = st_C[gi * T + j0 + 1];
-            Pend w4[4];
-            w4[0] = gather_out(g, tc, om, P4[0], row0, j0);
-            w4[1] = gather_out(g, tc, om, P4[1], row0, j0 + 1);
-            w4[2].ok = w4[3].ok = false;
-            int rd = row0, ru = row0;
-            const int ns = max(nd, nu);
-            for (int s = 0; s < ns; s++) {
-                const bool dd = s < nd, du = s < nu;
-                uint32_t d_in = 0, d_out = 0, u_in = 0, u_out = 0;
-                const uint32_t Kd = pivot_k(P4[0], P4[1]), Ku = pivot_k(P4[2], P4[3]);
-                if (dd && du) {
-                    vcount_du(I_a + 2 * (rd * Sw + j0), I_a + 2 * ((ru - 1) * Sw + j0), kt.v, p.nv_even, p.nv, Kd,
-                              Ku, d_in, d_out, u_in, u_out);
-                } else if (dd) {
-                    vcount(I_a + 2 * (rd * Sw + j0), kt.v, p.nv_even, p.nv, Kd, d_in, d_out);
-                } else {
-                    vcount(I_a + 2 * ((ru - 1) * Sw + j0), kt.v, p.nv_even, p.nv, Ku, u_in, u_out);
-                }
-#pragma unroll
-                for (int i = 0; i < 4; i++) store_out(g, w4[i]);
-                int dA, dB;
-                if (dd) {
-                    half_diff(d_out, d_in, dA, dB);
-                    C4[0] += dA;
-                    C4[1] += dB;
-                    rd++;
-                }
-                if (du) {
-                    half_diff(u_in, u_out, dA, dB);
-                    C4[2] += dA;
-                    C4[3] += dB;
-                    ru--;
-                }
-                T4[0] = target_at2(g, p, tc, rd, j0);
-                T4[1] = target_at2(g, p, tc, rd, j0 + 1);
-                T4[2] = target_at2(g, p, tc, ru, j0);
-                T4[3] = target_at2(g, p, tc, ru, j0 + 1);
-                refine8x4<CIRCLE>(c, j0 + r, rd + r, ru + r, P4, C4, T4, dd ? 0 : 2, du ? 4 : 2, M4);
-                if ((M4[0] | M4[1] | M4[2] | M4[3]) < 0) atomicOr(p.status, 1);
-#pragma unroll
-                for (int i = 0; i < 4; i++) {
-                    const bool act = (i < 2) ? dd : du;
-                    w4[i].ok = false;
-                    if (act) {
-                        const int m = max(M4[i], 0);
-                        w4[i] = gather_out(g, tc, om, m, (i < 2) ? rd : ru, j0 + (i & 1));
-                        P4[i] = m;
-                        C4[i] = T4[i];
-                    }
-                }
-            }
-#pragma unroll
-            for (int i = 0; i < 4; i++) store_out(g, w4[i]);
-        }
-        return;
-    }
-
     // ---- D. vertical sweeps: thread = (direction, group, column pair) ------
     for (int u = tid; u < 2 * G * TH; u += blockDim.x) {
         const int q = u % TH, rest = u / TH, gi = rest % G;
         const bool down = rest < G;
         const int row0 = seed_row(gi);
-        const int rend = (gi == G - 1) ? T : (gi + 1) * R;  // exclusive
+        const int rend = (gi == G - 1) ? TY : (gi + 1) * R;  // exclusive
         const int j0 = 2 * q, j1 = j0 + 1;
         int PA = st_P[gi * T + j0], cA = st_C[gi * T + j0];
         int PB = st_P[gi * T + j1], cB = st_C[gi * T + j1];
@@ -759,11 +599,11 @@ __global__ void __launch_bounds__(512) k2_pair(Geom g, PairParams p, const __gri
 template __global__ void k2_pair<true>(Geom, PairParams, const __grid_constant__ PairTab, const uint16_t*);
 template __global__ void k2_pair<false>(Geom, PairParams, const __grid_constant__ PairTab, const uint16_t*);
 
-size_t k2_pair_smem_bytes(int N, int Npad, int r, int G, int T) {
+size_t k2_pair_smem_bytes(int N, int Npad, int r, int G, int T, int TY) {
     const int Ipad = (N + 15) & ~7;
     const int gt = G * T;
     return 2 * (size_t)(Npad + 16) + 2 * (size_t)Ipad +
-           4 * (size_t)(2 * gt + (gt > T ? gt : T) + 32 + 2 * G + 2 * r + 1) + 16;
+           4 * (size_t)(2 * gt + (gt > TY ? gt : TY) + 32 + 2 * G + 2 * r + 1) + 16;
 }
 
 // Host: build the pair tables for input-tile row stride Sw.  Returns false if

@@ -378,6 +378,88 @@ __global__ void __launch_bounds__(1024) k1_count(Geom g, uint16_t* __restrict__ 
     store_omega(g, om, omega_slot(g, omega_out));
 }
 
+// k1_count with the tile held in registers: warp w owns input rows w + 32j,
+// lane l owns columns l + 32k (j, k < NK = ceil(S/32)), so every value is read
+// from global memory ONCE, with all NK*NK loads of a thread in flight together
+// (the two-pass k1_count re-reads the tile and exposes the L2 latency per row).
+// 1024 threads; same histogram / scan / scatter as k1_count.
+template <int DT, int NK>
+__global__ void __launch_bounds__(1024) k1_count_reg(Geom g, uint16_t* __restrict__ omega_out) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    constexpr int NB = DT == DT_U8 ? 256 : 65536;
+    constexpr int NW = NB / 2;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const TileCoord tc = tile_coord(g, g.tile_begin + blockIdx.x);
+    const int S = g.Sw, SH = g.Sh;
+    uint32_t* hw = reinterpret_cast<uint32_t*>(smem);
+    uint16_t* om = reinterpret_cast<uint16_t*>(hw + NW);
+    uint32_t v[NK][NK];
+    {
+        long long xo[NK];
+#pragma unroll
+        for (int k = 0; k < NK; k++) {
+            int x = tc.ox0 + lane + 32 * k - g.r + g.vshift;
+            x = x < 0 ? 0 : (x >= g.W ? g.W - 1 : x);
+            xo[k] = (long long)x * g.s_x;
+        }
+#pragma unroll
+        for (int j = 0; j < NK; j++) {
+            const int y = wid + 32 * j;
+            int yy = tc.oy0 + y - g.r + g.vshift;
+            yy = yy < 0 ? 0 : (yy >= g.H ? g.H - 1 : yy);
+            const long long ro = (long long)yy * g.s_y;
+#pragma unroll
+            for (int k = 0; k < NK; k++) {
+                const bool ok = y < SH && lane + 32 * k < S;
+                uint32_t val = 0xffffffffu;
+                if (ok) {
+                    val = DT == DT_U8 ? (uint32_t)__ldg((const uint8_t*)tc.src + ro + xo[k])
+                                      : (uint32_t)__ldg((const uint16_t*)tc.src + ro + xo[k]);
+                }
+                v[j][k] = val;
+            }
+        }
+    }
+    {
+        uint4* h4 = reinterpret_cast<uint4*>(hw);
+        for (int i = tid; i < NW / 4; i += blockDim.x) h4[i] = make_uint4(0, 0, 0, 0);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < NK; j++)
+#pragma unroll
+        for (int k = 0; k < NK; k++)
+            if (v[j][k] != 0xffffffffu) atomicAdd(&hw[v[j][k] >> 1], 1u << ((v[j][k] & 1) << 4));
+    __syncthreads();
+    hist16_exclusive_scan(hw, NW);
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < NK; j++)
+#pragma unroll
+        for (int k = 0; k < NK; k++) {
+            const uint32_t val = v[j][k];
+            if (val != 0xffffffffu) {
+                const uint32_t sh = (val & 1) << 4;
+                const uint32_t old = atomicAdd(&hw[val >> 1], 1u << sh);
+                om[(old >> sh) & 0xffffu] = (uint16_t)((lane + 32 * k) | ((wid + 32 * j) << 8));
+            }
+        }
+    for (int i = g.N + tid; i < g.Npad; i += blockDim.x) om[i] = 0xffffu;
+    __syncthreads();
+    store_omega(g, om, omega_slot(g, omega_out));
+}
+
+#define IMF_K1R(DT) \
+    template __global__ void k1_count_reg<DT, 1>(Geom, uint16_t*); \
+    template __global__ void k1_count_reg<DT, 2>(Geom, uint16_t*); \
+    template __global__ void k1_count_reg<DT, 3>(Geom, uint16_t*); \
+    template __global__ void k1_count_reg<DT, 4>(Geom, uint16_t*); \
+    template __global__ void k1_count_reg<DT, 5>(Geom, uint16_t*); \
+    template __global__ void k1_count_reg<DT, 6>(Geom, uint16_t*);
+IMF_K1R(DT_U8)
+IMF_K1R(DT_U16)
+#undef IMF_K1R
+
 template __global__ void k1_count<DT_U8>(Geom, uint16_t*);
 template __global__ void k1_count<DT_U16>(Geom, uint16_t*);
 
