@@ -164,7 +164,7 @@ def work_per_chpx(kernel):
 
 
 def load_ncu_traffic():
-    p = os.path.join(ROOT, "profiles", "ncu_select_c2.json")
+    p = os.path.join(ROOT, "profiles", "ncu_k2_pair_c2_r1.json")
     try:
         with open(p) as f:
             d = json.load(f)
@@ -268,6 +268,7 @@ def run_ours(args):
            for _ in range(args.steps)]
     sort_ms = select_ms = 0.0
     k2_launches = 0
+    k2_name = "k2_select"
     launches0 = L.imf_launch_count()
     barrier()
     with ClockSampler(local) as clk:
@@ -277,7 +278,10 @@ def run_ours(args):
             step(profile=True)
             evs[i][1].record()
             a, b, n = ctypes.c_float(), ctypes.c_float(), ctypes.c_int32()
-            L.imf_profile_last(ctypes.byref(a), ctypes.byref(b), ctypes.byref(n), None, None, None)
+            qs = ctypes.c_int32()
+            L.imf_profile_last(ctypes.byref(a), ctypes.byref(b), ctypes.byref(n), None, None,
+                               ctypes.byref(qs))
+            k2_name = {2: "k2_pair", 1: "k2_select (omega in L2)"}.get(qs.value, "k2_select")
             sort_ms += a.value
             select_ms += b.value
             k2_launches += n.value
@@ -356,7 +360,7 @@ def run_ours(args):
         "gpu_launches": int(launches),
         "kernel_ms_per_step": {"sort_k1": round(sort_max / args.steps, 4),
                                "select_k2": round(select_max / args.steps, 4)},
-        "roofline": {"bound": "int32", "kernel": "k2_select",
+        "roofline": {"bound": "int32", "kernel": k2_name,
                      "achieved": round(achieved / 1e12, 3),
                      "peak": round(peak.value / 1e12, 3), "unit": "Tops/s",
                      "frac": round(achieved / peak.value, 4),

@@ -107,6 +107,16 @@ int imf_filter(const imf_image* src, imf_image* dst, const imf_kernel* kernel, i
                const int32_t* target_map, int32_t tmin, int32_t tmax, const imf_options* opt,
                void* workspace, size_t workspace_bytes, void* stream);
 
+/*
+ * Multi-percentile "bracket" (core.py:412-426 bracket_filter):
+ * n outputs dsts[0..n) at scalar selection ranks targets[0..n), one ordinal
+ * transform (K1) per tile shared by all n selections.  Same conventions and
+ * workspace size as imf_filter.
+ */
+int imf_filter_bracket(const imf_image* src, imf_image* dsts, int32_t n, const int32_t* targets,
+                       const imf_kernel* kernel, const imf_options* opt, void* workspace,
+                       size_t workspace_bytes, void* stream);
+
 /* Synchronizes `stream` and returns IMF_OK or IMF_ERR_DEFECT for the last
  * imf_filter that used `workspace`. */
 int imf_workspace_status(void* workspace, void* stream);

@@ -22,7 +22,8 @@ IMF_ERR_DEFECT = 3
 IMF_ERR_WORKSPACE = 4
 IMF_ERR_UNSUPPORTED = 5
 
-EXPORTED = ("imf_workspace_size", "imf_filter", "imf_workspace_status", "imf_filter_host",
+EXPORTED = ("imf_workspace_size", "imf_filter", "imf_filter_bracket", "imf_workspace_status",
+            "imf_filter_host",
             "imf_strerror", "imf_version", "imf_last_error", "imf_launch_count",
             "imf_profile_last", "imf_int_peak")
 
@@ -69,6 +70,10 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
                                ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, P(ImfOptions),
                                ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]
     lib.imf_filter.restype = ctypes.c_int
+    lib.imf_filter_bracket.argtypes = [P(ImfImage), P(ImfImage), ctypes.c_int32, ctypes.c_void_p,
+                                       P(ImfKernel), P(ImfOptions), ctypes.c_void_p,
+                                       ctypes.c_size_t, ctypes.c_void_p]
+    lib.imf_filter_bracket.restype = ctypes.c_int
     lib.imf_workspace_status.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
     lib.imf_workspace_status.restype = ctypes.c_int
     lib.imf_filter_host.argtypes = [P(ImfImage), P(ImfImage), P(ImfKernel), ctypes.c_int32,

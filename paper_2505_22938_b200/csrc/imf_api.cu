@@ -314,19 +314,30 @@ size_t imf_workspace_size(const imf_image* src, const imf_kernel* kernel, const 
     return p.ws_total;
 }
 
-int imf_filter(const imf_image* src, imf_image* dst, const imf_kernel* kernel, int32_t target,
-               const int32_t* target_map, int32_t tmin, int32_t tmax, const imf_options* opt,
-               void* workspace, size_t workspace_bytes, void* stream) {
-    if (!dst || !src || !src->data || !dst->data || src->data == dst->data) return IMF_ERR_INVALID;
-    if (dst->dtype != src->dtype || dst->batch != src->batch || dst->channels != src->channels)
-        return IMF_ERR_INVALID;
-    if (!target_map) tmin = tmax = target;
-    if (tmin < 0 || tmax >= kernel->area || tmin > tmax || target < 0 || target >= kernel->area)
-        return IMF_ERR_INVALID;
+}  // extern "C"
+
+// One K1 (ordinal transform) per chunk of tiles, then one K2 (selection) per
+// requested output: n scalar targets (the "bracket", core.py:412-426) reuse
+// the same omega.  n == 1 with an optional per-pixel target map is imf_filter.
+static int filter_impl(const imf_image* src, imf_image* dsts, int n, const int32_t* targets,
+                       const int32_t* target_map, int32_t tmin, int32_t tmax, const imf_kernel* kernel,
+                       const imf_options* opt, void* workspace, size_t workspace_bytes, void* stream) {
+    if (!src || !kernel || !opt || !dsts || n < 1 || !targets || !src->data) return IMF_ERR_INVALID;
+    if (target_map && n != 1) return IMF_ERR_INVALID;
+    for (int i = 0; i < n; i++) {
+        const imf_image* dst = dsts + i;
+        if (!dst->data || src->data == dst->data) return IMF_ERR_INVALID;
+        if (dst->dtype != src->dtype || dst->batch != src->batch || dst->channels != src->channels)
+            return IMF_ERR_INVALID;
+        if (targets[i] < 0 || targets[i] >= kernel->area) return IMF_ERR_INVALID;
+    }
+    if (!target_map) tmin = tmax = targets[0];
+    if (tmin < 0 || tmax >= kernel->area || tmin > tmax) return IMF_ERR_INVALID;
     Plan p;
     int st = make_plan(src, kernel, opt, &p);
     if (st) return st;
-    if (dst->height != p.full_out_h || dst->width != p.g.out_w) return IMF_ERR_INVALID;
+    for (int i = 0; i < n; i++)
+        if (dsts[i].height != p.full_out_h || dsts[i].width != p.g.out_w) return IMF_ERR_INVALID;
     if (!workspace || workspace_bytes < p.ws_total) return IMF_ERR_WORKSPACE;
     cudaStream_t s = (cudaStream_t)stream;
     if (cudaError_t e = set_attrs()) return cuda_fail(e, "cudaFuncSetAttribute");
@@ -344,11 +355,6 @@ int imf_filter(const imf_image* src, imf_image* dst, const imf_kernel* kernel, i
 
     Geom g = p.g;
     g.src = src->data;
-    g.dst = dst->data;
-    g.d_b = dst->stride_b;
-    g.d_y = dst->stride_y;
-    g.d_x = dst->stride_x;
-    g.d_c = dst->stride_c;
 
     SelParams sp;
     memset(&sp, 0, sizeof(sp));
@@ -356,7 +362,7 @@ int imf_filter(const imf_image* src, imf_image* dst, const imf_kernel* kernel, i
     sp.R2 = kernel->radius * (kernel->radius + 1);
     sp.ncols = kernel->ncols;
     sp.nrows = kernel->nrows;
-    sp.target = target;
+    sp.target = targets[0];
     sp.tmap = target_map;
     sp.G = p.G;
     sp.paired = p.paired;
@@ -373,7 +379,7 @@ int imf_filter(const imf_image* src, imf_image* dst, const imf_kernel* kernel, i
             return IMF_ERR_UNSUPPORTED;
         pp.circle = kernel->shape_code == IMF_SHAPE_CIRCLE && p.g.Tw + r <= 128;
         pp.R2p1 = r * (r + 1) + 1;
-        pp.target = target;
+        pp.target = targets[0];
         pp.tmap = target_map;
         pp.G = p.G;
         pp.status = status;
@@ -396,6 +402,13 @@ int imf_filter(const imf_image* src, imf_image* dst, const imf_kernel* kernel, i
         }
         launch_k1(p, g, nb, omega, k1g, s);
         if (prof) cudaEventRecord(e1, s);
+        for (int i = 0; i < n; i++) {
+        g.dst = dsts[i].data;
+        g.d_b = dsts[i].stride_b;
+        g.d_y = dsts[i].stride_y;
+        g.d_x = dsts[i].stride_x;
+        g.d_c = dsts[i].stride_c;
+        sp.target = pp.target = targets[i];
         if (p.pair) {
             if (pp.circle)
                 k2_pair<true><<<nb, p.k2_threads, p.k2_smem, s>>>(g, pp, ptab, omega);
@@ -409,13 +422,14 @@ int imf_filter(const imf_image* src, imf_image* dst, const imf_kernel* kernel, i
             k2_select<true, true><<<nb, p.k2_threads, p.k2_smem, s>>>(g, sp, kt, omega);
         else
             k2_select<false, true><<<nb, p.k2_threads, p.k2_smem, s>>>(g, sp, kt, omega);
+        }
         if (prof) {
             cudaEventRecord(e2, s);
             ev.push_back(e0);
             ev.push_back(e1);
             ev.push_back(e2);
         }
-        g_launches += 2;
+        g_launches += 1 + n;
     }
     if (cudaError_t e = cudaGetLastError()) return cuda_fail(e, "kernel launch");
     if (prof) {
@@ -436,6 +450,29 @@ int imf_filter(const imf_image* src, imf_image* dst, const imf_kernel* kernel, i
         g_prof.chunk = p.chunk_tiles;
     }
     return IMF_OK;
+}
+
+extern "C" {
+
+int imf_filter(const imf_image* src, imf_image* dst, const imf_kernel* kernel, int32_t target,
+               const int32_t* target_map, int32_t tmin, int32_t tmax, const imf_options* opt,
+               void* workspace, size_t workspace_bytes, void* stream) {
+    if (!dst) return IMF_ERR_INVALID;
+    return filter_impl(src, dst, 1, &target, target_map, tmin, tmax, kernel, opt, workspace, workspace_bytes,
+                       stream);
+}
+
+int imf_filter_bracket(const imf_image* src, imf_image* dsts, int32_t n, const int32_t* targets,
+                       const imf_kernel* kernel, const imf_options* opt, void* workspace,
+                       size_t workspace_bytes, void* stream) {
+    if (n < 1 || !targets) return IMF_ERR_INVALID;
+    int32_t tmin = targets[0], tmax = targets[0];
+    for (int i = 1; i < n; i++) {
+        tmin = std::min(tmin, targets[i]);
+        tmax = std::max(tmax, targets[i]);
+    }
+    return filter_impl(src, dsts, n, targets, nullptr, tmin, tmax, kernel, opt, workspace, workspace_bytes,
+                       stream);
 }
 
 int imf_profile_last(float* sort_ms, float* select_ms, int32_t* launches, int64_t* tiles,

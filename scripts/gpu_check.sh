@@ -17,7 +17,7 @@ fi
 if [[ $mode == all || $mode == ncu ]]; then
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
     --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/ncu_bench.log 2>&1
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:k2_select -s 2 -c 1 \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:k2_ -s 2 -c 1 \
     -o gpurun_out/prof_k2 -f python scripts/quick_bench.py c2 > gpurun_out/ncu_k2.log 2>&1
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:k1_ -s 2 -c 1 \
     -o gpurun_out/prof_k1 -f python scripts/quick_bench.py c2 > gpurun_out/ncu_k1.log 2>&1
