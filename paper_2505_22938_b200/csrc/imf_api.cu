@@ -166,6 +166,7 @@ int make_plan(const imf_image* src, const imf_kernel* k, const imf_options* opt,
     g.tiles_y = (row1 - row0 + g.Th - 1) / g.Th;
     p.full_out_h = out_h;
     p.total_tiles = (long long)g.tiles_x * g.tiles_y * g.C * g.B;
+    if (p.total_tiles >= (1ll << 31)) return IMF_ERR_UNSUPPORTED;  // tile_coord uses 32-bit indices
 
     p.k1_count = g.dtype != DT_F32 && k1_count_smem_bytes(g.dtype, g.Npad) <= kSmemMax;
     p.k1_threads = p.k1_count ? kK1Threads : kK1SortThreads;
@@ -571,16 +572,34 @@ int imf_filter_host(const imf_image* src, imf_image* dst, const imf_kernel* kern
     const int r = kernel->radius, vshift = opt->boundary == IMF_BOUNDARY_VALID ? r : 0;
     const int H = src->height, OH = p.full_out_h;
     const bool pipe = rows_outermost(src) && rows_outermost(dst) && OH > 2 * p.g.Th;
-    // stripes of whole tile rows, about eight per image
-    const int tiles_y = (OH + p.g.Th - 1) / p.g.Th;
-    const int stripe = pipe ? p.g.Th * std::max(1, (tiles_y + 7) / 8) : OH;
+    // Stripes of whole tile rows: a short first stripe (the filter starts after
+    // a small upload), a short last one (little left to download after the
+    // last filter), and ~3 long middle stripes (few launches, full waves).
+    std::vector<int> cuts{0};
+    if (pipe) {
+        const int tiles_y = (OH + p.g.Th - 1) / p.g.Th;
+        const int edge = std::max(1, env_int("IMF_STRIPE_EDGE", 2));
+        const int mid = std::max(1, env_int("IMF_STRIPE_MID", 3));
+        if (tiles_y <= 2 * edge + 1) {
+            for (int t = 1; t <= tiles_y; t++) cuts.push_back(t);
+        } else {
+            cuts.push_back(edge);
+            const int body = tiles_y - 2 * edge;
+            for (int i = 1; i <= mid; i++) cuts.push_back(edge + (int)((long long)body * i / mid));
+            cuts.push_back(tiles_y);
+        }
+        for (int& c : cuts) c = std::min(OH, c * p.g.Th);
+        cuts.erase(std::unique(cuts.begin(), cuts.end()), cuts.end());
+    } else {
+        cuts.push_back(OH);
+    }
     if (!rc) {
         cudaStreamWaitEvent(g_hs.up, e_alloc, 0);
         for (int bi = 0; bi < src->batch && !rc; bi++) {
             const long long sbase = (long long)bi * src->stride_b, dbase = (long long)bi * dst->stride_b;
             int up_hi = 0;  // input rows [0, up_hi) of image bi are uploaded
-            for (int y0 = 0; y0 < OH && !rc; y0 += stripe) {
-                const int y1 = std::min(OH, y0 + stripe);
+            for (size_t si = 0; si + 1 < cuts.size() && !rc; si++) {
+                const int y0 = cuts[si], y1 = cuts[si + 1];
                 if (pipe) {
                     const int need = std::min(H, y1 - 1 + r + vshift + 1);
                     if (need > up_hi) {

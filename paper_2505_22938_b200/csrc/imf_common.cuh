@@ -66,12 +66,21 @@ struct SelParams {
     int* status;         // device status word (1 = scan defect)
 };
 
-__device__ __forceinline__ TileCoord tile_coord(const Geom& g, long long t) {
+__device__ __forceinline__ TileCoord tile_coord(const Geom& g, long long t64) {
     TileCoord tc;
-    tc.tx = (int)(t % g.tiles_x); t /= g.tiles_x;
-    tc.ty = (int)(t % g.tiles_y); t /= g.tiles_y;
-    tc.c = (int)(t % g.C); t /= g.C;
-    tc.b = (int)t;
+    // tile indices fit 32 bits (<= 2^31 tiles per call); 32-bit unsigned
+    // division is a few instructions, the 64-bit one a ~100-instruction call
+    unsigned t = (unsigned)t64;
+    const unsigned tx = (unsigned)g.tiles_x, ty = (unsigned)g.tiles_y, C = (unsigned)g.C;
+    unsigned q = t / tx;
+    tc.tx = (int)(t - q * tx);
+    t = q;
+    q = t / ty;
+    tc.ty = (int)(t - q * ty);
+    t = q;
+    q = t / C;
+    tc.c = (int)(t - q * C);
+    tc.b = (int)q;
     tc.oy0 = g.oy_base + tc.ty * g.Th;
     tc.ox0 = tc.tx * g.Tw;
     int esz = g.dtype == DT_U8 ? 1 : (g.dtype == DT_U16 ? 2 : 4);

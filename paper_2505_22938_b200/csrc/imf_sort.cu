@@ -225,16 +225,19 @@ __device__ __forceinline__ void hist16_exclusive_scan(uint32_t* hw, const int NW
     const int per = NW / nw;  // words per warp (NW and nw are powers of two)
     if (per >= 128) {
         // 16-byte chunks: lane l of the warp handles chunk i*32 + l of the warp's
-        // range (conflict-free), 8 counters per lane per step.
+        // range (conflict-free), 8 counters per lane per step.  Every prefix of a
+        // tile's counters is < 65536, so the scan runs on PACKED words: adding
+        // words adds both 16-bit halves independently (no carry can cross), and
+        // counter 2i's exclusive prefix is lo + hi of the packed word prefix.
         uint4* wb = reinterpret_cast<uint4*>(hw + wid * per);
         const int nch = per >> 2;  // chunks per warp, multiple of 32
         uint32_t sum = 0;
         for (int i = lane; i < nch; i += 32) {
             const uint4 q = wb[i];
-            sum += (q.x & 0xffffu) + (q.x >> 16) + (q.y & 0xffffu) + (q.y >> 16) +
-                   (q.z & 0xffffu) + (q.z >> 16) + (q.w & 0xffffu) + (q.w >> 16);
+            sum += q.x + q.y + q.z + q.w;
         }
         sum = __reduce_add_sync(0xffffffffu, sum);
+        sum = (sum & 0xffffu) + (sum >> 16);
         if (lane == 0) wt[wid] = sum;
         __syncthreads();
         if (wid == 0) {
@@ -247,27 +250,28 @@ __device__ __forceinline__ void hist16_exclusive_scan(uint32_t* hw, const int NW
             if (lane < nw) wt[lane] = x - v;
         }
         __syncthreads();
-        uint32_t carry = wt[wid];
+        uint32_t carry = wt[wid];  // plain (unpacked) count before this chunk row
         for (int i0 = 0; i0 < nch; i0 += 32) {
             uint4 q = wb[i0 + lane];
-            const uint32_t c0 = q.x & 0xffffu, c1 = q.x >> 16, c2 = q.y & 0xffffu, c3 = q.y >> 16;
-            const uint32_t c4 = q.z & 0xffffu, c5 = q.z >> 16, c6 = q.w & 0xffffu, c7 = q.w >> 16;
-            const uint32_t tot = c0 + c1 + c2 + c3 + c4 + c5 + c6 + c7;
+            const uint32_t p1 = q.x, p2 = p1 + q.y, p3 = p2 + q.z, tot = p3 + q.w;  // packed prefixes
             uint32_t incl = tot;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
                 if (lane >= o) incl += t;
             }
-            uint32_t e = carry + incl - tot;
-            const uint32_t e1 = e + c0, e2 = e1 + c1, e3 = e2 + c2, e4 = e3 + c3;
-            const uint32_t e5 = e4 + c4, e6 = e5 + c5, e7 = e6 + c6;
-            q.x = e | (e1 << 16);
-            q.y = e2 | (e3 << 16);
-            q.z = e4 | (e5 << 16);
-            q.w = e6 | (e7 << 16);
+            const uint32_t ex = incl - tot;  // packed exclusive prefix of this lane's chunk
+            const uint32_t base = carry + (ex & 0xffffu) + (ex >> 16);
+            // counters before word k: base + flat(packed prefix of words < k)
+            const uint32_t b0 = base, b1 = base + (p1 & 0xffffu) + (p1 >> 16);
+            const uint32_t b2 = base + (p2 & 0xffffu) + (p2 >> 16), b3 = base + (p3 & 0xffffu) + (p3 >> 16);
+            q.x = b0 | ((b0 + (q.x & 0xffffu)) << 16);
+            q.y = b1 | ((b1 + (q.y & 0xffffu)) << 16);
+            q.z = b2 | ((b2 + (q.z & 0xffffu)) << 16);
+            q.w = b3 | ((b3 + (q.w & 0xffffu)) << 16);
             wb[i0 + lane] = q;
-            carry += __shfl_sync(0xffffffffu, incl, 31);
+            const uint32_t last = __shfl_sync(0xffffffffu, incl, 31);
+            carry += (last & 0xffffu) + (last >> 16);
         }
         return;
     }

@@ -24,6 +24,7 @@ cub = [f for f in os.listdir(tmp) if f.endswith(".cubin")][0]
 syms = subprocess.run(["cuobjdump", "-symbols", os.path.join(tmp, cub)], capture_output=True, text=True).stdout
 cands = re.findall(r"(_ZN3imf\S+)", syms)
 def norm(x):
+    x = re.sub(r"\((?:imf::)?\w+\)(?=-?\d)", "", x)
     x = x.replace("(bool)", "").replace("imf::", "").replace("void ", "").replace(" ", "")
     return x.replace("true", "1").replace("false", "0")
 want = norm(kname)
