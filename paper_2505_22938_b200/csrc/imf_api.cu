@@ -103,7 +103,8 @@ int make_plan(const imf_image* src, const imf_kernel* k, const imf_options* opt,
             int G = std::max(1, std::min(opt->seed_rows > 0 ? opt->seed_rows : env_int("IMF_SEED_ROWS", 8), Th));
             const int tpg = Tw;  // threads per seed-row group: (direction, column pair)
             while (G > 1 && ((G * tpg + 31) & ~31) > 512) G--;
-            const size_t ks = k2_pair_smem_bytes(N, Npad, r, G, Tw, Th);
+            const bool pomg = env_int("IMF_PAIR_OMG", 0) != 0;
+            const size_t ks = k2_pair_smem_bytes(N, Npad, r, G, Tw, Th, pomg);
             if (N <= 32768 && ((G * tpg + 31) & ~31) <= 512 && ks <= kSmemMax && k->ncols <= PT_MAX &&
                 k->nrows <= PT_MAX) {
                 best = 1.0;
@@ -117,7 +118,7 @@ int make_plan(const imf_image* src, const imf_kernel* k, const imf_options* opt,
                 p.G = G;
                 p.k2_threads = std::max((G * tpg + 31) & ~31, 64);  // whole warps (phase A/B ballots)
                 p.k2_smem = ks;
-                p.omg = false;
+                p.omg = pomg;
             }
         }
     }
@@ -259,8 +260,10 @@ cudaError_t set_attrs() {
     if (!e) e = allow_smem(k2_select<false, false>, optin);
     if (!e) e = allow_smem(k2_select<true, true>, optin);
     if (!e) e = allow_smem(k2_select<false, true>, optin);
-    if (!e) e = allow_smem(k2_pair<true>, optin);
-    if (!e) e = allow_smem(k2_pair<false>, optin);
+    if (!e) e = allow_smem(k2_pair<true, false>, optin);
+    if (!e) e = allow_smem(k2_pair<false, false>, optin);
+    if (!e) e = allow_smem(k2_pair<true, true>, optin);
+    if (!e) e = allow_smem(k2_pair<false, true>, optin);
     if (!e) g_attr_done = true;
     return e;
 }
@@ -411,10 +414,14 @@ static int filter_impl(const imf_image* src, imf_image* dsts, int n, const int32
         g.d_c = dsts[i].stride_c;
         sp.target = pp.target = targets[i];
         if (p.pair) {
-            if (pp.circle)
-                k2_pair<true><<<nb, p.k2_threads, p.k2_smem, s>>>(g, pp, ptab, omega);
+            if (pp.circle && !p.omg)
+                k2_pair<true, false><<<nb, p.k2_threads, p.k2_smem, s>>>(g, pp, ptab, omega);
+            else if (!p.omg)
+                k2_pair<false, false><<<nb, p.k2_threads, p.k2_smem, s>>>(g, pp, ptab, omega);
+            else if (pp.circle)
+                k2_pair<true, true><<<nb, p.k2_threads, p.k2_smem, s>>>(g, pp, ptab, omega);
             else
-                k2_pair<false><<<nb, p.k2_threads, p.k2_smem, s>>>(g, pp, ptab, omega);
+                k2_pair<false, true><<<nb, p.k2_threads, p.k2_smem, s>>>(g, pp, ptab, omega);
         } else if (sp.circle && !p.omg)
             k2_select<true, false><<<nb, p.k2_threads, p.k2_smem, s>>>(g, sp, kt, omega);
         else if (!p.omg)

@@ -152,9 +152,13 @@ struct PairCtx {
 };
 
 // Membership bits of ranks v0..v0+7 (bit i = rank v0+i) of the window at (cx, cy).
-template <bool CIRCLE>
+template <bool CIRCLE, bool OMG>
 __device__ __forceinline__ uint32_t test8(const PairCtx& c, int v0, uint32_t Kc, int cx, int cy) {
-    const uint4 q = lds128(c.om_a + 2 * v0);
+    uint4 q;
+    if (OMG)  // omega in its L2-resident global slot (16-byte aligned)
+        q = __ldg(reinterpret_cast<const uint4*>(c.om + v0));
+    else
+        q = lds128(c.om_a + 2 * v0);
     const uint32_t w[4] = {q.x, q.y, q.z, q.w};
     uint32_t m = 0;
     if (CIRCLE) {
@@ -185,7 +189,7 @@ __device__ __forceinline__ uint32_t test8(const PairCtx& c, int v0, uint32_t Kc,
 // t-th smallest rank of the window at (cx, cy) from the exact state (P, cnt):
 // walk omega from P toward the target 8 ranks per step (core.py:87-146 with an
 // exact pivot).  -1 if the walk leaves [0, N) (core.py:31-36).
-template <bool CIRCLE>
+template <bool CIRCLE, bool OMG>
 __device__ int refine8(const PairCtx& c, int cx, int cy, int P, int cnt, int t) {
     const bool up = cnt <= t;
     int need = up ? t - cnt : cnt - t - 1;
@@ -203,7 +207,7 @@ __device__ int refine8(const PairCtx& c, int cx, int cy, int P, int cnt, int t) 
     const uint32_t Kc = (uint32_t)((128 - cx) + ((128 - cy) << 8)) * 0x10001u;
     for (;;) {
         if (v0 < 0 || v0 >= c.N) return -1;
-        uint32_t m = test8<CIRCLE>(c, v0, Kc, cx, cy) & mask;
+        uint32_t m = test8<CIRCLE, OMG>(c, v0, Kc, cx, cy) & mask;
         if (v0 + 8 > c.N) m &= (1u << (c.N - v0)) - 1u;
         const int pc = __popc(m);
         if (need < pc) return v0 + nth_bit8(m, up ? need : pc - 1 - need);
@@ -219,7 +223,7 @@ __device__ int refine8(const PairCtx& c, int cx, int cy, int P, int cnt, int t) 
 // loop only locates the 8-rank block holding each answer; the bit search runs
 // once after it (inside the loop it would cost every iteration issue slots
 // whenever any lane of the warp resolves).
-template <bool CIRCLE>
+template <bool CIRCLE, bool OMG>
 __device__ __forceinline__ void refine8x2(const PairCtx& c, int cx, int cy, int PA, int cntA, int tA, int PB,
                                           int cntB, int tB, int& mA, int& mB) {
     bool up;
@@ -257,7 +261,7 @@ __device__ __forceinline__ void refine8x2(const PairCtx& c, int cx, int cy, int 
             baseB = -1;
             break;
         }
-        uint32_t m = test8<CIRCLE>(c, v0, Kc, cx, cy) & mask;
+        uint32_t m = test8<CIRCLE, OMG>(c, v0, Kc, cx, cy) & mask;
         if (v0 + 8 > c.N) m &= (1u << (c.N - v0)) - 1u;
         const int pc = __popc(m);
         if (need < pc) {
@@ -373,7 +377,7 @@ __device__ int refine_warp2(const PairCtx& c, int cx, int cy, int P, int cnt, in
     }
 }
 
-template <bool CIRCLE>
+template <bool CIRCLE, bool OMG>
 __global__ void __launch_bounds__(512) k2_pair(Geom g, PairParams p, const __grid_constant__ PairTab kt,
                                                const uint16_t* __restrict__ omega_in) {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -383,8 +387,10 @@ __global__ void __launch_bounds__(512) k2_pair(Geom g, PairParams p, const __gri
     const TileCoord tc = tile_coord(g, g.tile_begin + blockIdx.x);
 
     const uint16_t* om_g = omega_in + (long long)blockIdx.x * (Npad + 2 * OMEGA_SLOT_PAD) + OMEGA_SLOT_PAD;
-    uint16_t* om = reinterpret_cast<uint16_t*>(smem) + 8;  // 8 sentinels before rank 0
-    uint16_t* I = om + Npad + 8;                               // 16-byte aligned (Npad % 64 == 0)
+    // omega: shared copy (8 sentinels before rank 0), or the global slot (OMG)
+    uint16_t* om_sh = reinterpret_cast<uint16_t*>(smem) + 8;
+    const uint16_t* om = OMG ? om_g : om_sh;
+    uint16_t* I = OMG ? reinterpret_cast<uint16_t*>(smem) : om_sh + Npad + 8;  // 16-byte aligned
     const int Ipad = (N + 15) & ~7;
     int* st_P = reinterpret_cast<int*>(I + Ipad);
     int* st_C = st_P + G * T;
@@ -397,10 +403,10 @@ __global__ void __launch_bounds__(512) k2_pair(Geom g, PairParams p, const __gri
     // ---- 0. stage omega, build the ordinal image --------------------------
     {
         const uint4* src = reinterpret_cast<const uint4*>(om_g);
-        uint4* dst = reinterpret_cast<uint4*>(om);
+        uint4* dst = reinterpret_cast<uint4*>(om_sh);
         for (int i = tid; i < (Npad >> 3); i += blockDim.x) {
             const uint4 v = src[i];
-            dst[i] = v;
+            if (!OMG) dst[i] = v;
             const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
             for (int q = 0; q < 8; q++) {
@@ -411,9 +417,9 @@ __global__ void __launch_bounds__(512) k2_pair(Geom g, PairParams p, const __gri
                 }
             }
         }
-        if (tid < 8) {
-            om[-8 + tid] = 0;
-            om[Npad + tid] = 0;
+        if (!OMG && tid < 8) {
+            om_sh[-8 + tid] = 0;
+            om_sh[Npad + tid] = 0;
         }
         for (int i = N + tid; i < Ipad; i += blockDim.x) I[i] = 0;
         if (tid < 32) hist[tid] = 0;
@@ -422,7 +428,7 @@ __global__ void __launch_bounds__(512) k2_pair(Geom g, PairParams p, const __gri
     __syncthreads();
 
     const uint32_t I_a = (uint32_t)__cvta_generic_to_shared(I);
-    const PairCtx c{(uint32_t)__cvta_generic_to_shared(om), om, span_s, N, r, p.R2p1};
+    const PairCtx c{OMG ? 0u : (uint32_t)__cvta_generic_to_shared(om_sh), om, span_s, N, r, p.R2p1};
     const int R = TY / G;
     const int g0 = G >> 1;
     const int cs = (T >> 1) & ~1;  // seed column (even: a pair base)
@@ -532,7 +538,7 @@ __global__ void __launch_bounds__(512) k2_pair(Geom g, PairParams p, const __gri
             for (int i = j; i < cs; i++) cnt -= deltas[gi * T + i];
         }
         const int tgt = target_at2(g, p, tc, row, j);
-        int m = (j == cs) ? P : refine8<CIRCLE>(c, j + r, row + r, P, cnt, tgt);
+        int m = (j == cs) ? P : refine8<CIRCLE, OMG>(c, j + r, row + r, P, cnt, tgt);
         if (m < 0) {
             atomicOr(p.status, 1);
             m = 0;
@@ -578,7 +584,7 @@ __global__ void __launch_bounds__(512) k2_pair(Geom g, PairParams p, const __gri
             const int tA = target_at2(g, p, tc, row, j0);
             const int tB = target_at2(g, p, tc, row, j1);
             int mA, mB;
-            refine8x2<CIRCLE>(c, j0 + r, row + r, PA, cA, tA, PB, cB, tB, mA, mB);
+            refine8x2<CIRCLE, OMG>(c, j0 + r, row + r, PA, cA, tA, PB, cB, tB, mA, mB);
             if ((mA | mB) < 0) {
                 atomicOr(p.status, 1);
                 mA = max(mA, 0);
@@ -596,13 +602,15 @@ __global__ void __launch_bounds__(512) k2_pair(Geom g, PairParams p, const __gri
     }
 }
 
-template __global__ void k2_pair<true>(Geom, PairParams, const __grid_constant__ PairTab, const uint16_t*);
-template __global__ void k2_pair<false>(Geom, PairParams, const __grid_constant__ PairTab, const uint16_t*);
+template __global__ void k2_pair<true, false>(Geom, PairParams, const __grid_constant__ PairTab, const uint16_t*);
+template __global__ void k2_pair<false, false>(Geom, PairParams, const __grid_constant__ PairTab, const uint16_t*);
+template __global__ void k2_pair<true, true>(Geom, PairParams, const __grid_constant__ PairTab, const uint16_t*);
+template __global__ void k2_pair<false, true>(Geom, PairParams, const __grid_constant__ PairTab, const uint16_t*);
 
-size_t k2_pair_smem_bytes(int N, int Npad, int r, int G, int T, int TY) {
+size_t k2_pair_smem_bytes(int N, int Npad, int r, int G, int T, int TY, bool omg) {
     const int Ipad = (N + 15) & ~7;
     const int gt = G * T;
-    return 2 * (size_t)(Npad + 16) + 2 * (size_t)Ipad +
+    return (omg ? 0 : 2 * (size_t)(Npad + 16)) + 2 * (size_t)Ipad +
            4 * (size_t)(2 * gt + (gt > TY ? gt : TY) + 32 + 2 * G + 2 * r + 1) + 16;
 }
 

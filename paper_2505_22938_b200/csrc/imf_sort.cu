@@ -95,26 +95,31 @@ __device__ void stable_pass(int N, uint32_t* cnt, DigitFn digit, EmitFn emit) {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int CH = ((N + nw * 32 - 1) / (nw * 32)) * 32;
     const int k0 = wid * CH, k1 = min(N, k0 + CH);
-    for (int i = threadIdx.x; i < 256 * nw; i += blockDim.x) cnt[i] = 0;
+    // counters digit-major with a padded row (nw + 1 per digit): the lanes of a
+    // warp touch cnt[d * (nw + 1) + wid] for different digits d, which a row of
+    // exactly nw (= 16) words would fold onto 2 banks; the pad slot stays 0 and
+    // the digit-major exclusive scan is unchanged
+    const int row = nw + 1;
+    for (int i = threadIdx.x; i < 256 * row; i += blockDim.x) cnt[i] = 0;
     __syncthreads();
     for (int it = 0; it < CH; it += 32) {
         int k = k0 + it + lane;
         bool valid = k < k1;
         uint32_t d = valid ? digit(k) : 0xffffffffu;
         unsigned peers = __match_any_sync(FULL, d);
-        if (valid && lane == __ffs(peers) - 1) cnt[d * nw + wid] += __popc(peers);
+        if (valid && lane == __ffs(peers) - 1) cnt[d * row + wid] += __popc(peers);
         __syncwarp();
     }
     __syncthreads();
-    block_exclusive_scan(cnt, 256 * nw);
+    block_exclusive_scan(cnt, 256 * row);
     for (int it = 0; it < CH; it += 32) {
         int k = k0 + it + lane;
         bool valid = k < k1;
         uint32_t d = valid ? digit(k) : 0xffffffffu;
         unsigned peers = __match_any_sync(FULL, d);
-        uint32_t base = valid ? cnt[d * nw + wid] : 0;
+        uint32_t base = valid ? cnt[d * row + wid] : 0;
         __syncwarp();
-        if (valid && lane == __ffs(peers) - 1) cnt[d * nw + wid] = base + __popc(peers);
+        if (valid && lane == __ffs(peers) - 1) cnt[d * row + wid] = base + __popc(peers);
         __syncwarp();
         if (valid) emit(k, (int)(base + __popc(peers & lanemask_lt())));
     }
@@ -157,7 +162,7 @@ __global__ void __launch_bounds__(1024) k1_sort(Geom g, uint16_t* __restrict__ o
     const int nw = blockDim.x >> 5;
     uint32_t* hist = reinterpret_cast<uint32_t*>(smem);
     uint32_t* cnt = hist + 256;
-    uint16_t* om = reinterpret_cast<uint16_t*>(cnt + (DT == DT_U8 ? 0 : 256 * nw));
+    uint16_t* om = reinterpret_cast<uint16_t*>(cnt + (DT == DT_U8 ? 0 : 256 * (nw + 1)));
     unsigned char* big = GMEM ? gscratch + blockIdx.x * gscratch_stride
                               : reinterpret_cast<unsigned char*>(om + g.Npad);
     uint16_t* om_g = omega_slot(g, omega_out);
@@ -479,7 +484,7 @@ template __global__ void k1_sort<DT_F32, true>(Geom, uint16_t*, unsigned char*, 
 
 // Shared-memory bytes K1 needs for a tile (GMEM: large arrays in global scratch).
 size_t k1_smem_bytes(int dtype, int Npad, int nwarps, bool gmem) {
-    size_t b = 256 * 4 + (dtype == DT_U8 ? 0 : 256 * 4 * (size_t)nwarps) + 2 * (size_t)Npad;
+    size_t b = 256 * 4 + (dtype == DT_U8 ? 0 : 256 * 4 * (size_t)(nwarps + 1)) + 2 * (size_t)Npad;
     if (gmem || dtype == DT_U8) return b;
     if (dtype == DT_U16) return b + 3 * (size_t)Npad;
     return b + 6 * (size_t)Npad;
