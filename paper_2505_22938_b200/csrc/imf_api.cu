@@ -43,6 +43,7 @@ struct Plan {
     int G, k2_threads, k1_threads, paired;
     bool k1_gmem, k1_count, omg;
     int full_out_h;
+    int hs;     // k2_pair: ordinal image holds rank >> hs
     bool pair;  // K2 fast path (imf_pair.cu): two windows per thread, 15-bit ranks
     size_t k1_smem, k2_smem, k1_gs_per_tile;
     long long total_tiles, chunk_tiles;
@@ -93,22 +94,29 @@ int make_plan(const imf_image* src, const imf_kernel* k, const imf_options* opt,
         if (k->shape_code == IMF_SHAPE_CIRCLE) Tw = std::min(Tw, 128 - r);
         Tw &= ~1;
         const int Sw = Tw + 2 * r;
-        int Th = std::min(Tw, 32768 / std::max(Sw, 1) - 2 * r);
+        int Th = std::min(Tw, 65536 / std::max(Sw, 1) - 2 * r);
         if (k->shape_code == IMF_SHAPE_CIRCLE) Th = std::min(Th, 128 - r);
         // rectangular tiles (Th < Tw) measured slower than the generic path
-        // (short sweeps, more seed rows per output row): square tiles only
-        if (Tw >= 2 && Th >= (env_int("IMF_PAIR_RECT", 0) ? std::max(2, Tw / 4) : Tw)) {
+        // (short sweeps, more seed rows per output row): square tiles only, and
+        // no smaller than the default 64 (small tiles sort too much per output)
+        const bool shape_ok = Tw >= std::min(Tmax, 64) &&
+                              Th >= (env_int("IMF_PAIR_RECT", 0) ? std::max(2, Tw / 4) : Tw);
+        if (Tw >= 2 && shape_ok) {
             const int Sh = Th + 2 * r;
             const int N = Sw * Sh, Npad = (N + 63) & ~63;
             int G = std::max(1, std::min(opt->seed_rows > 0 ? opt->seed_rows : env_int("IMF_SEED_ROWS", 8), Th));
             const int tpg = Tw;  // threads per seed-row group: (direction, column pair)
             while (G > 1 && ((G * tpg + 31) & ~31) > 512) G--;
-            const bool pomg = env_int("IMF_PAIR_OMG", 0) != 0;
+            // omega in L2 when omega + I would leave room for only one CTA per SM
+            const int forced = env_int("IMF_PAIR_OMG", -1);
+            bool pomg = forced >= 0 ? forced != 0
+                                    : k2_pair_smem_bytes(N, Npad, r, G, Tw, Th, false) > 113 * 1024;
             const size_t ks = k2_pair_smem_bytes(N, Npad, r, G, Tw, Th, pomg);
-            if (N <= 32768 && ((G * tpg + 31) & ~31) <= 512 && ks <= kSmemMax && k->ncols <= PT_MAX &&
+            if (N <= 65536 && ((G * tpg + 31) & ~31) <= 512 && ks <= kSmemMax && k->ncols <= PT_MAX &&
                 k->nrows <= PT_MAX) {
                 best = 1.0;
                 p.pair = true;
+                p.hs = N > 32768 ? 1 : 0;  // ranks >= 2^15: halved ordinal image, even pivots
                 p.g.Tw = Tw;
                 p.g.Th = Th;
                 p.g.Sw = Sw;
@@ -386,6 +394,7 @@ static int filter_impl(const imf_image* src, imf_image* dsts, int n, const int32
         pp.target = targets[0];
         pp.tmap = target_map;
         pp.G = p.G;
+        pp.hs = p.hs;
         pp.status = status;
     }
 

@@ -33,7 +33,7 @@
 
 namespace imf {
 
-constexpr int PT_MAX = 184;  // >= S for N <= 32768 (S <= 181), rounded to 8
+constexpr int PT_MAX = 184;  // >= kernel rows / columns (2r+1) of every pair-path geometry
 
 // Byte offsets into I relative to a window pair's base 2*(row*Sw + 2q), in
 // the constant bank.  Every list holds its 4-byte-aligned entries first; the
@@ -53,6 +53,7 @@ struct PairParams {
     int target;
     const int* tmap;
     int G;
+    int hs;          // 1: I holds rank >> 1 (tiles with 32768 < N <= 65536), pivots even
     int* status;
 };
 
@@ -377,6 +378,33 @@ __device__ int refine_warp2(const PairCtx& c, int cx, int cy, int P, int cnt, in
     }
 }
 
+// Is rank v's pixel in the window at (cx, cy)?  (ordinal.py:175-185)
+template <bool CIRCLE>
+__device__ __forceinline__ bool inside1(const PairCtx& c, int v, int cx, int cy) {
+    const uint32_t e = c.om[v];
+    const int dx = (int)(e & 0xffu) - cx, dyr = (int)(e >> 8) - cy;
+    if (CIRCLE) return dx * dx + dyr * dyr <= c.R2p1 - 1;
+    const int dy = dyr + c.r;
+    if ((unsigned)dy > (unsigned)(2 * c.r)) return false;
+    const int sp = c.span[dy];
+    return (unsigned)(dx - (int)(short)(sp & 0xffff)) < (unsigned)(sp >> 16);
+}
+
+// Solved window (answer m, target t) -> slide state (pivot P, count below P).
+// With halved ranks (hs) the ordinal image holds rank >> 1, which compares
+// exactly only against EVEN pivots: P = m & ~1, and when m is odd the count
+// below P is t minus [rank m-1 is in the window].
+template <bool CIRCLE>
+__device__ __forceinline__ void to_state(const PairCtx& c, int hs, int m, int t, int cx, int cy, int& P,
+                                         int& cnt) {
+    P = m;
+    cnt = t;
+    if (hs && (m & 1)) {
+        P = m - 1;
+        cnt = t - (inside1<CIRCLE>(c, m - 1, cx, cy) ? 1 : 0);
+    }
+}
+
 template <bool CIRCLE, bool OMG>
 __global__ void __launch_bounds__(512) k2_pair(Geom g, PairParams p, const __grid_constant__ PairTab kt,
                                                const uint16_t* __restrict__ omega_in) {
@@ -384,6 +412,7 @@ __global__ void __launch_bounds__(512) k2_pair(Geom g, PairParams p, const __gri
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nwarps = blockDim.x >> 5;
     const int N = g.N, Npad = g.Npad, Sw = g.Sw, r = g.r;
     const int T = g.Tw, TY = g.Th, G = p.G, TH = T >> 1;  // T: tile columns, TY: tile rows
+    const int hs = p.hs;
     const TileCoord tc = tile_coord(g, g.tile_begin + blockIdx.x);
 
     const uint16_t* om_g = omega_in + (long long)blockIdx.x * (Npad + 2 * OMEGA_SLOT_PAD) + OMEGA_SLOT_PAD;
@@ -413,7 +442,7 @@ __global__ void __launch_bounds__(512) k2_pair(Geom g, PairParams p, const __gri
                 const int rank = (i << 3) + q;
                 if (rank < N) {
                     const uint32_t e = (q & 1) ? (w[q >> 1] >> 16) : (w[q >> 1] & 0xffffu);
-                    I[(int)(e >> 8) * Sw + (int)(e & 0xffu)] = (uint16_t)rank;
+                    I[(int)(e >> 8) * Sw + (int)(e & 0xffu)] = (uint16_t)(rank >> hs);
                 }
             }
         }
@@ -435,7 +464,7 @@ __global__ void __launch_bounds__(512) k2_pair(Geom g, PairParams p, const __gri
     auto seed_row = [&](int gi) { return gi * R + (R >> 1); };
 
     // ---- A. direct seed: 32-bin rank histogram over the window ------------
-    const int sh = max(0, 32 - __clz(max(N - 1, 1)) - 5);
+    const int sh = max(0, 32 - __clz(max(((N - 1) >> hs), 1)) - 5);  // 32 bins over I's range
     {
         const int cx = cs + r, cy = seed_row(g0) + r;
         unsigned lm[5];
@@ -473,7 +502,7 @@ __global__ void __launch_bounds__(512) k2_pair(Geom g, PairParams p, const __gri
         }
         const int B = __ffs(__ballot_sync(0xffffffffu, cum > tgt)) - 1;
         const int cnt = __shfl_sync(0xffffffffu, cum - tot, B);
-        const int m = refine_warp2<CIRCLE>(c, cs + r, row + r, B << sh, cnt, tgt);
+        const int m = refine_warp2<CIRCLE>(c, cs + r, row + r, B << (sh + hs), cnt, tgt);
         if (lane == 0) {
             if (m < 0) atomicOr(p.status, 1);
             seedP[g0] = max(m, 0);
@@ -485,8 +514,9 @@ __global__ void __launch_bounds__(512) k2_pair(Geom g, PairParams p, const __gri
     // ---- B. other seed rows' centre windows: vertical deltas at column cs --
     const int ytop = seed_row(0), ybot = seed_row(G - 1);
     if (G > 1) {
-        const int P0 = seedP[g0];
-        const uint32_t K0 = pivot_k(P0, P0);
+        int P0, C0;
+        to_state<CIRCLE>(c, hs, seedP[g0], seedC[g0], cs + r, seed_row(g0) + r, P0, C0);
+        const uint32_t K0 = pivot_k(P0 >> hs, P0 >> hs);
         for (int y = ytop + tid; y < ybot; y += blockDim.x) {  // step y -> y+1 at column cs
             uint32_t gi_, go_;
             vcount(I_a + 2 * (y * Sw + cs), kt.v, p.nv_even, p.nv, K0, gi_, go_);
@@ -502,7 +532,7 @@ __global__ void __launch_bounds__(512) k2_pair(Geom g, PairParams p, const __gri
             } else {
                 for (int y = y1 + lane; y < y0; y += 32) part -= deltas[y];
             }
-            const int cnt = seedC[g0] + (int)__reduce_add_sync(0xffffffffu, (unsigned)part);
+            const int cnt = C0 + (int)__reduce_add_sync(0xffffffffu, (unsigned)part);
             const int tgt = target_at2(g, p, tc, y1, cs);
             const int m = refine_warp2<CIRCLE>(c, cs + r, y1 + r, P0, cnt, tgt);
             if (lane == 0) {
@@ -517,8 +547,9 @@ __global__ void __launch_bounds__(512) k2_pair(Geom g, PairParams p, const __gri
     // ---- C. seed rows: horizontal deltas (pairs of steps) at the row pivot --
     for (int u = tid; u < G * TH; u += blockDim.x) {  // steps 2q -> 2q+1, 2q+1 -> 2q+2 of row gi
         const int gi = u / TH, q = u - gi * TH;
-        const int P = seedP[gi];
-        const uint32_t K = pivot_k(P, P);
+        int P, C0;
+        to_state<CIRCLE>(c, hs, seedP[gi], seedC[gi], cs + r, seed_row(gi) + r, P, C0);
+        const uint32_t K = pivot_k(P >> hs, P >> hs);
         const uint32_t b = I_a + 2 * (seed_row(gi) * Sw + 2 * q);
         const uint32_t ge_in = hcount(b, kt.he, p.nhe_even, p.nh, K);
         const uint32_t ge_out = hcount(b, kt.hx, p.nhx_even, p.nh, K);
@@ -530,15 +561,15 @@ __global__ void __launch_bounds__(512) k2_pair(Geom g, PairParams p, const __gri
     __syncthreads();
     for (int u = tid; u < G * T; u += blockDim.x) {
         const int gi = u / T, j = u - gi * T, row = seed_row(gi);
-        const int P = seedP[gi];
-        int cnt = seedC[gi];
+        int P, cnt;
+        to_state<CIRCLE>(c, hs, seedP[gi], seedC[gi], cs + r, row + r, P, cnt);
         if (j > cs) {
             for (int i = cs; i < j; i++) cnt += deltas[gi * T + i];
         } else {
             for (int i = j; i < cs; i++) cnt -= deltas[gi * T + i];
         }
         const int tgt = target_at2(g, p, tc, row, j);
-        int m = (j == cs) ? P : refine8<CIRCLE, OMG>(c, j + r, row + r, P, cnt, tgt);
+        int m = (j == cs) ? seedP[gi] : refine8<CIRCLE, OMG>(c, j + r, row + r, P, cnt, tgt);
         if (m < 0) {
             atomicOr(p.status, 1);
             m = 0;
@@ -555,17 +586,19 @@ __global__ void __launch_bounds__(512) k2_pair(Geom g, PairParams p, const __gri
         const int row0 = seed_row(gi);
         const int rend = (gi == G - 1) ? TY : (gi + 1) * R;  // exclusive
         const int j0 = 2 * q, j1 = j0 + 1;
-        int PA = st_P[gi * T + j0], cA = st_C[gi * T + j0];
-        int PB = st_P[gi * T + j1], cB = st_C[gi * T + j1];
+        const int mA0 = st_P[gi * T + j0], mB0 = st_P[gi * T + j1];
+        int PA, cA, PB, cB;
+        to_state<CIRCLE>(c, hs, mA0, st_C[gi * T + j0], j0 + r, row0 + r, PA, cA);
+        to_state<CIRCLE>(c, hs, mB0, st_C[gi * T + j1], j1 + r, row0 + r, PB, cB);
         Pend wa{0, 0, false}, wb{0, 0, false};
         if (down) {
-            wa = gather_out(g, tc, om, PA, row0, j0);
-            wb = gather_out(g, tc, om, PB, row0, j1);
+            wa = gather_out(g, tc, om, mA0, row0, j0);
+            wb = gather_out(g, tc, om, mB0, row0, j1);
         }
         const int nsteps = down ? (rend - 1 - row0) : (row0 - gi * R);
         int row = row0;
         for (int s = 0; s < nsteps; s++) {
-            const uint32_t K = pivot_k(PA, PB);
+            const uint32_t K = pivot_k(PA >> hs, PB >> hs);
             uint32_t ge_in, ge_out;
             int dA, dB;
             if (down) {
@@ -592,10 +625,8 @@ __global__ void __launch_bounds__(512) k2_pair(Geom g, PairParams p, const __gri
             }
             wa = gather_out(g, tc, om, mA, row, j0);
             wb = gather_out(g, tc, om, mB, row, j1);
-            PA = mA;
-            cA = tA;
-            PB = mB;
-            cB = tB;
+            to_state<CIRCLE>(c, hs, mA, tA, j0 + r, row + r, PA, cA);
+            to_state<CIRCLE>(c, hs, mB, tB, j1 + r, row + r, PB, cB);
         }
         store_out(g, wa);
         store_out(g, wb);
