@@ -42,12 +42,14 @@ struct Plan {
     Geom g;
     int G, k2_threads, k1_threads, paired;
     bool k1_gmem, k1_count, omg;
+    bool k1_f32b;         // f32 bucket ordinal transform (+ k1_sort fallback on flagged tiles)
+    size_t k1b_smem;
     int full_out_h;
     int hs;     // k2_pair: ordinal image holds rank >> hs
     bool pair;  // K2 fast path (imf_pair.cu): two windows per thread, 15-bit ranks
     size_t k1_smem, k2_smem, k1_gs_per_tile;
     long long total_tiles, chunk_tiles;
-    size_t ws_ktab, ws_omega, ws_k1g, ws_total;
+    size_t ws_ktab, ws_omega, ws_k1g, ws_flags, ws_total;
     int ktab_n;
 };
 
@@ -80,9 +82,16 @@ int make_plan(const imf_image* src, const imf_kernel* k, const imf_options* opt,
 
     Plan& p = *pl;
     memset(&p, 0, sizeof(p));
-    const int Tmax = std::max(1, std::min(opt->tile_size > 0 ? opt->tile_size : env_int("IMF_TILE", 64),
-                                          255 - 2 * r));
+    const int Tmax0 = std::max(1, std::min(opt->tile_size > 0 ? opt->tile_size : env_int("IMF_TILE", 64),
+                                           255 - 2 * r));
     const int G0 = opt->seed_rows > 0 ? opt->seed_rows : env_int("IMF_SEED_ROWS", 4);
+    // f32 tiles use the bucket ordinal transform when N <= 23,716 (S <= 154):
+    // cap the tile at 154 - 2r while that keeps it >= 48 (r <= 53)
+    int Tmax = Tmax0;
+    if (src->dtype == IMF_DTYPE_F32 && env_int("IMF_F32_BUCKET", 1) && opt->tile_size <= 0) {
+        const int tb = (154 - 2 * r) & ~1;  // S <= 154: hist + 4.125 N bytes fit
+        if (tb >= 48) Tmax = std::min(Tmax, tb);
+    }
     const int paired = env_int("IMF_PAIRED", 0);
     double best = -1.0;
     // K2 fast path: tile ranks < 2^15 (S <= 181), even T, and T + r <= 128 for
@@ -105,7 +114,7 @@ int make_plan(const imf_image* src, const imf_kernel* k, const imf_options* opt,
             const int Sh = Th + 2 * r;
             const int N = Sw * Sh, Npad = (N + 63) & ~63;
             int G = std::max(1, std::min(opt->seed_rows > 0 ? opt->seed_rows : env_int("IMF_SEED_ROWS", 8), Th));
-            const int tpg = Tw;  // threads per seed-row group: (direction, column pair)
+            const int tpg = 2 * (((Tw >> 1) + 31) & ~31);  // threads per seed-row group: 2 dirs x pairs (whole warps)
             while (G > 1 && ((G * tpg + 31) & ~31) > 512) G--;
             // omega in L2 when omega + I would leave room for only one CTA per SM
             const int forced = env_int("IMF_PAIR_OMG", -1);
@@ -178,6 +187,8 @@ int make_plan(const imf_image* src, const imf_kernel* k, const imf_options* opt,
     if (p.total_tiles >= (1ll << 31)) return IMF_ERR_UNSUPPORTED;  // tile_coord uses 32-bit indices
 
     p.k1_count = g.dtype != DT_F32 && k1_count_smem_bytes(g.dtype, g.Npad) <= kSmemMax;
+    p.k1b_smem = k1_f32_bucket_smem_bytes(g.N);
+    p.k1_f32b = g.dtype == DT_F32 && env_int("IMF_F32_BUCKET", 1) && g.Sw <= 160 && p.k1b_smem <= kSmemMax;
     p.k1_threads = p.k1_count ? kK1Threads : kK1SortThreads;
     p.k1_gmem = !p.k1_count && k1_smem_bytes(g.dtype, g.Npad, p.k1_threads / 32, false) > kSmemMax;
     p.k1_smem = p.k1_count ? k1_count_smem_bytes(g.dtype, g.Npad)
@@ -195,7 +206,8 @@ int make_plan(const imf_image* src, const imf_kernel* k, const imf_options* opt,
     p.ws_ktab = ((size_t)p.ktab_n * 4 + 255) & ~(size_t)255;
     p.ws_omega = (((size_t)chunk * slot) + 255) & ~(size_t)255;
     p.ws_k1g = (size_t)chunk * p.k1_gs_per_tile;
-    p.ws_total = kStatusBytes + p.ws_ktab + p.ws_omega + p.ws_k1g;
+    p.ws_flags = p.k1_f32b ? (((size_t)(chunk + 1) * 4 + 255) & ~(size_t)255) : 0;
+    p.ws_total = kStatusBytes + p.ws_ktab + p.ws_omega + p.ws_k1g + p.ws_flags;
     return IMF_OK;
 }
 
@@ -264,6 +276,11 @@ cudaError_t set_attrs() {
     IMF_K1R_ATTR(DT_U8)
     IMF_K1R_ATTR(DT_U16)
 #undef IMF_K1R_ATTR
+    if (!e) e = allow_smem(k1_f32_bucket<1>, optin);
+    if (!e) e = allow_smem(k1_f32_bucket<2>, optin);
+    if (!e) e = allow_smem(k1_f32_bucket<3>, optin);
+    if (!e) e = allow_smem(k1_f32_bucket<4>, optin);
+    if (!e) e = allow_smem(k1_f32_bucket<5>, optin);
     if (!e) e = allow_smem(k2_select<true, false>, optin);
     if (!e) e = allow_smem(k2_select<false, false>, optin);
     if (!e) e = allow_smem(k2_select<true, true>, optin);
@@ -277,9 +294,27 @@ cudaError_t set_attrs() {
 }
 
 void launch_k1(const Plan& p, const Geom& g, int nblocks, uint16_t* omega, unsigned char* k1g,
-               cudaStream_t s) {
+               int* flags, cudaStream_t s) {
     const dim3 grid(nblocks), block(p.k1_threads);
     const long long gs = (long long)p.k1_gs_per_tile;
+    if (p.k1_f32b) {
+        const dim3 b1024(1024);
+        cudaMemsetAsync(flags, 0, sizeof(int), s);  // fallback list count
+        switch ((g.Sw + 31) >> 5) {
+            case 1: k1_f32_bucket<1><<<grid, b1024, p.k1b_smem, s>>>(g, omega, flags); break;
+            case 2: k1_f32_bucket<2><<<grid, b1024, p.k1b_smem, s>>>(g, omega, flags); break;
+            case 3: k1_f32_bucket<3><<<grid, b1024, p.k1b_smem, s>>>(g, omega, flags); break;
+            case 4: k1_f32_bucket<4><<<grid, b1024, p.k1b_smem, s>>>(g, omega, flags); break;
+            default: k1_f32_bucket<5><<<grid, b1024, p.k1b_smem, s>>>(g, omega, flags); break;
+        }
+        // tiles with a bucket above kMaxBucket: LSD radix sort over the list
+        const dim3 fgrid(std::min(nblocks, 148));
+        if (p.k1_gmem)
+            k1_sort<DT_F32, true><<<fgrid, block, p.k1_smem, s>>>(g, omega, k1g, gs, flags);
+        else
+            k1_sort<DT_F32, false><<<fgrid, block, p.k1_smem, s>>>(g, omega, k1g, gs, flags);
+        return;
+    }
     if (p.k1_count) {
         const int nk = (g.Sw + 31) >> 5;
         if (nk <= 6 && env_int("IMF_K1REG", 1)) {
@@ -308,11 +343,11 @@ void launch_k1(const Plan& p, const Geom& g, int nblocks, uint16_t* omega, unsig
     }
     switch (g.dtype * 2 + (p.k1_gmem ? 1 : 0)) {
         case 0:
-        case 1: k1_sort<DT_U8, false><<<grid, block, p.k1_smem, s>>>(g, omega, k1g, gs); break;
-        case 2: k1_sort<DT_U16, false><<<grid, block, p.k1_smem, s>>>(g, omega, k1g, gs); break;
-        case 3: k1_sort<DT_U16, true><<<grid, block, p.k1_smem, s>>>(g, omega, k1g, gs); break;
-        case 4: k1_sort<DT_F32, false><<<grid, block, p.k1_smem, s>>>(g, omega, k1g, gs); break;
-        default: k1_sort<DT_F32, true><<<grid, block, p.k1_smem, s>>>(g, omega, k1g, gs); break;
+        case 1: k1_sort<DT_U8, false><<<grid, block, p.k1_smem, s>>>(g, omega, k1g, gs, nullptr); break;
+        case 2: k1_sort<DT_U16, false><<<grid, block, p.k1_smem, s>>>(g, omega, k1g, gs, nullptr); break;
+        case 3: k1_sort<DT_U16, true><<<grid, block, p.k1_smem, s>>>(g, omega, k1g, gs, nullptr); break;
+        case 4: k1_sort<DT_F32, false><<<grid, block, p.k1_smem, s>>>(g, omega, k1g, gs, nullptr); break;
+        default: k1_sort<DT_F32, true><<<grid, block, p.k1_smem, s>>>(g, omega, k1g, gs, nullptr); break;
     }
 }
 
@@ -359,6 +394,7 @@ static int filter_impl(const imf_image* src, imf_image* dsts, int n, const int32
     int* ktab_d = (int*)(ws + kStatusBytes);
     uint16_t* omega = (uint16_t*)(ws + kStatusBytes + p.ws_ktab);
     unsigned char* k1g = ws + kStatusBytes + p.ws_ktab + p.ws_omega;
+    int* k1flags = (int*)(ws + kStatusBytes + p.ws_ktab + p.ws_omega + p.ws_k1g);
 
     static thread_local KTab kt;
     build_ktab_struct(kernel, p.g.Sw, kt);
@@ -413,7 +449,7 @@ static int filter_impl(const imf_image* src, imf_image* dsts, int n, const int32
             cudaEventCreate(&e2);
             cudaEventRecord(e0, s);
         }
-        launch_k1(p, g, nb, omega, k1g, s);
+        launch_k1(p, g, nb, omega, k1g, k1flags, s);
         if (prof) cudaEventRecord(e1, s);
         for (int i = 0; i < n; i++) {
         g.dst = dsts[i].data;

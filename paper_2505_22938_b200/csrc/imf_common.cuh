@@ -81,8 +81,12 @@ __device__ __forceinline__ TileCoord tile_coord(const Geom& g, long long t64) {
     q = t / C;
     tc.c = (int)(t - q * C);
     tc.b = (int)q;
-    tc.oy0 = g.oy_base + tc.ty * g.Th;
-    tc.ox0 = tc.tx * g.Tw;
+    // The last tile of a row / column is shifted back to end at the image edge
+    // (overlapping its neighbour; both write identical values) instead of
+    // hanging past it: windows far into the clamped margin are all ties and
+    // cost the refine far more than the overlap does.
+    tc.oy0 = g.oy_base + min(tc.ty * g.Th, max(g.out_h - g.oy_base - g.Th, 0));
+    tc.ox0 = min(tc.tx * g.Tw, max(g.out_w - g.Tw, 0));
     int esz = g.dtype == DT_U8 ? 1 : (g.dtype == DT_U16 ? 2 : 4);
     tc.src = (const char*)g.src + (tc.b * g.s_b + tc.c * g.s_c) * esz;
     return tc;

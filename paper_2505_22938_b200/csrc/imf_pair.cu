@@ -580,8 +580,12 @@ __global__ void __launch_bounds__(512) k2_pair(Geom g, PairParams p, const __gri
     __syncthreads();
 
     // ---- D. vertical sweeps: thread = (direction, group, column pair) ------
-    for (int u = tid; u < 2 * G * TH; u += blockDim.x) {
-        const int q = u % TH, rest = u / TH, gi = rest % G;
+    // lanes of a (direction, group) padded to whole warps: every warp sweeps
+    // one row band in one direction (uniform trip counts, one I row per load)
+    const int THP = (TH + 31) & ~31;
+    for (int u = tid; u < 2 * G * THP; u += blockDim.x) {
+        const int q = u % THP, rest = u / THP, gi = rest % G;
+        if (q >= TH) continue;
         const bool down = rest < G;
         const int row0 = seed_row(gi);
         const int rend = (gi == G - 1) ? TY : (gi + 1) * R;  // exclusive

@@ -135,8 +135,9 @@ __device__ __forceinline__ uint16_t pack_pos(int i, int Sw, float invS) {
 // Copy the finished omega (smem, N entries) to its global slot, 16 B at a time.
 // Global omega slot of a tile: OMEGA_SLOT_PAD sentinel entries on both sides
 // of Npad ranks, so scans may step a few ranks past either end.
-__device__ __forceinline__ uint16_t* omega_slot(const Geom& g, uint16_t* base) {
-    return base + (long long)blockIdx.x * (g.Npad + 2 * OMEGA_SLOT_PAD) + OMEGA_SLOT_PAD;
+__device__ __forceinline__ uint16_t* omega_slot(const Geom& g, uint16_t* base, int bt = -1) {
+    if (bt < 0) bt = blockIdx.x;
+    return base + (long long)bt * (g.Npad + 2 * OMEGA_SLOT_PAD) + OMEGA_SLOT_PAD;
 }
 
 __device__ __forceinline__ void store_omega(const Geom& g, const uint16_t* om_s, uint16_t* om_g) {
@@ -151,11 +152,10 @@ __device__ __forceinline__ void store_omega(const Geom& g, const uint16_t* om_s,
 }
 
 template <int DT, bool GMEM>
-__global__ void __launch_bounds__(1024) k1_sort(Geom g, uint16_t* __restrict__ omega_out,
-                                               unsigned char* __restrict__ gscratch,
-                                               long long gscratch_stride) {
+__device__ void k1_sort_tile(const Geom& g, uint16_t* __restrict__ omega_out, unsigned char* __restrict__ gscratch,
+                             long long gscratch_stride, const int bt) {
     extern __shared__ __align__(16) unsigned char smem[];
-    const long long t = g.tile_begin + blockIdx.x;
+    const long long t = g.tile_begin + bt;
     const TileCoord tc = tile_coord(g, t);
     const int N = g.N, Sw = g.Sw;
     const float invS = 1.0f / (float)Sw;
@@ -163,9 +163,9 @@ __global__ void __launch_bounds__(1024) k1_sort(Geom g, uint16_t* __restrict__ o
     uint32_t* hist = reinterpret_cast<uint32_t*>(smem);
     uint32_t* cnt = hist + 256;
     uint16_t* om = reinterpret_cast<uint16_t*>(cnt + (DT == DT_U8 ? 0 : 256 * (nw + 1)));
-    unsigned char* big = GMEM ? gscratch + blockIdx.x * gscratch_stride
+    unsigned char* big = GMEM ? gscratch + bt * gscratch_stride
                               : reinterpret_cast<unsigned char*>(om + g.Npad);
-    uint16_t* om_g = omega_slot(g, omega_out);
+    uint16_t* om_g = omega_slot(g, omega_out, bt);
 
     if (DT == DT_U8) {
         auto digit = [&](int i) {
@@ -220,11 +220,30 @@ __global__ void __launch_bounds__(1024) k1_sort(Geom g, uint16_t* __restrict__ o
     store_omega(g, om, om_g);
 }
 
+// One CTA per tile; or, with `only` (the f32 bucket kernel's fallback list:
+// only[0] = count, only[1..] = chunk tile indices), a small grid looping over
+// the listed tiles.
+template <int DT, bool GMEM>
+__global__ void __launch_bounds__(1024) k1_sort(Geom g, uint16_t* __restrict__ omega_out,
+                                               unsigned char* __restrict__ gscratch,
+                                               long long gscratch_stride, const int* __restrict__ only) {
+    if (!only) {
+        k1_sort_tile<DT, GMEM>(g, omega_out, gscratch, gscratch_stride, blockIdx.x);
+        return;
+    }
+    const int n = only[0];
+    for (int i = blockIdx.x; i < n; i += gridDim.x) {
+        k1_sort_tile<DT, GMEM>(g, omega_out, gscratch, gscratch_stride, only[1 + i]);
+        __syncthreads();
+    }
+}
+
 // Exclusive scan, in place, of the 2*NW 16-bit counters packed two per word
 // in hw[0..NW).  Warp w owns words [w*NW/nw, (w+1)*NW/nw); lanes stride by one
 // word, so every shared access is bank-conflict free.  Ends with the counters
 // replaced by their exclusive prefix (no trailing barrier).
-__device__ __forceinline__ void hist16_exclusive_scan(uint32_t* hw, const int NW) {
+__device__ __forceinline__ void hist16_exclusive_scan(uint32_t* hw, const int NW,
+                                                      uint32_t* starts = nullptr) {
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
     __shared__ uint32_t wt[32];
     const int per = NW / nw;  // words per warp (NW and nw are powers of two)
@@ -270,6 +289,15 @@ __device__ __forceinline__ void hist16_exclusive_scan(uint32_t* hw, const int NW
             // counters before word k: base + flat(packed prefix of words < k)
             const uint32_t b0 = base, b1 = base + (p1 & 0xffffu) + (p1 >> 16);
             const uint32_t b2 = base + (p2 & 0xffffu) + (p2 >> 16), b3 = base + (p3 & 0xffffu) + (p3 >> 16);
+            if (starts) {  // bit at every non-empty counter's first position (bucket starts)
+                const uint32_t cw[4] = {q.x, q.y, q.z, q.w}, bw[4] = {b0, b1, b2, b3};
+#pragma unroll
+                for (int k = 0; k < 4; k++) {
+                    const uint32_t lo = cw[k] & 0xffffu, e0 = bw[k], e1 = bw[k] + lo;
+                    if (lo) atomicOr(&starts[e0 >> 5], 1u << (e0 & 31));
+                    if (cw[k] >> 16) atomicOr(&starts[e1 >> 5], 1u << (e1 & 31));
+                }
+            }
             q.x = b0 | ((b0 + (q.x & 0xffffu)) << 16);
             q.y = b1 | ((b1 + (q.y & 0xffffu)) << 16);
             q.z = b2 | ((b2 + (q.z & 0xffffu)) << 16);
@@ -469,6 +497,117 @@ IMF_K1R(DT_U8)
 IMF_K1R(DT_U16)
 #undef IMF_K1R
 
+// f32 ordinal transform by buckets: count-sort the u32 order keys (ordinal.py:
+// 109-123) by their HIGH 16 bits with the u16 machinery (register-resident tile,
+// 64K-bin packed histogram, packed scan), scatter entries (low16 << 16 | pos)
+// into bucket order, then rank each entry inside its bucket by counting the
+// smaller entries (buckets are contiguous; a bitmap marks their starts).  Ties
+// break by position (output-neutral).  Cost ~ sum of squared bucket sizes: a
+// tile whose largest bucket exceeds kMaxBucket (narrow value range, flat
+// regions) writes flag 1 and no omega; a k1_sort launch redoes those tiles.
+constexpr int kMaxBucket = 256;
+
+template <int NK>
+__global__ void __launch_bounds__(1024) k1_f32_bucket(Geom g, uint16_t* __restrict__ omega_out,
+                                                     int* __restrict__ fallback) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    constexpr int NW = 32768;  // histogram words (65536 16-bit counters)
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const TileCoord tc = tile_coord(g, g.tile_begin + blockIdx.x);
+    const int S = g.Sw, SH = g.Sh, N = g.N;
+    uint32_t* hw = reinterpret_cast<uint32_t*>(smem);
+    uint32_t* ent = hw + NW;                  // N entries
+    uint32_t* starts = ent + ((N + 3) & ~3);  // bucket-start bitmap, ceil(N/32) words
+    const int nsw = (N + 31) >> 5;
+    __shared__ int s_max;
+    uint32_t v[NK][NK];
+    {
+        long long xo[NK];
+#pragma unroll
+        for (int k = 0; k < NK; k++) {
+            int x = tc.ox0 + lane + 32 * k - g.r + g.vshift;
+            x = x < 0 ? 0 : (x >= g.W ? g.W - 1 : x);
+            xo[k] = (long long)x * g.s_x;
+        }
+#pragma unroll
+        for (int j = 0; j < NK; j++) {
+            const int y = wid + 32 * j;
+            int yy = tc.oy0 + y - g.r + g.vshift;
+            yy = yy < 0 ? 0 : (yy >= g.H ? g.H - 1 : yy);
+            const long long ro = (long long)yy * g.s_y;
+#pragma unroll
+            for (int k = 0; k < NK; k++) {
+                const bool ok = y < SH && lane + 32 * k < S;
+                v[j][k] = ok ? float_key(__ldg((const uint32_t*)tc.src + ro + xo[k])) : 0u;
+            }
+        }
+    }
+    {
+        uint4* h4 = reinterpret_cast<uint4*>(hw);
+        for (int i = tid; i < NW / 4; i += blockDim.x) h4[i] = make_uint4(0, 0, 0, 0);
+        for (int i = tid; i < nsw; i += blockDim.x) starts[i] = 0;
+        if (tid == 0) s_max = 0;
+    }
+    __syncthreads();
+    int mx = 0;
+#pragma unroll
+    for (int j = 0; j < NK; j++)
+#pragma unroll
+        for (int k = 0; k < NK; k++)
+            if (wid + 32 * j < SH && lane + 32 * k < S) {
+                const uint32_t h = v[j][k] >> 16, sh = (h & 1) << 4;
+                const uint32_t old = atomicAdd(&hw[h >> 1], 1u << sh);
+                mx = max(mx, (int)((old >> sh) & 0xffffu) + 1);
+            }
+    mx = __reduce_max_sync(0xffffffffu, mx);
+    if (lane == 0) atomicMax(&s_max, mx);
+    __syncthreads();
+    if (s_max > kMaxBucket) {  // block-uniform: hand the tile to the radix sort
+        if (tid == 0) fallback[1 + atomicAdd(fallback, 1)] = blockIdx.x;
+        return;
+    }
+    hist16_exclusive_scan(hw, NW, starts);
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < NK; j++)
+#pragma unroll
+        for (int k = 0; k < NK; k++)
+            if (wid + 32 * j < SH && lane + 32 * k < S) {
+                const uint32_t key = v[j][k], h = key >> 16, sh = (h & 1) << 4;
+                const uint32_t old = atomicAdd(&hw[h >> 1], 1u << sh);
+                ent[(old >> sh) & 0xffffu] = (key << 16) | (uint32_t)((lane + 32 * k) | ((wid + 32 * j) << 8));
+            }
+    __syncthreads();
+    uint16_t* om = reinterpret_cast<uint16_t*>(hw);  // the histogram is dead: omega goes here
+    for (int sp = tid; sp < N; sp += blockDim.x) {
+        const uint32_t e = ent[sp];
+        int w = sp >> 5;
+        uint32_t m = starts[w] & (0xffffffffu >> (31 - (sp & 31)));  // start bits <= sp
+        while (!m) m = starts[--w];
+        const int b0 = (w << 5) + 31 - __clz(m);
+        w = sp >> 5;
+        m = (sp & 31) == 31 ? 0u : starts[w] & (0xfffffffeu << (sp & 31));  // start bits > sp
+        while (!m && ++w < nsw) m = starts[w];
+        const int b1 = m ? (w << 5) + __ffs(m) - 1 : N;
+        int rk = b0;
+        for (int q = b0; q < b1; q++) rk += ent[q] < e ? 1 : 0;
+        om[rk] = (uint16_t)(e & 0xffffu);
+    }
+    for (int i = N + tid; i < g.Npad; i += blockDim.x) om[i] = 0xffffu;
+    __syncthreads();
+    store_omega(g, om, omega_slot(g, omega_out));
+}
+
+template __global__ void k1_f32_bucket<1>(Geom, uint16_t*, int*);
+template __global__ void k1_f32_bucket<2>(Geom, uint16_t*, int*);
+template __global__ void k1_f32_bucket<3>(Geom, uint16_t*, int*);
+template __global__ void k1_f32_bucket<4>(Geom, uint16_t*, int*);
+template __global__ void k1_f32_bucket<5>(Geom, uint16_t*, int*);
+
+size_t k1_f32_bucket_smem_bytes(int N) {
+    return 32768 * 4 + 4 * (size_t)((N + 3) & ~3) + 4 * (size_t)((N + 31) >> 5) + 16;
+}
+
 template __global__ void k1_count<DT_U8>(Geom, uint16_t*);
 template __global__ void k1_count<DT_U16>(Geom, uint16_t*);
 
@@ -476,11 +615,11 @@ size_t k1_count_smem_bytes(int dtype, int Npad) {
     return (dtype == DT_U8 ? 128 * 4 : 32768 * 4) + 2 * (size_t)Npad;
 }
 
-template __global__ void k1_sort<DT_U8, false>(Geom, uint16_t*, unsigned char*, long long);
-template __global__ void k1_sort<DT_U16, false>(Geom, uint16_t*, unsigned char*, long long);
-template __global__ void k1_sort<DT_U16, true>(Geom, uint16_t*, unsigned char*, long long);
-template __global__ void k1_sort<DT_F32, false>(Geom, uint16_t*, unsigned char*, long long);
-template __global__ void k1_sort<DT_F32, true>(Geom, uint16_t*, unsigned char*, long long);
+template __global__ void k1_sort<DT_U8, false>(Geom, uint16_t*, unsigned char*, long long, const int*);
+template __global__ void k1_sort<DT_U16, false>(Geom, uint16_t*, unsigned char*, long long, const int*);
+template __global__ void k1_sort<DT_U16, true>(Geom, uint16_t*, unsigned char*, long long, const int*);
+template __global__ void k1_sort<DT_F32, false>(Geom, uint16_t*, unsigned char*, long long, const int*);
+template __global__ void k1_sort<DT_F32, true>(Geom, uint16_t*, unsigned char*, long long, const int*);
 
 // Shared-memory bytes K1 needs for a tile (GMEM: large arrays in global scratch).
 size_t k1_smem_bytes(int dtype, int Npad, int nwarps, bool gmem) {
