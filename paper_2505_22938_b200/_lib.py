@@ -13,7 +13,7 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libisomedian_b200.so")
+LIB_PATH = os.environ.get("IMF_LIB") or os.path.join(_HERE, "libisomedian_b200.so")
 
 IMF_OK = 0
 IMF_ERR_INVALID = 1

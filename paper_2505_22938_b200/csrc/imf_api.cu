@@ -119,8 +119,8 @@ int make_plan(const imf_image* src, const imf_kernel* k, const imf_options* opt,
             // omega in L2 when omega + I would leave room for only one CTA per SM
             const int forced = env_int("IMF_PAIR_OMG", -1);
             bool pomg = forced >= 0 ? forced != 0
-                                    : k2_pair_smem_bytes(N, Npad, r, G, Tw, Th, false) > 113 * 1024;
-            const size_t ks = k2_pair_smem_bytes(N, Npad, r, G, Tw, Th, pomg);
+                                    : k2_pair_smem_bytes(N, Npad, N, r, G, Tw, Th, false) > 113 * 1024;
+            const size_t ks = k2_pair_smem_bytes(N, Npad, N, r, G, Tw, Th, pomg);
             if (N <= 65536 && ((G * tpg + 31) & ~31) <= 512 && ks <= kSmemMax && k->ncols <= PT_MAX &&
                 k->nrows <= PT_MAX) {
                 best = 1.0;
@@ -194,6 +194,35 @@ int make_plan(const imf_image* src, const imf_kernel* k, const imf_options* opt,
     p.k1_smem = p.k1_count ? k1_count_smem_bytes(g.dtype, g.Npad)
                            : k1_smem_bytes(g.dtype, g.Npad, p.k1_threads / 32, p.k1_gmem);
     p.k1_gs_per_tile = p.k1_gmem ? k1_gscratch_bytes(g.dtype, g.Npad) : 0;
+
+    // Rounded-rect footprint (pair path, circle kernels, register-resident K1):
+    // rank only input pixels within distance^2 r(r+1) of the output rectangle
+    // -- the union of the tile's windows -- so omega is shorter and denser.
+    const bool k1reg = p.k1_count && ((g.Sw + 31) >> 5) <= 6 && env_int("IMF_K1REG", 1);
+    if (p.pair && k->shape_code == IMF_SHAPE_CIRCLE && k1reg && env_int("IMF_FOOTPRINT", 1)) {
+        const int R2 = r * (r + 1);
+        int nfp = 0;
+        for (int y = 0; y < g.Sh; y++) {
+            const int ey = std::max(0, std::max(r - y, y - (r + g.Th - 1)));
+            const int D = R2 - ey * ey;
+            if (D < 0) continue;
+            int w = 0;
+            while ((w + 1) * (w + 1) <= D) w++;
+            nfp += std::min(g.Sw - 1, r + g.Tw - 1 + w) - std::max(0, r - w) + 1;
+        }
+        const int NI = g.Sw * g.Sh;
+        g.fp = 1;
+        g.fpR2 = R2;
+        g.N = nfp;
+        g.Npad = (nfp + 63) & ~63;
+        p.hs = nfp > 32768 ? 1 : 0;
+        const int forced = env_int("IMF_PAIR_OMG", -1);
+        const bool pomg = forced >= 0 ? forced != 0
+                                      : k2_pair_smem_bytes(g.N, g.Npad, NI, r, p.G, g.Tw, g.Th, false) > 113 * 1024;
+        p.omg = pomg;
+        p.k2_smem = k2_pair_smem_bytes(g.N, g.Npad, NI, r, p.G, g.Tw, g.Th, pomg);
+        p.k1_smem = k1_count_smem_bytes(g.dtype, g.Npad);
+    }
 
     p.ktab_n = 2 * k->ncols + 2 * k->nrows + 2 * r + 1;
     const size_t slot = 2 * (size_t)(g.Npad + 2 * OMEGA_SLOT_PAD);

@@ -33,7 +33,8 @@ struct Geom {
     int oy_base;                   // first output row of this launch (row stripe)
     int vshift;                    // r in valid mode, 0 in replicate mode
     int r;
-    int Tw, Th, Sw, Sh, N, Npad;   // Npad: N rounded up to a multiple of 64
+    int Tw, Th, Sw, Sh, N, Npad;   // N: ranked pixels per tile; Npad: N rounded up to a multiple of 64
+    int fp, fpR2;                  // fp: only pixels within dist^2 <= fpR2 of the output rect are ranked
     int tiles_x, tiles_y;
     long long tile_begin;          // first tile of this launch (chunking)
 };
@@ -99,6 +100,18 @@ __device__ __forceinline__ long long src_offset(const Geom& g, const TileCoord& 
     y = y < 0 ? 0 : (y >= g.H ? g.H - 1 : y);
     x = x < 0 ? 0 : (x >= g.W ? g.W - 1 : x);
     return (long long)y * g.s_y + (long long)x * g.s_x;
+}
+
+// Rounded-rect tile footprint (tiling.py:148-162 is the CPU
+// analog): input-tile pixel (x, y) is in some circle window of the tile iff its
+// squared distance to the output rectangle [r, r+Tw) x [r, r+Th) is <= r(r+1)
+// (kernels.py:70-71).  Pixels outside are never ranked: omega is shorter and
+// denser (output-neutral: they belong to no window).
+__device__ __forceinline__ bool in_footprint(const Geom& g, int x, int y) {
+    if (!g.fp) return true;
+    const int ex = max(0, max(g.r - x, x - (g.r + g.Tw - 1)));
+    const int ey = max(0, max(g.r - y, y - (g.r + g.Th - 1)));
+    return ex * ex + ey * ey <= g.fpR2;
 }
 
 __device__ __forceinline__ uint32_t float_key(uint32_t u) {

@@ -218,79 +218,86 @@ __device__ int refine8(const PairCtx& c, int cx, int cy, int P, int cnt, int t) 
     }
 }
 
-// Both windows of a pair (columns cx and cx+1, same row) in ONE loop: a lane
-// moves on to window B as soon as A's answer block is found, so a warp
-// iterates max(steps_A + steps_B) instead of max(steps_A) + max(steps_B).  The
-// loop only locates the 8-rank block holding each answer; the bit search runs
-// once after it (inside the loop it would cost every iteration issue slots
-// whenever any lane of the warp resolves).
+// Both windows of a pair (columns cx and cx+1, same row) walk in the same
+// loop, one 8-rank step of EACH per iteration (independent work, so the two
+// LDS.128 + membership chains overlap): a warp iterates max over lanes of
+// max(steps_A, steps_B) rather than of steps_A + steps_B.  The loop only
+// locates the 8-rank block holding each answer; the bit search runs once after
+// it.  Ranks >= N hold the 0xffff sentinel, which the packed circle test and
+// the span test both place outside every window, so the last block needs no
+// mask; a walk leaving [0, N) (inconsistent state, core.py:31-36) yields -1.
+struct Walk {
+    int v0, need, step, base, k;
+    uint32_t mask, Kc, msk;
+    bool up, done;
+};
+
+__device__ __forceinline__ void walk_init(Walk& w, int P, int cnt, int t, int cx, int cy) {
+    w.up = cnt <= t;
+    w.need = w.up ? t - cnt : cnt - t - 1;
+    if (w.up) {
+        w.v0 = P & ~7;
+        w.mask = (0xffu << (P - w.v0)) & 0xffu;
+    } else {
+        w.v0 = (P - 1) & ~7;  // P == 0: v0 = -8, reported as a defect
+        w.mask = (P > 0) ? (1u << (P - w.v0)) - 1u : 0xffu;
+    }
+    w.step = w.up ? 8 : -8;
+    w.Kc = (uint32_t)((128 - cx) + ((128 - cy) << 8)) * 0x10001u;
+    w.done = false;
+    w.base = -1;
+    w.k = 0;
+    w.msk = 0;
+}
+
+template <bool CIRCLE, bool OMG>
+__device__ __forceinline__ void walk_step(const PairCtx& c, Walk& w, int cx, int cy) {
+    if (w.done) return;
+    if ((unsigned)w.v0 >= (unsigned)c.N) {  // left [0, N): defect
+        w.done = true;
+        return;
+    }
+    const uint32_t m = test8<CIRCLE, OMG>(c, w.v0, w.Kc, cx, cy) & w.mask;
+    const int pc = __popc(m);
+    if (w.need < pc) {
+        w.done = true;
+        w.base = w.v0;
+        w.msk = m;
+        w.k = w.up ? w.need : pc - 1 - w.need;
+    } else {
+        w.need -= pc;
+        w.v0 += w.step;
+        w.mask = 0xffu;
+    }
+}
+
+#ifdef IMF_STATS
+__device__ unsigned long long g_stats[256];  // [0..63] lane steps/window-pair, [64..127] warp trip counts
+#endif
+
 template <bool CIRCLE, bool OMG>
 __device__ __forceinline__ void refine8x2(const PairCtx& c, int cx, int cy, int PA, int cntA, int tA, int PB,
                                           int cntB, int tB, int& mA, int& mB) {
-    bool up;
-    int need, v0, step, P = PA, cnt = cntA, t = tA;
-    bool second = false;
-    uint32_t mask, Kc;
-    auto init = [&]() {
-        up = cnt <= t;
-        need = up ? t - cnt : cnt - t - 1;
-        if (up) {
-            v0 = P & ~7;
-            mask = (0xffu << (P - v0)) & 0xffu;
-        } else {
-            v0 = (P - 1) & ~7;  // P == 0: v0 = -8, reported as a defect below
-            mask = (P > 0) ? (1u << (P - v0)) - 1u : 0xffu;
-        }
-        step = up ? 8 : -8;
-        Kc = (uint32_t)((128 - cx) + ((128 - cy) << 8)) * 0x10001u;
-    };
-    init();
-    int baseA = -1, kA = 0, baseB = -1, kB = 0;
-    uint32_t mskA = 0, mskB = 0;
-    for (;;) {
-        if (v0 < 0 || v0 >= c.N) {  // inconsistent state (core.py:31-36)
-            if (!second) {
-                baseA = -1;
-                second = true;
-                cx += 1;
-                P = PB;
-                cnt = cntB;
-                t = tB;
-                init();
-                continue;
-            }
-            baseB = -1;
-            break;
-        }
-        uint32_t m = test8<CIRCLE, OMG>(c, v0, Kc, cx, cy) & mask;
-        if (v0 + 8 > c.N) m &= (1u << (c.N - v0)) - 1u;
-        const int pc = __popc(m);
-        if (need < pc) {
-            const int k = up ? need : pc - 1 - need;
-            if (!second) {
-                baseA = v0;
-                mskA = m;
-                kA = k;
-                second = true;
-                cx += 1;
-                P = PB;
-                cnt = cntB;
-                t = tB;
-                init();
-            } else {
-                baseB = v0;
-                mskB = m;
-                kB = k;
-                break;
-            }
-        } else {
-            need -= pc;
-            v0 += step;
-            mask = 0xffu;
-        }
-    }
-    mA = baseA < 0 ? -1 : baseA + nth_bit8(mskA, kA);
-    mB = baseB < 0 ? -1 : baseB + nth_bit8(mskB, kB);
+    Walk a, b;
+    walk_init(a, PA, cntA, tA, cx, cy);
+    walk_init(b, PB, cntB, tB, cx + 1, cy);
+#ifdef IMF_STATS
+    int nit = 0;
+#endif
+    do {
+#ifdef IMF_STATS
+        nit++;
+#endif
+        walk_step<CIRCLE, OMG>(c, a, cx, cy);
+        walk_step<CIRCLE, OMG>(c, b, cx + 1, cy);
+    } while (!(a.done && b.done));
+    mA = a.base < 0 ? -1 : a.base + nth_bit8(a.msk, a.k);
+    mB = b.base < 0 ? -1 : b.base + nth_bit8(b.msk, b.k);
+#ifdef IMF_STATS
+    atomicAdd(&g_stats[min(nit, 63)], 1ull);
+    const int mx = __reduce_max_sync(__activemask(), nit);
+    if ((threadIdx.x & 31) == __ffs(__activemask()) - 1) atomicAdd(&g_stats[64 + min(mx, 63)], 1ull);
+#endif
 }
 
 // Gather C[m] (the input value at omega[m]'s position, core.py:366) and the
@@ -420,7 +427,7 @@ __global__ void __launch_bounds__(512) k2_pair(Geom g, PairParams p, const __gri
     uint16_t* om_sh = reinterpret_cast<uint16_t*>(smem) + 8;
     const uint16_t* om = OMG ? om_g : om_sh;
     uint16_t* I = OMG ? reinterpret_cast<uint16_t*>(smem) : om_sh + Npad + 8;  // 16-byte aligned
-    const int Ipad = (N + 15) & ~7;
+    const int Ipad = (Sw * g.Sh + 15) & ~7;  // I covers the whole Sw x Sh input tile
     int* st_P = reinterpret_cast<int*>(I + Ipad);
     int* st_C = st_P + G * T;
     int* deltas = st_C + G * T;                // max(G*T, TY) entries
@@ -447,10 +454,10 @@ __global__ void __launch_bounds__(512) k2_pair(Geom g, PairParams p, const __gri
             }
         }
         if (!OMG && tid < 8) {
-            om_sh[-8 + tid] = 0;
-            om_sh[Npad + tid] = 0;
+            om_sh[-8 + tid] = 0xffffu;  // sentinels: outside every window
+            om_sh[Npad + tid] = 0xffffu;
         }
-        for (int i = N + tid; i < Ipad; i += blockDim.x) I[i] = 0;
+        for (int i = Sw * g.Sh + tid; i < Ipad; i += blockDim.x) I[i] = 0;
         if (tid < 32) hist[tid] = 0;
         for (int i = tid; i < 2 * r + 1; i += blockDim.x) span_s[i] = kt.span[i];
     }
@@ -642,8 +649,8 @@ template __global__ void k2_pair<false, false>(Geom, PairParams, const __grid_co
 template __global__ void k2_pair<true, true>(Geom, PairParams, const __grid_constant__ PairTab, const uint16_t*);
 template __global__ void k2_pair<false, true>(Geom, PairParams, const __grid_constant__ PairTab, const uint16_t*);
 
-size_t k2_pair_smem_bytes(int N, int Npad, int r, int G, int T, int TY, bool omg) {
-    const int Ipad = (N + 15) & ~7;
+size_t k2_pair_smem_bytes(int N, int Npad, int NI, int r, int G, int T, int TY, bool omg) {
+    const int Ipad = (NI + 15) & ~7;
     const int gt = G * T;
     return (omg ? 0 : 2 * (size_t)(Npad + 16)) + 2 * (size_t)Ipad +
            4 * (size_t)(2 * gt + (gt > TY ? gt : TY) + 32 + 2 * G + 2 * r + 1) + 16;
@@ -691,3 +698,14 @@ bool build_pair_tab(const int* row_dy, const int* row_xlo, const int* row_xhi, i
 }
 
 }  // namespace imf
+
+#ifdef IMF_STATS
+extern "C" int imf_stats(unsigned long long* out, int reset) {
+    if (cudaMemcpyFromSymbol(out, imf::g_stats, sizeof(imf::g_stats))) return 2;
+    if (reset) {
+        static const unsigned long long z[256] = {};
+        cudaMemcpyToSymbol(imf::g_stats, z, sizeof(z));
+    }
+    return 0;
+}
+#endif

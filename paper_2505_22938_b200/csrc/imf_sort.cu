@@ -447,7 +447,7 @@ __global__ void __launch_bounds__(1024) k1_count_reg(Geom g, uint16_t* __restric
             const long long ro = (long long)yy * g.s_y;
 #pragma unroll
             for (int k = 0; k < NK; k++) {
-                const bool ok = y < SH && lane + 32 * k < S;
+                const bool ok = y < SH && lane + 32 * k < S && in_footprint(g, lane + 32 * k, y);
                 uint32_t val = 0xffffffffu;
                 if (ok) {
                     val = DT == DT_U8 ? (uint32_t)__ldg((const uint8_t*)tc.src + ro + xo[k])
@@ -521,6 +521,7 @@ __global__ void __launch_bounds__(1024) k1_f32_bucket(Geom g, uint16_t* __restri
     const int nsw = (N + 31) >> 5;
     __shared__ int s_max;
     uint32_t v[NK][NK];
+    unsigned long long okm = 0;  // which of this thread's pixels are ranked
     {
         long long xo[NK];
 #pragma unroll
@@ -537,8 +538,9 @@ __global__ void __launch_bounds__(1024) k1_f32_bucket(Geom g, uint16_t* __restri
             const long long ro = (long long)yy * g.s_y;
 #pragma unroll
             for (int k = 0; k < NK; k++) {
-                const bool ok = y < SH && lane + 32 * k < S;
+                const bool ok = y < SH && lane + 32 * k < S && in_footprint(g, lane + 32 * k, y);
                 v[j][k] = ok ? float_key(__ldg((const uint32_t*)tc.src + ro + xo[k])) : 0u;
+                okm |= (ok ? 1ull : 0ull) << (j * NK + k);
             }
         }
     }
@@ -554,7 +556,7 @@ __global__ void __launch_bounds__(1024) k1_f32_bucket(Geom g, uint16_t* __restri
     for (int j = 0; j < NK; j++)
 #pragma unroll
         for (int k = 0; k < NK; k++)
-            if (wid + 32 * j < SH && lane + 32 * k < S) {
+            if ((okm >> (j * NK + k)) & 1ull) {
                 const uint32_t h = v[j][k] >> 16, sh = (h & 1) << 4;
                 const uint32_t old = atomicAdd(&hw[h >> 1], 1u << sh);
                 mx = max(mx, (int)((old >> sh) & 0xffffu) + 1);
@@ -572,7 +574,7 @@ __global__ void __launch_bounds__(1024) k1_f32_bucket(Geom g, uint16_t* __restri
     for (int j = 0; j < NK; j++)
 #pragma unroll
         for (int k = 0; k < NK; k++)
-            if (wid + 32 * j < SH && lane + 32 * k < S) {
+            if ((okm >> (j * NK + k)) & 1ull) {
                 const uint32_t key = v[j][k], h = key >> 16, sh = (h & 1) << 4;
                 const uint32_t old = atomicAdd(&hw[h >> 1], 1u << sh);
                 ent[(old >> sh) & 0xffffu] = (key << 16) | (uint32_t)((lane + 32 * k) | ((wid + 32 * j) << 8));
