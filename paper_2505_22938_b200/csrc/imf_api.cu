@@ -43,6 +43,7 @@ struct Plan {
     int G, k2_threads, k1_threads, paired;
     bool k1_gmem, k1_count, omg;
     bool k1_f32b;         // f32 bucket ordinal transform (+ k1_sort fallback on flagged tiles)
+    bool k1_f32b_g;       // ... with the bucket entries in a global scratch slot per tile
     size_t k1b_smem;
     int full_out_h;
     int hs;     // k2_pair: ordinal image holds rank >> hs
@@ -189,11 +190,18 @@ int make_plan(const imf_image* src, const imf_kernel* k, const imf_options* opt,
     p.k1_count = g.dtype != DT_F32 && k1_count_smem_bytes(g.dtype, g.Npad) <= kSmemMax;
     p.k1b_smem = k1_f32_bucket_smem_bytes(g.N);
     p.k1_f32b = g.dtype == DT_F32 && env_int("IMF_F32_BUCKET", 1) && g.Sw <= 160 && p.k1b_smem <= kSmemMax;
+    if (g.dtype == DT_F32 && !p.k1_f32b && env_int("IMF_F32_BUCKET", 1)) {
+        p.k1_f32b = p.k1_f32b_g = true;
+        p.k1b_smem = k1_f32_bucket_g_smem_bytes(g.N);
+    }
     p.k1_threads = p.k1_count ? kK1Threads : kK1SortThreads;
     p.k1_gmem = !p.k1_count && k1_smem_bytes(g.dtype, g.Npad, p.k1_threads / 32, false) > kSmemMax;
     p.k1_smem = p.k1_count ? k1_count_smem_bytes(g.dtype, g.Npad)
                            : k1_smem_bytes(g.dtype, g.Npad, p.k1_threads / 32, p.k1_gmem);
     p.k1_gs_per_tile = p.k1_gmem ? k1_gscratch_bytes(g.dtype, g.Npad) : 0;
+    // the global-entries bucket kernel needs 4 B per pixel; the LSD fallback
+    // reuses the same slot (k1_gscratch_bytes(f32) = 6 B per pixel when it needs one)
+    if (p.k1_f32b_g) p.k1_gs_per_tile = std::max(p.k1_gs_per_tile, (size_t)4 * g.Npad);
 
     // Rounded-rect footprint (pair path, circle kernels, register-resident K1):
     // rank only input pixels within distance^2 r(r+1) of the output rectangle
@@ -310,6 +318,7 @@ cudaError_t set_attrs() {
     if (!e) e = allow_smem(k1_f32_bucket<3>, optin);
     if (!e) e = allow_smem(k1_f32_bucket<4>, optin);
     if (!e) e = allow_smem(k1_f32_bucket<5>, optin);
+    if (!e) e = allow_smem(k1_f32_bucket_g, optin);
     if (!e) e = allow_smem(k2_select<true, false>, optin);
     if (!e) e = allow_smem(k2_select<false, false>, optin);
     if (!e) e = allow_smem(k2_select<true, true>, optin);
@@ -329,6 +338,9 @@ void launch_k1(const Plan& p, const Geom& g, int nblocks, uint16_t* omega, unsig
     if (p.k1_f32b) {
         const dim3 b1024(1024);
         cudaMemsetAsync(flags, 0, sizeof(int), s);  // fallback list count
+        if (p.k1_f32b_g)
+            k1_f32_bucket_g<<<grid, b1024, p.k1b_smem, s>>>(g, omega, flags, (uint32_t*)k1g, gs / 4);
+        else
         switch ((g.Sw + 31) >> 5) {
             case 1: k1_f32_bucket<1><<<grid, b1024, p.k1b_smem, s>>>(g, omega, flags); break;
             case 2: k1_f32_bucket<2><<<grid, b1024, p.k1b_smem, s>>>(g, omega, flags); break;

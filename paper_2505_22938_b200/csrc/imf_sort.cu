@@ -243,7 +243,8 @@ __global__ void __launch_bounds__(1024) k1_sort(Geom g, uint16_t* __restrict__ o
 // word, so every shared access is bank-conflict free.  Ends with the counters
 // replaced by their exclusive prefix (no trailing barrier).
 __device__ __forceinline__ void hist16_exclusive_scan(uint32_t* hw, const int NW,
-                                                      uint32_t* starts = nullptr) {
+                                                      uint32_t* starts = nullptr,
+                                                      unsigned long long* sumsq = nullptr) {
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
     __shared__ uint32_t wt[32];
     const int per = NW / nw;  // words per warp (NW and nw are powers of two)
@@ -291,12 +292,18 @@ __device__ __forceinline__ void hist16_exclusive_scan(uint32_t* hw, const int NW
             const uint32_t b2 = base + (p2 & 0xffffu) + (p2 >> 16), b3 = base + (p3 & 0xffffu) + (p3 >> 16);
             if (starts) {  // bit at every non-empty counter's first position (bucket starts)
                 const uint32_t cw[4] = {q.x, q.y, q.z, q.w}, bw[4] = {b0, b1, b2, b3};
+                unsigned long long sq = 0;
 #pragma unroll
                 for (int k = 0; k < 4; k++) {
-                    const uint32_t lo = cw[k] & 0xffffu, e0 = bw[k], e1 = bw[k] + lo;
+                    const uint32_t lo = cw[k] & 0xffffu, hi = cw[k] >> 16, e0 = bw[k], e1 = bw[k] + lo;
                     if (lo) atomicOr(&starts[e0 >> 5], 1u << (e0 & 31));
-                    if (cw[k] >> 16) atomicOr(&starts[e1 >> 5], 1u << (e1 & 31));
+                    if (hi) atomicOr(&starts[e1 >> 5], 1u << (e1 & 31));
+                    sq += (unsigned long long)(lo * lo) + (unsigned long long)(hi * hi);
                 }
+                // clamp per lane at 2^26 (> kMaxSumSq: the tile falls back anyway) so
+                // the 32-bit warp sum cannot wrap
+                const unsigned wsq = __reduce_add_sync(0xffffffffu, (unsigned)min(sq, 1ull << 26));
+                if (lane == 0 && wsq) atomicAdd(sumsq, (unsigned long long)wsq);
             }
             q.x = b0 | ((b0 + (q.x & 0xffffu)) << 16);
             q.y = b1 | ((b1 + (q.y & 0xffffu)) << 16);
@@ -505,7 +512,9 @@ IMF_K1R(DT_U16)
 // break by position (output-neutral).  Cost ~ sum of squared bucket sizes: a
 // tile whose largest bucket exceeds kMaxBucket (narrow value range, flat
 // regions) writes flag 1 and no omega; a k1_sort launch redoes those tiles.
-constexpr int kMaxBucket = 256;
+// Ranking cost is sum(n_b^2) entry compares per tile; above this (about 60K per
+// thread of a 1024-thread CTA) the tile goes to the LSD radix sort instead.
+constexpr unsigned long long kMaxSumSq = 64ull << 20;
 
 template <int NK>
 __global__ void __launch_bounds__(1024) k1_f32_bucket(Geom g, uint16_t* __restrict__ omega_out,
@@ -519,7 +528,7 @@ __global__ void __launch_bounds__(1024) k1_f32_bucket(Geom g, uint16_t* __restri
     uint32_t* ent = hw + NW;                  // N entries
     uint32_t* starts = ent + ((N + 3) & ~3);  // bucket-start bitmap, ceil(N/32) words
     const int nsw = (N + 31) >> 5;
-    __shared__ int s_max;
+    __shared__ unsigned long long s_sumsq;
     uint32_t v[NK][NK];
     unsigned long long okm = 0;  // which of this thread's pixels are ranked
     {
@@ -548,28 +557,24 @@ __global__ void __launch_bounds__(1024) k1_f32_bucket(Geom g, uint16_t* __restri
         uint4* h4 = reinterpret_cast<uint4*>(hw);
         for (int i = tid; i < NW / 4; i += blockDim.x) h4[i] = make_uint4(0, 0, 0, 0);
         for (int i = tid; i < nsw; i += blockDim.x) starts[i] = 0;
-        if (tid == 0) s_max = 0;
+        if (tid == 0) s_sumsq = 0;
     }
     __syncthreads();
-    int mx = 0;
 #pragma unroll
     for (int j = 0; j < NK; j++)
 #pragma unroll
         for (int k = 0; k < NK; k++)
             if ((okm >> (j * NK + k)) & 1ull) {
                 const uint32_t h = v[j][k] >> 16, sh = (h & 1) << 4;
-                const uint32_t old = atomicAdd(&hw[h >> 1], 1u << sh);
-                mx = max(mx, (int)((old >> sh) & 0xffffu) + 1);
+                atomicAdd(&hw[h >> 1], 1u << sh);
             }
-    mx = __reduce_max_sync(0xffffffffu, mx);
-    if (lane == 0) atomicMax(&s_max, mx);
     __syncthreads();
-    if (s_max > kMaxBucket) {  // block-uniform: hand the tile to the radix sort
+    hist16_exclusive_scan(hw, NW, starts, &s_sumsq);
+    __syncthreads();
+    if (s_sumsq > kMaxSumSq) {  // block-uniform: hand the tile to the radix sort
         if (tid == 0) fallback[1 + atomicAdd(fallback, 1)] = blockIdx.x;
         return;
     }
-    hist16_exclusive_scan(hw, NW, starts);
-    __syncthreads();
 #pragma unroll
     for (int j = 0; j < NK; j++)
 #pragma unroll
@@ -599,6 +604,93 @@ __global__ void __launch_bounds__(1024) k1_f32_bucket(Geom g, uint16_t* __restri
     __syncthreads();
     store_omega(g, om, omega_slot(g, omega_out));
 }
+
+// k1_f32_bucket for tiles too large for shared-memory entries (N > ~23.7K,
+// e.g. r >= 54): the bucket-ordered entries live in the tile's global scratch
+// slot (L2-resident: written once, read bucket by bucket), the keys are read
+// from the image twice instead of held in registers, and only the 128 KB
+// histogram (later omega) and the bucket-start bitmap stay in shared memory.
+__global__ void __launch_bounds__(1024) k1_f32_bucket_g(Geom g, uint16_t* __restrict__ omega_out,
+                                                       int* __restrict__ fallback,
+                                                       uint32_t* __restrict__ gent, long long gent_stride) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    constexpr int NW = 32768;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+    const TileCoord tc = tile_coord(g, g.tile_begin + blockIdx.x);
+    const int S = g.Sw, SH = g.Sh, N = g.N;
+    uint32_t* hw = reinterpret_cast<uint32_t*>(smem);
+    uint32_t* starts = hw + NW;
+    const int nsw = (N + 31) >> 5;
+    uint32_t* ent = gent + blockIdx.x * gent_stride;
+    __shared__ unsigned long long s_sumsq;
+    {
+        uint4* h4 = reinterpret_cast<uint4*>(hw);
+        for (int i = tid; i < NW / 4; i += blockDim.x) h4[i] = make_uint4(0, 0, 0, 0);
+        for (int i = tid; i < nsw; i += blockDim.x) starts[i] = 0;
+        if (tid == 0) s_sumsq = 0;
+    }
+    __syncthreads();
+    const int nk = (S + 31) >> 5;
+    for (int y = wid; y < SH; y += nw) {
+        int yy = tc.oy0 + y - g.r + g.vshift;
+        yy = yy < 0 ? 0 : (yy >= g.H ? g.H - 1 : yy);
+        const char* rp = tc.src + (long long)yy * g.s_y * 4;
+        for (int k = 0; k < nk; k++) {
+            const int x = lane + 32 * k;
+            if (x < S) {
+                int xx = tc.ox0 + x - g.r + g.vshift;
+                xx = xx < 0 ? 0 : (xx >= g.W ? g.W - 1 : xx);
+                const uint32_t h = float_key(__ldg((const uint32_t*)rp + (long long)xx * g.s_x)) >> 16;
+                const uint32_t sh = (h & 1) << 4;
+                atomicAdd(&hw[h >> 1], 1u << sh);
+            }
+        }
+    }
+    __syncthreads();
+    hist16_exclusive_scan(hw, NW, starts, &s_sumsq);
+    __syncthreads();
+    if (s_sumsq > kMaxSumSq) {
+        if (tid == 0) fallback[1 + atomicAdd(fallback, 1)] = blockIdx.x;
+        return;
+    }
+    for (int y = wid; y < SH; y += nw) {
+        int yy = tc.oy0 + y - g.r + g.vshift;
+        yy = yy < 0 ? 0 : (yy >= g.H ? g.H - 1 : yy);
+        const char* rp = tc.src + (long long)yy * g.s_y * 4;
+        for (int k = 0; k < nk; k++) {
+            const int x = lane + 32 * k;
+            if (x < S) {
+                int xx = tc.ox0 + x - g.r + g.vshift;
+                xx = xx < 0 ? 0 : (xx >= g.W ? g.W - 1 : xx);
+                const uint32_t key = float_key(__ldg((const uint32_t*)rp + (long long)xx * g.s_x));
+                const uint32_t h = key >> 16, sh = (h & 1) << 4;
+                const uint32_t old = atomicAdd(&hw[h >> 1], 1u << sh);
+                ent[(old >> sh) & 0xffffu] = (key << 16) | (uint32_t)(x | (y << 8));
+            }
+        }
+    }
+    __syncthreads();  // block-scope ordering of the entry stores (global, same CTA)
+    uint16_t* om = reinterpret_cast<uint16_t*>(hw);
+    for (int sp = tid; sp < N; sp += blockDim.x) {
+        const uint32_t e = ent[sp];
+        int w = sp >> 5;
+        uint32_t m = starts[w] & (0xffffffffu >> (31 - (sp & 31)));
+        while (!m) m = starts[--w];
+        const int b0 = (w << 5) + 31 - __clz(m);
+        w = sp >> 5;
+        m = (sp & 31) == 31 ? 0u : starts[w] & (0xfffffffeu << (sp & 31));
+        while (!m && ++w < nsw) m = starts[w];
+        const int b1 = m ? (w << 5) + __ffs(m) - 1 : N;
+        int rk = b0;
+        for (int q = b0; q < b1; q++) rk += ent[q] < e ? 1 : 0;
+        om[rk] = (uint16_t)(e & 0xffffu);
+    }
+    for (int i = N + tid; i < g.Npad; i += blockDim.x) om[i] = 0xffffu;
+    __syncthreads();
+    store_omega(g, om, omega_slot(g, omega_out));
+}
+
+size_t k1_f32_bucket_g_smem_bytes(int N) { return 32768 * 4 + 4 * (size_t)((N + 31) >> 5) + 16; }
 
 template __global__ void k1_f32_bucket<1>(Geom, uint16_t*, int*);
 template __global__ void k1_f32_bucket<2>(Geom, uint16_t*, int*);
