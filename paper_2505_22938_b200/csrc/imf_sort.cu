@@ -18,6 +18,8 @@
 //   f32: 4 byte passes on the u32 order key (1 unstable)  smem ~8N bytes
 // When the tile does not fit shared memory, the large arrays live in a
 // per-CTA global scratch slot (L2-resident) -- same code, GMEM=true.
+#include <algorithm>
+
 #include "imf_common.cuh"
 
 namespace imf {
@@ -349,6 +351,15 @@ __device__ __forceinline__ void hist16_exclusive_scan(uint32_t* hw, const int NW
         }
         const uint32_t ex = carry + incl - tot;
         if (ok) wb[i0 + lane] = ex | ((ex + lo) << 16);
+        if (starts && ok) {  // bucket starts, as in the chunked branch
+            const uint32_t hi = w >> 16;
+            if (lo) atomicOr(&starts[ex >> 5], 1u << (ex & 31));
+            if (hi) atomicOr(&starts[(ex + lo) >> 5], 1u << ((ex + lo) & 31));
+            if (sumsq) {
+                const unsigned long long sq = (unsigned long long)lo * lo + (unsigned long long)hi * hi;
+                atomicAdd(sumsq, sq);
+            }
+        }
         carry += __shfl_sync(0xffffffffu, incl, 31);
     }
 }
@@ -503,6 +514,7 @@ __global__ void __launch_bounds__(1024) k1_count_reg(Geom g, uint16_t* __restric
 IMF_K1R(DT_U8)
 IMF_K1R(DT_U16)
 #undef IMF_K1R
+
 
 // f32 ordinal transform by buckets: count-sort the u32 order keys (ordinal.py:
 // 109-123) by their HIGH 16 bits with the u16 machinery (register-resident tile,
