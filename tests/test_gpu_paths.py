@@ -1,0 +1,70 @@
+"""Every alternate engine path stays bit-exact (the planner picks one per
+geometry; environment switches force the others on the same inputs).
+
+Paths: pair fast path vs the generic selection kernel (IMF_PAIR), omega in
+shared memory vs in L2 (IMF_PAIR_OMG), rounded-rect footprint on/off
+(IMF_FOOTPRINT), f32 bucket transform vs LSD radix sort (IMF_F32_BUCKET),
+register-resident vs two-pass u16 counting sort (IMF_K1REG), the pair path on
+non-circle kernels (IMF_PAIR_ANY), rectangular pair tiles (IMF_PAIR_RECT),
+and tile / seed-row overrides.  Compared against the C oracle, which is itself
+pinned to the reference's golden outputs (tests/test_oracle.py)."""
+import os
+
+import numpy as np
+import pytest
+
+import cases as C
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+VARIANTS = [
+    {},
+    {"IMF_PAIR": "0"},
+    {"IMF_PAIR_OMG": "1"},
+    {"IMF_FOOTPRINT": "0"},
+    {"IMF_F32_BUCKET": "0"},
+    {"IMF_K1REG": "0"},
+    {"IMF_PAIR_ANY": "1"},
+    {"IMF_PAIR_RECT": "1", "IMF_TILE": "64"},
+    {"IMF_TILE": "40", "IMF_SEED_ROWS": "4"},
+    {"IMF_STRIPE_EDGE": "1", "IMF_STRIPE_MID": "5"},
+]
+
+CASES = [  # (dtype, shape, kernel spec)
+    ("uint16", (211, 301, 3), ("circle", 48, 0, 0.0)),
+    ("uint16", (150, 170), ("circle", 62, 0, 0.0)),       # halved ranks (N > 32768)
+    ("float32", (180, 200), ("circle", 20, 0, 0.0)),
+    ("float32", (260, 240), ("circle", 60, 0, 0.0)),      # f32 global-entries bucket
+    ("uint8", (190, 170, 2), ("regular_polygon", 11, 6, 15.0)),
+    ("uint8", (120, 130), ("square", 7, 0, 0.0)),
+]
+
+
+def _input(dt, shape, seed):
+    rng = np.random.default_rng(seed)
+    if dt == "float32":
+        img = rng.standard_normal(shape).astype(np.float32)
+        img[:, :5] = 0.25  # a flat band: ties and a large bucket
+        return img
+    hi = np.iinfo(dt).max + 1
+    img = rng.integers(0, hi, shape).astype(dt)
+    img[:9] = img[0, 0]     # flat rows: ties across the tile
+    return img
+
+
+@pytest.mark.parametrize("variant", VARIANTS, ids=lambda v: ",".join(f"{k}={x}" for k, x in v.items()) or "default")
+def test_variant_bit_exact(variant, monkeypatch):
+    from paper_2505_22938_b200 import FilterParams, ShapeSpec, filter_image
+    for k, v in variant.items():
+        monkeypatch.setenv(k, v)
+    for i, (dt, shape, spec) in enumerate(CASES):
+        img = _input(dt, shape, i)
+        for boundary in ("replicate", "valid"):
+            if boundary == "valid" and min(shape[:2]) <= 2 * spec[1]:
+                continue
+            for p in (0.5, 0.13):
+                params = FilterParams(shape=ShapeSpec(*spec), percentile=p, boundary=boundary)
+                got = filter_image(img, params)
+                want = oracle.fast_filter(img, params.shape, p, boundary)
+                assert got.tobytes() == want.tobytes(), (variant, dt, shape, spec, boundary, p)
