@@ -50,7 +50,8 @@ struct Plan {
     bool pair;  // K2 fast path (imf_pair.cu): two windows per thread, 15-bit ranks
     size_t k1_smem, k2_smem, k1_gs_per_tile;
     long long total_tiles, chunk_tiles;
-    size_t ws_ktab, ws_omega, ws_k1g, ws_flags, ws_total;
+    size_t ws_ktab, ws_omega, ws_k1g, ws_flags, ws_lane, ws_total;
+    int lanes;  // chunk streams (1 or 2)
     int ktab_n;
 };
 
@@ -235,7 +236,14 @@ int make_plan(const imf_image* src, const imf_kernel* k, const imf_options* opt,
     p.ktab_n = 2 * k->ncols + 2 * k->nrows + 2 * r + 1;
     const size_t slot = 2 * (size_t)(g.Npad + 2 * OMEGA_SLOT_PAD);
     const size_t per_tile = slot + p.k1_gs_per_tile;
-    long long chunk = (long long)(kOmegaScratchTarget / per_tile);
+    // Two lanes (streams) alternate chunks when there are enough tiles: each
+    // lane's K1 fills the other's K2 tail.  The omega scratch target is split
+    // between them; each lane has its own scratch, k1 scratch and flag list.
+    // Chunks below ~2 full K2 waves (2 x 296 CTAs) leave the GPU idle, so two
+    // lanes only when there are >= 4 such chunks' worth of tiles.
+    p.lanes = (p.total_tiles >= 4 * 296 && env_int("IMF_LANES", 2) > 1) ? 2 : 1;
+    long long chunk = (long long)(kOmegaScratchTarget / p.lanes / per_tile);
+    if (p.lanes == 2) chunk = std::min<long long>(chunk, std::max<long long>(592, (p.total_tiles + 5) / 6));
     chunk = std::max<long long>(chunk, 148);
     chunk = std::min<long long>(chunk, p.total_tiles);
     chunk = std::min<long long>(chunk, 65535LL * 1024);
@@ -244,7 +252,8 @@ int make_plan(const imf_image* src, const imf_kernel* k, const imf_options* opt,
     p.ws_omega = (((size_t)chunk * slot) + 255) & ~(size_t)255;
     p.ws_k1g = (size_t)chunk * p.k1_gs_per_tile;
     p.ws_flags = p.k1_f32b ? (((size_t)(chunk + 1) * 4 + 255) & ~(size_t)255) : 0;
-    p.ws_total = kStatusBytes + p.ws_ktab + p.ws_omega + p.ws_k1g + p.ws_flags;
+    p.ws_lane = p.ws_omega + p.ws_k1g + p.ws_flags;
+    p.ws_total = kStatusBytes + p.ws_ktab + p.lanes * p.ws_lane;
     return IMF_OK;
 }
 
@@ -433,9 +442,7 @@ static int filter_impl(const imf_image* src, imf_image* dsts, int n, const int32
     unsigned char* ws = (unsigned char*)workspace;
     int* status = (int*)ws;
     int* ktab_d = (int*)(ws + kStatusBytes);
-    uint16_t* omega = (uint16_t*)(ws + kStatusBytes + p.ws_ktab);
-    unsigned char* k1g = ws + kStatusBytes + p.ws_ktab + p.ws_omega;
-    int* k1flags = (int*)(ws + kStatusBytes + p.ws_ktab + p.ws_omega + p.ws_k1g);
+    unsigned char* lane_base[2] = {ws + kStatusBytes + p.ws_ktab, ws + kStatusBytes + p.ws_ktab + p.ws_lane};
 
     static thread_local KTab kt;
     build_ktab_struct(kernel, p.g.Sw, kt);
@@ -480,9 +487,35 @@ static int filter_impl(const imf_image* src, imf_image* dsts, int n, const int32
     // sums in imf_profile_last().  Used by bench.py for the roofline figure.
     const bool prof = (opt->flags & IMF_FLAG_PROFILE) != 0;
     std::vector<cudaEvent_t> ev;
-    for (long long t0 = 0; t0 < p.total_tiles; t0 += p.chunk_tiles) {
+    // second lane: fork from s, join back into s at the end (stream-ordered API)
+    const int lanes = prof ? 1 : p.lanes;
+    cudaStream_t ls[2] = {s, nullptr};
+    cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+    if (lanes == 2) {
+        static thread_local cudaStream_t lane2 = nullptr;
+        static thread_local int lane2_dev = -1;
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (lane2_dev != dev) {
+            if (cudaError_t e = cudaStreamCreateWithFlags(&lane2, cudaStreamNonBlocking))
+                return cuda_fail(e, "lane stream");
+            lane2_dev = dev;
+        }
+        ls[1] = lane2;
+        cudaEventCreateWithFlags(&fork_ev, cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&join_ev, cudaEventDisableTiming);
+        cudaEventRecord(fork_ev, s);  // after the status memset
+        cudaStreamWaitEvent(ls[1], fork_ev, 0);
+    }
+    int ci = 0;
+    for (long long t0 = 0; t0 < p.total_tiles; t0 += p.chunk_tiles, ci++) {
         const int nb = (int)std::min(p.chunk_tiles, p.total_tiles - t0);
         g.tile_begin = t0;
+        const int li = lanes == 2 ? (ci & 1) : 0;
+        cudaStream_t s = ls[li];
+        uint16_t* omega = (uint16_t*)lane_base[li];
+        unsigned char* k1g = lane_base[li] + p.ws_omega;
+        int* k1flags = (int*)(lane_base[li] + p.ws_omega + p.ws_k1g);
         cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr;
         if (prof) {
             cudaEventCreate(&e0);
@@ -524,6 +557,12 @@ static int filter_impl(const imf_image* src, imf_image* dsts, int n, const int32
             ev.push_back(e2);
         }
         g_launches += 1 + n;
+    }
+    if (lanes == 2) {
+        cudaEventRecord(join_ev, ls[1]);
+        cudaStreamWaitEvent(s, join_ev, 0);
+        cudaEventDestroy(fork_ev);  // released once the recorded work completes
+        cudaEventDestroy(join_ev);
     }
     if (cudaError_t e = cudaGetLastError()) return cuda_fail(e, "kernel launch");
     if (prof) {

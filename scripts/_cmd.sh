@@ -1,2 +1,4 @@
 python -c "from paper_2505_22938_b200 import build as b; assert not b.stale(), \"stale .so\"" || exit 3
-for e in "IMF_STRIPE_EDGE=1 IMF_STRIPE_MID=8" "IMF_STRIPE_EDGE=1 IMF_STRIPE_MID=12" "IMF_STRIPE_EDGE=2 IMF_STRIPE_MID=8" "IMF_STRIPE_EDGE=1 IMF_STRIPE_MID=16" "IMF_STRIPE_EDGE=1 IMF_STRIPE_MID=6" "IMF_STRIPE_LANES=3 IMF_STRIPE_EDGE=1 IMF_STRIPE_MID=8"; do echo $e; env $e timeout 300 python scripts/quick_e2e.py 0; done
+timeout 900 python -m pytest tests -x -q -m gpu 2>&1 | tail -2
+timeout 600 python scripts/quick_bench.py c1 c2 c3 c4 c5 | cut -c1-120
+timeout 300 python scripts/quick_e2e.py 0
