@@ -40,7 +40,7 @@ constexpr size_t kOmegaScratchTarget = 96ull << 20;  // stays mostly L2-resident
 
 struct Plan {
     Geom g;
-    int G, k2_threads, k1_threads, paired;
+    int G, k2_threads, k1_threads;
     bool k1_gmem, k1_count, omg;
     bool k1_f32b;         // f32 bucket ordinal transform (+ k1_sort fallback on flagged tiles)
     bool k1_f32b_g;       // ... with the bucket entries in a global scratch slot per tile
@@ -50,9 +50,8 @@ struct Plan {
     bool pair;  // K2 fast path (imf_pair.cu): two windows per thread, 15-bit ranks
     size_t k1_smem, k2_smem, k1_gs_per_tile;
     long long total_tiles, chunk_tiles;
-    size_t ws_ktab, ws_omega, ws_k1g, ws_flags, ws_lane, ws_total;
+    size_t ws_omega, ws_k1g, ws_flags, ws_lane, ws_total;
     int lanes;  // chunk streams (1 or 2)
-    int ktab_n;
 };
 
 int env_int(const char* name, int dflt) {
@@ -94,7 +93,6 @@ int make_plan(const imf_image* src, const imf_kernel* k, const imf_options* opt,
         const int tb = (154 - 2 * r) & ~1;  // S <= 154: hist + 4.125 N bytes fit
         if (tb >= 48) Tmax = std::min(Tmax, tb);
     }
-    const int paired = env_int("IMF_PAIRED", 0);
     double best = -1.0;
     // K2 fast path: tile ranks < 2^15 (S <= 181), even T, and T + r <= 128 for
     // the packed circle test.  Largest such tile.
@@ -145,8 +143,7 @@ int make_plan(const imf_image* src, const imf_kernel* k, const imf_options* opt,
         const int S = T + 2 * r;
         const int N = S * S, Npad = (N + 63) & ~63;
         const int G = std::max(1, std::min(G0, T));
-        const int thr = std::min(((T * G * (paired ? 1 : 2) + 31) / 32) * 32, 512);
-        if (paired && T * G > 512) continue;
+        const int thr = std::min(((T * G * 2 + 31) / 32) * 32, 512);
         for (int omg = 0; omg < 2; omg++) {
             const size_t k2s = k2_smem_bytes(N, Npad, k->ncols, k->nrows, r, G, T, T, omg != 0);
             if (k2s > kSmemMax) continue;
@@ -158,7 +155,6 @@ int make_plan(const imf_image* src, const imf_kernel* k, const imf_options* opt,
                 p.g.N = N;
                 p.g.Npad = Npad;
                 p.G = G;
-                p.paired = paired;
                 p.k2_threads = thr;
                 p.k2_smem = k2s;
                 p.omg = omg != 0;
@@ -233,7 +229,6 @@ int make_plan(const imf_image* src, const imf_kernel* k, const imf_options* opt,
         p.k1_smem = k1_count_smem_bytes(g.dtype, g.Npad);
     }
 
-    p.ktab_n = 2 * k->ncols + 2 * k->nrows + 2 * r + 1;
     const size_t slot = 2 * (size_t)(g.Npad + 2 * OMEGA_SLOT_PAD);
     const size_t per_tile = slot + p.k1_gs_per_tile;
     // Two lanes (streams) alternate chunks when there are enough tiles: each
@@ -248,12 +243,11 @@ int make_plan(const imf_image* src, const imf_kernel* k, const imf_options* opt,
     chunk = std::min<long long>(chunk, p.total_tiles);
     chunk = std::min<long long>(chunk, 65535LL * 1024);
     p.chunk_tiles = chunk;
-    p.ws_ktab = ((size_t)p.ktab_n * 4 + 255) & ~(size_t)255;
     p.ws_omega = (((size_t)chunk * slot) + 255) & ~(size_t)255;
     p.ws_k1g = (size_t)chunk * p.k1_gs_per_tile;
     p.ws_flags = p.k1_f32b ? (((size_t)(chunk + 1) * 4 + 255) & ~(size_t)255) : 0;
     p.ws_lane = p.ws_omega + p.ws_k1g + p.ws_flags;
-    p.ws_total = kStatusBytes + p.ws_ktab + p.lanes * p.ws_lane;
+    p.ws_total = kStatusBytes + p.lanes * p.ws_lane;
     return IMF_OK;
 }
 
@@ -270,24 +264,6 @@ void build_ktab_struct(const imf_kernel* k, int Sw, KTab& t) {
     }
 }
 
-void build_ktab(const imf_kernel* k, int Sw, std::vector<int>& t) {
-    const int r = k->radius;
-    t.assign(2 * k->ncols + 2 * k->nrows + 2 * r + 1, 0);
-    int o = 0;
-    for (int i = 0; i < k->ncols; i++) {
-        t[o++] = (k->col_ybot[i] + 1) * Sw + k->col_dx[i];  // VE: entering on a down slide
-        t[o++] = k->col_ytop[i] * Sw + k->col_dx[i];        // VX: exiting on a down slide
-    }
-    for (int i = 0; i < k->nrows; i++) {
-        t[o++] = k->row_dy[i] * Sw + k->row_xhi[i];  // HP: entering on a right slide
-        t[o++] = k->row_dy[i] * Sw + k->row_xlo[i];  // HM: exiting on a right slide
-    }
-    for (int i = 0; i < k->nrows; i++) {
-        const int dy = k->row_dy[i];
-        const int w = k->row_xhi[i] - k->row_xlo[i];
-        t[o + dy + r] = (k->row_xlo[i] & 0xffff) | (w << 16);
-    }
-}
 
 bool g_attr_done = false;
 
@@ -441,8 +417,7 @@ static int filter_impl(const imf_image* src, imf_image* dsts, int n, const int32
 
     unsigned char* ws = (unsigned char*)workspace;
     int* status = (int*)ws;
-    int* ktab_d = (int*)(ws + kStatusBytes);
-    unsigned char* lane_base[2] = {ws + kStatusBytes + p.ws_ktab, ws + kStatusBytes + p.ws_ktab + p.ws_lane};
+    unsigned char* lane_base[2] = {ws + kStatusBytes, ws + kStatusBytes + p.ws_lane};
 
     static thread_local KTab kt;
     build_ktab_struct(kernel, p.g.Sw, kt);
@@ -461,8 +436,6 @@ static int filter_impl(const imf_image* src, imf_image* dsts, int n, const int32
     sp.target = targets[0];
     sp.tmap = target_map;
     sp.G = p.G;
-    sp.paired = p.paired;
-    sp.ktab = ktab_d;
     sp.status = status;
 
     static thread_local PairTab ptab;

@@ -8,10 +8,10 @@
 //   key       u32 order key of a pixel: the value for u8/u16, the float order key
 //             for f32 (ordinal.py:109-123) -- no float compare ever runs on device.
 //   omega     the rank -> position map (the paper's omnigram), u16 per rank,
-//             packed x | y << 8 (ordinal.py:56-59); S_w, S_h <= 256.
-//   Iq        the quantized ordinal image: Iq[y*S_w + x] = clamp((rank >> qs) - qb, 0, 255).
-//             Comparisons against pivots that are multiples of 2^qs with
-//             (pivot >> qs) - qb in [1, 255] are exact.
+//             packed x | y << 8 (ordinal.py:56-59); S_w, S_h <= 255.
+//   I         the ordinal image: I[y*S_w + x] = rank of input-tile pixel (x, y)
+//             (rank >> 1 in the pair kernel's halved mode, compared only
+//             against even pivots).
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -62,8 +62,6 @@ struct SelParams {
     int target;          // scalar target rank (tiling.py:176-177 / kernels.py:191-192)
     const int* tmap;     // per-pixel target ranks [out_h*out_w] or nullptr
     int G;               // seed rows per tile
-    int paired;          // 1: one thread slides a window down and one up (phase D)
-    const int* ktab;     // [ncols pairs (VE,VX)][nrows pairs (HP,HM)][2r+1 spans]
     int* status;         // device status word (1 = scan defect)
 };
 
@@ -131,15 +129,6 @@ __device__ __forceinline__ uint32_t load_key(const Geom& g, const TileCoord& tc,
 __device__ __forceinline__ void lin_to_xy(int i, int Sw, float invS, int& x, int& y) {
     y = __float2int_rz(((float)i + 0.5f) * invS);
     x = i - y * Sw;
-}
-
-// omega is stored in 128-byte segments (64 ranks); the eight 16-byte chunks of
-// segment s are XOR-swizzled by (s & 7) so that lanes scanning different
-// segments with 16-byte loads hit different bank groups.
-__device__ __forceinline__ int omega_index(int v) {
-    int s = v >> 6, w = v & 63;
-    int chunk = (w >> 3) ^ (s & 7);
-    return (s << 6) | (chunk << 3) | (w & 7);
 }
 
 __device__ __forceinline__ unsigned lanemask_lt() {

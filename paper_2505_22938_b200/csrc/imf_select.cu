@@ -169,24 +169,6 @@ __device__ __forceinline__ int slide_delta(const unsigned char* __restrict__ Ib,
     return swap ? (int)eout - (int)ein : (int)ein - (int)eout;
 }
 
-// Two slides through the same column table: a down slide at base bd (pivot
-// Pd) and an up slide at base bu (pivot Pu), sharing every offset load.
-__device__ __forceinline__ void slide_delta2(const unsigned char* __restrict__ bd,
-                                             const unsigned char* __restrict__ bu, const int2* tab,
-                                             int n, int Pd, int Pu, int& dd, int& du) {
-    unsigned din = 0, dout = 0, uin = 0, uout = 0;
-#pragma unroll 4
-    for (int k = 0; k < n; k++) {
-        const int2 o = tab[k];
-        acc_lt(din, *reinterpret_cast<const uint16_t*>(bd + o.x), (unsigned)Pd);
-        acc_lt(dout, *reinterpret_cast<const uint16_t*>(bd + o.y), (unsigned)Pd);
-        acc_lt(uout, *reinterpret_cast<const uint16_t*>(bu + o.x), (unsigned)Pu);
-        acc_lt(uin, *reinterpret_cast<const uint16_t*>(bu + o.y), (unsigned)Pu);
-    }
-    dd = (int)din - (int)dout;
-    du = (int)uin - (int)uout;
-}
-
 // Warp-collaborative slide delta: lanes split the n table entries.
 __device__ __forceinline__ int slide_delta_warp(const unsigned char* __restrict__ Ib, const int2* tab,
                                                 int n, int P, int lane) {
@@ -367,63 +349,6 @@ __global__ void __launch_bounds__(512) k2_select(Geom g, SelParams p, const __gr
     __syncthreads();
 
     // ---- D. vertical sweeps --------------------------------------------------
-    if (p.paired) {
-        // each thread slides one window down and one up from its seed row, in
-        // lockstep: warp-uniform slide loops, the offset loads shared by both.
-        const int nup = R >> 1, ndn = R - (R >> 1) - 1;
-        const int extra = Th - G * R;
-        const bool live = tid < G * Tw;
-        const int u = live ? tid : G * Tw - 1;
-        const int j = u % Tw, gi = u / Tw;
-        const int row0 = seed_row(gi), cx = j + r;
-        int Pd = st_P[u], cd = st_C[u], Pu = Pd, cu = cd;
-        if (live) write_out(c, tc, Pd, row0, j);
-        const unsigned char* Ic = Ib0 + 2 * cx;
-        const int nmax = max(nup, ndn);
-        for (int s = 0; s < nmax; s++) {
-            const int rd = row0 + s, ru = row0 - s;
-            if (s < ndn && s < nup) {
-                int dd, du;
-                slide_delta2(Ic + (rd + r) * rowB, Ic + (ru + r - 1) * rowB, vtab, p.ncols, Pd, Pu,
-                             dd, du);
-                cd += dd;
-                cu += du;
-            } else if (s < ndn) {
-                cd += slide_delta(Ic + (rd + r) * rowB, vtab, p.ncols, Pd, false);
-            } else {
-                cu += slide_delta(Ic + (ru + r - 1) * rowB, vtab, p.ncols, Pu, true);
-            }
-            if (s < ndn) {
-                const int tgt = target_at(g, p, tc, rd + 1, j);
-                const int m = refine_thread<CIRCLE>(c, cx, rd + 1 + r, Pd, cd, tgt);
-                if (m < 0) atomicOr(p.status, 1);
-                if (live) write_out(c, tc, max(m, 0), rd + 1, j);
-                Pd = max(m, 0);
-                cd = tgt;
-            }
-            if (s < nup) {
-                const int tgt = target_at(g, p, tc, ru - 1, j);
-                const int m = refine_thread<CIRCLE>(c, cx, ru - 1 + r, Pu, cu, tgt);
-                if (m < 0) atomicOr(p.status, 1);
-                if (live) write_out(c, tc, max(m, 0), ru - 1, j);
-                Pu = max(m, 0);
-                cu = tgt;
-            }
-        }
-        if (gi == G - 1) {
-            for (int e = 0; e < extra; e++) {
-                const int row = row0 + ndn + e;
-                cd += slide_delta(Ic + (row + r) * rowB, vtab, p.ncols, Pd, false);
-                const int tgt = target_at(g, p, tc, row + 1, j);
-                const int m = refine_thread<CIRCLE>(c, cx, row + 1 + r, Pd, cd, tgt);
-                if (m < 0) atomicOr(p.status, 1);
-                if (live) write_out(c, tc, max(m, 0), row + 1, j);
-                Pd = max(m, 0);
-                cd = tgt;
-            }
-        }
-        return;
-    }
     for (int u = tid; u < G * Tw * 2; u += blockDim.x) {
         const int j = u % Tw, rest = u / Tw, gi = rest >> 1;
         const bool down = (rest & 1) == 0;
