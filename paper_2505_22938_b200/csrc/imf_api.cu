@@ -96,15 +96,18 @@ int make_plan(const imf_image* src, const imf_kernel* k, const imf_options* opt,
     double best = -1.0;
     // K2 fast path: tile ranks < 2^15 (S <= 181), even T, and T + r <= 128 for
     // the packed circle test.  Largest such tile.
-    if (env_int("IMF_PAIR", 1) && (k->shape_code == IMF_SHAPE_CIRCLE || env_int("IMF_PAIR_ANY", 0))) {
+    // circles and squares have packed membership tests; other shapes (span
+    // table per rank) are faster on the general path
+    const bool packed_shape = k->shape_code == IMF_SHAPE_CIRCLE || k->shape_code == IMF_SHAPE_SQUARE;
+    if (env_int("IMF_PAIR", 1) && (packed_shape || env_int("IMF_PAIR_ANY", 0))) {
         // columns: even, <= Tmax, packed circle test needs Tw + r <= 128; rows: the
         // tallest tile keeping N = Sw * Sh <= 32768 (ranks < 2^15), at most Tw
         int Tw = std::min(Tmax, 255 - 2 * r);
-        if (k->shape_code == IMF_SHAPE_CIRCLE) Tw = std::min(Tw, 128 - r);
+        if (packed_shape) Tw = std::min(Tw, 128 - r);
         Tw &= ~1;
         const int Sw = Tw + 2 * r;
         int Th = std::min(Tw, 65536 / std::max(Sw, 1) - 2 * r);
-        if (k->shape_code == IMF_SHAPE_CIRCLE) Th = std::min(Th, 128 - r);
+        if (packed_shape) Th = std::min(Th, 128 - r);
         // rectangular tiles (Th < Tw) measured slower than the generic path
         // (short sweeps, more seed rows per output row): square tiles only, and
         // no smaller than the default 64 (small tiles sort too much per output)
@@ -308,10 +311,12 @@ cudaError_t set_attrs() {
     if (!e) e = allow_smem(k2_select<false, false>, optin);
     if (!e) e = allow_smem(k2_select<true, true>, optin);
     if (!e) e = allow_smem(k2_select<false, true>, optin);
-    if (!e) e = allow_smem(k2_pair<true, false>, optin);
-    if (!e) e = allow_smem(k2_pair<false, false>, optin);
-    if (!e) e = allow_smem(k2_pair<true, true>, optin);
-    if (!e) e = allow_smem(k2_pair<false, true>, optin);
+    if (!e) e = allow_smem(k2_pair<SH_SPAN, false>, optin);
+    if (!e) e = allow_smem(k2_pair<SH_CIRCLE, false>, optin);
+    if (!e) e = allow_smem(k2_pair<SH_SQUARE, false>, optin);
+    if (!e) e = allow_smem(k2_pair<SH_SPAN, true>, optin);
+    if (!e) e = allow_smem(k2_pair<SH_CIRCLE, true>, optin);
+    if (!e) e = allow_smem(k2_pair<SH_SQUARE, true>, optin);
     if (!e) g_attr_done = true;
     return e;
 }
@@ -446,7 +451,10 @@ static int filter_impl(const imf_image* src, imf_image* dsts, int n, const int32
         if (!build_pair_tab(kernel->row_dy, kernel->row_xlo, kernel->row_xhi, kernel->nrows, kernel->col_dx,
                             kernel->col_ytop, kernel->col_ybot, kernel->ncols, r, p.g.Sw, ptab, pp))
             return IMF_ERR_UNSUPPORTED;
-        pp.circle = kernel->shape_code == IMF_SHAPE_CIRCLE && p.g.Tw + r <= 128;
+        const bool bytes_ok = p.g.Tw + r <= 128 && p.g.Th + r <= 128;  // |dx|, |dy| <= 127 in a tile
+        pp.shape = !bytes_ok ? SH_SPAN
+                   : kernel->shape_code == IMF_SHAPE_CIRCLE ? SH_CIRCLE
+                   : kernel->shape_code == IMF_SHAPE_SQUARE ? SH_SQUARE : SH_SPAN;
         pp.R2p1 = r * (r + 1) + 1;
         pp.target = targets[0];
         pp.tmap = target_map;
@@ -506,14 +514,16 @@ static int filter_impl(const imf_image* src, imf_image* dsts, int n, const int32
         g.d_c = dsts[i].stride_c;
         sp.target = pp.target = targets[i];
         if (p.pair) {
-            if (pp.circle && !p.omg)
-                k2_pair<true, false><<<nb, p.k2_threads, p.k2_smem, s>>>(g, pp, ptab, omega);
-            else if (!p.omg)
-                k2_pair<false, false><<<nb, p.k2_threads, p.k2_smem, s>>>(g, pp, ptab, omega);
-            else if (pp.circle)
-                k2_pair<true, true><<<nb, p.k2_threads, p.k2_smem, s>>>(g, pp, ptab, omega);
-            else
-                k2_pair<false, true><<<nb, p.k2_threads, p.k2_smem, s>>>(g, pp, ptab, omega);
+#define IMF_K2P_LAUNCH(S, O) k2_pair<S, O><<<nb, p.k2_threads, p.k2_smem, s>>>(g, pp, ptab, omega)
+            switch (pp.shape * 2 + (p.omg ? 1 : 0)) {
+                case SH_CIRCLE * 2: IMF_K2P_LAUNCH(SH_CIRCLE, false); break;
+                case SH_CIRCLE * 2 + 1: IMF_K2P_LAUNCH(SH_CIRCLE, true); break;
+                case SH_SQUARE * 2: IMF_K2P_LAUNCH(SH_SQUARE, false); break;
+                case SH_SQUARE * 2 + 1: IMF_K2P_LAUNCH(SH_SQUARE, true); break;
+                case SH_SPAN * 2 + 1: IMF_K2P_LAUNCH(SH_SPAN, true); break;
+                default: IMF_K2P_LAUNCH(SH_SPAN, false); break;
+            }
+#undef IMF_K2P_LAUNCH
         } else if (sp.circle && !p.omg)
             k2_select<true, false><<<nb, p.k2_threads, p.k2_smem, s>>>(g, sp, kt, omega);
         else if (!p.omg)

@@ -33,6 +33,11 @@
 
 namespace imf {
 
+// Membership test families of the pair kernel (template parameter SHAPE).
+constexpr int SH_SPAN = 0;    // any convex kernel: per-row span table (kernels.py:127-182)
+constexpr int SH_CIRCLE = 1;  // 4(dx^2+dy^2) <= (2r+1)^2 (kernels.py:70-71), packed bytes + IDP.4A
+constexpr int SH_SQUARE = 2;  // |dx|, |dy| <= r (kernels.py:72-73), packed 16-bit range tests
+
 constexpr int PT_MAX = 184;  // >= kernel rows / columns (2r+1) of every pair-path geometry
 
 // Byte offsets into I relative to a window pair's base 2*(row*Sw + 2q), in
@@ -46,7 +51,7 @@ struct PairTab {
 };
 
 struct PairParams {
-    int circle;      // 1: packed circle test (requires T + r <= 128)
+    int shape;       // SH_*: membership test family (packed ones require T + r <= 128)
     int R2p1;        // r(r+1) + 1
     int nv, nv_even;
     int nh, nhe_even, nhx_even;
@@ -153,7 +158,7 @@ struct PairCtx {
 };
 
 // Membership bits of ranks v0..v0+7 (bit i = rank v0+i) of the window at (cx, cy).
-template <bool CIRCLE, bool OMG>
+template <int SHAPE, bool OMG>
 __device__ __forceinline__ uint32_t test8(const PairCtx& c, int v0, uint32_t Kc, int cx, int cy) {
     uint4 q;
     if (OMG)  // omega in its L2-resident global slot (16-byte aligned)
@@ -162,7 +167,7 @@ __device__ __forceinline__ uint32_t test8(const PairCtx& c, int v0, uint32_t Kc,
         q = lds128(c.om_a + 2 * v0);
     const uint32_t w[4] = {q.x, q.y, q.z, q.w};
     uint32_t m = 0;
-    if (CIRCLE) {
+    if (SHAPE == SH_CIRCLE) {
 #pragma unroll
         for (int i = 3; i >= 0; i--) {
             const int b = (int)((w[i] + Kc) ^ 0x80808080u);
@@ -170,6 +175,22 @@ __device__ __forceinline__ uint32_t test8(const PairCtx& c, int v0, uint32_t Kc,
             const int shi = __dp4a(b, (int)((uint32_t)b & 0xffff0000u), -c.R2p1);
             m = __funnelshift_l((uint32_t)shi, m, 1);
             m = __funnelshift_l((uint32_t)slo, m, 1);
+        }
+    } else if (SHAPE == SH_SQUARE) {
+        // bytes (dx+128, dy+128) of two ranks; per rank spread into 16-bit halves,
+        // bit 15 of h + (0x8000 - (128 - r)) is [d >= -r] and of h + (0x8000 - (129 + r))
+        // is [d > r]; inside iff both halves pass: (t >> 15) == 0x10001, whose
+        // sign-bit form is (t >> 15) + 0x7ffeffff
+        const uint32_t KA = (uint32_t)(0x8000 - (128 - c.r)) * 0x10001u;
+        const uint32_t KB = (uint32_t)(0x8000 - (129 + c.r)) * 0x10001u;
+#pragma unroll
+        for (int i = 3; i >= 0; i--) {
+            const uint32_t a = w[i] + Kc;
+            const uint32_t h1 = prmt(a, 0u, 0x4342u), h0 = prmt(a, 0u, 0x4140u);
+            const uint32_t t1 = (h1 + KA) & ~(h1 + KB) & 0x80008000u;
+            const uint32_t t0 = (h0 + KA) & ~(h0 + KB) & 0x80008000u;
+            m = __funnelshift_l((t1 >> 15) + 0x7ffeffffu, m, 1);
+            m = __funnelshift_l((t0 >> 15) + 0x7ffeffffu, m, 1);
         }
     } else {
 #pragma unroll
@@ -190,7 +211,7 @@ __device__ __forceinline__ uint32_t test8(const PairCtx& c, int v0, uint32_t Kc,
 // t-th smallest rank of the window at (cx, cy) from the exact state (P, cnt):
 // walk omega from P toward the target 8 ranks per step (core.py:87-146 with an
 // exact pivot).  -1 if the walk leaves [0, N) (core.py:31-36).
-template <bool CIRCLE, bool OMG>
+template <int SHAPE, bool OMG>
 __device__ int refine8(const PairCtx& c, int cx, int cy, int P, int cnt, int t) {
     const bool up = cnt <= t;
     int need = up ? t - cnt : cnt - t - 1;
@@ -208,7 +229,7 @@ __device__ int refine8(const PairCtx& c, int cx, int cy, int P, int cnt, int t) 
     const uint32_t Kc = (uint32_t)((128 - cx) + ((128 - cy) << 8)) * 0x10001u;
     for (;;) {
         if (v0 < 0 || v0 >= c.N) return -1;
-        uint32_t m = test8<CIRCLE, OMG>(c, v0, Kc, cx, cy) & mask;
+        uint32_t m = test8<SHAPE, OMG>(c, v0, Kc, cx, cy) & mask;
         if (v0 + 8 > c.N) m &= (1u << (c.N - v0)) - 1u;
         const int pc = __popc(m);
         if (need < pc) return v0 + nth_bit8(m, up ? need : pc - 1 - need);
@@ -250,14 +271,14 @@ __device__ __forceinline__ void walk_init(Walk& w, int P, int cnt, int t, int cx
     w.msk = 0;
 }
 
-template <bool CIRCLE, bool OMG>
+template <int SHAPE, bool OMG>
 __device__ __forceinline__ void walk_step(const PairCtx& c, Walk& w, int cx, int cy) {
     if (w.done) return;
     if ((unsigned)w.v0 >= (unsigned)c.N) {  // left [0, N): defect
         w.done = true;
         return;
     }
-    const uint32_t m = test8<CIRCLE, OMG>(c, w.v0, w.Kc, cx, cy) & w.mask;
+    const uint32_t m = test8<SHAPE, OMG>(c, w.v0, w.Kc, cx, cy) & w.mask;
     const int pc = __popc(m);
     if (w.need < pc) {
         w.done = true;
@@ -275,7 +296,7 @@ __device__ __forceinline__ void walk_step(const PairCtx& c, Walk& w, int cx, int
 __device__ unsigned long long g_stats[256];  // [0..63] lane steps/window-pair, [64..127] warp trip counts
 #endif
 
-template <bool CIRCLE, bool OMG>
+template <int SHAPE, bool OMG>
 __device__ __forceinline__ void refine8x2(const PairCtx& c, int cx, int cy, int PA, int cntA, int tA, int PB,
                                           int cntB, int tB, int& mA, int& mB) {
     Walk a, b;
@@ -288,8 +309,8 @@ __device__ __forceinline__ void refine8x2(const PairCtx& c, int cx, int cy, int 
 #ifdef IMF_STATS
         nit++;
 #endif
-        walk_step<CIRCLE, OMG>(c, a, cx, cy);
-        walk_step<CIRCLE, OMG>(c, b, cx + 1, cy);
+        walk_step<SHAPE, OMG>(c, a, cx, cy);
+        walk_step<SHAPE, OMG>(c, b, cx + 1, cy);
     } while (!(a.done && b.done));
     mA = a.base < 0 ? -1 : a.base + nth_bit8(a.msk, a.k);
     mB = b.base < 0 ? -1 : b.base + nth_bit8(b.msk, b.k);
@@ -348,7 +369,7 @@ __device__ __forceinline__ int target_at2(const Geom& g, const PairParams& p, co
 
 // Warp-collaborative refine for the few seed windows (lane l tests ranks
 // v0+2l, v0+2l+1 of each 64-rank block), generic membership.
-template <bool CIRCLE>
+template <int SHAPE>
 __device__ int refine_warp2(const PairCtx& c, int cx, int cy, int P, int cnt, int t) {
     const int lane = threadIdx.x & 31;
     const unsigned lt = lanemask_lt();
@@ -359,7 +380,8 @@ __device__ int refine_warp2(const PairCtx& c, int cx, int cy, int P, int cnt, in
         if (v < 0 || v >= c.N) return false;
         const uint32_t e = c.om[v];
         const int dx = (int)(e & 0xffu) - cx, dyr = (int)(e >> 8) - cy;
-        if (CIRCLE) return dx * dx + dyr * dyr <= R2;
+        if (SHAPE == SH_CIRCLE) return dx * dx + dyr * dyr <= R2;
+        if (SHAPE == SH_SQUARE) return max(abs(dx), abs(dyr)) <= c.r;
         const int dy = dyr + c.r;
         if ((unsigned)dy > (unsigned)(2 * c.r)) return false;
         const int sp = c.span[dy];
@@ -386,11 +408,12 @@ __device__ int refine_warp2(const PairCtx& c, int cx, int cy, int P, int cnt, in
 }
 
 // Is rank v's pixel in the window at (cx, cy)?  (ordinal.py:175-185)
-template <bool CIRCLE>
+template <int SHAPE>
 __device__ __forceinline__ bool inside1(const PairCtx& c, int v, int cx, int cy) {
     const uint32_t e = c.om[v];
     const int dx = (int)(e & 0xffu) - cx, dyr = (int)(e >> 8) - cy;
-    if (CIRCLE) return dx * dx + dyr * dyr <= c.R2p1 - 1;
+    if (SHAPE == SH_CIRCLE) return dx * dx + dyr * dyr <= c.R2p1 - 1;
+    if (SHAPE == SH_SQUARE) return max(abs(dx), abs(dyr)) <= c.r;
     const int dy = dyr + c.r;
     if ((unsigned)dy > (unsigned)(2 * c.r)) return false;
     const int sp = c.span[dy];
@@ -401,18 +424,18 @@ __device__ __forceinline__ bool inside1(const PairCtx& c, int v, int cx, int cy)
 // With halved ranks (hs) the ordinal image holds rank >> 1, which compares
 // exactly only against EVEN pivots: P = m & ~1, and when m is odd the count
 // below P is t minus [rank m-1 is in the window].
-template <bool CIRCLE>
+template <int SHAPE>
 __device__ __forceinline__ void to_state(const PairCtx& c, int hs, int m, int t, int cx, int cy, int& P,
                                          int& cnt) {
     P = m;
     cnt = t;
     if (hs && (m & 1)) {
         P = m - 1;
-        cnt = t - (inside1<CIRCLE>(c, m - 1, cx, cy) ? 1 : 0);
+        cnt = t - (inside1<SHAPE>(c, m - 1, cx, cy) ? 1 : 0);
     }
 }
 
-template <bool CIRCLE, bool OMG>
+template <int SHAPE, bool OMG>
 __global__ void __launch_bounds__(512) k2_pair(Geom g, PairParams p, const __grid_constant__ PairTab kt,
                                                const uint16_t* __restrict__ omega_in) {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -509,7 +532,7 @@ __global__ void __launch_bounds__(512) k2_pair(Geom g, PairParams p, const __gri
         }
         const int B = __ffs(__ballot_sync(0xffffffffu, cum > tgt)) - 1;
         const int cnt = __shfl_sync(0xffffffffu, cum - tot, B);
-        const int m = refine_warp2<CIRCLE>(c, cs + r, row + r, B << (sh + hs), cnt, tgt);
+        const int m = refine_warp2<SHAPE>(c, cs + r, row + r, B << (sh + hs), cnt, tgt);
         if (lane == 0) {
             if (m < 0) atomicOr(p.status, 1);
             seedP[g0] = max(m, 0);
@@ -522,7 +545,7 @@ __global__ void __launch_bounds__(512) k2_pair(Geom g, PairParams p, const __gri
     const int ytop = seed_row(0), ybot = seed_row(G - 1);
     if (G > 1) {
         int P0, C0;
-        to_state<CIRCLE>(c, hs, seedP[g0], seedC[g0], cs + r, seed_row(g0) + r, P0, C0);
+        to_state<SHAPE>(c, hs, seedP[g0], seedC[g0], cs + r, seed_row(g0) + r, P0, C0);
         const uint32_t K0 = pivot_k(P0 >> hs, P0 >> hs);
         for (int y = ytop + tid; y < ybot; y += blockDim.x) {  // step y -> y+1 at column cs
             uint32_t gi_, go_;
@@ -541,7 +564,7 @@ __global__ void __launch_bounds__(512) k2_pair(Geom g, PairParams p, const __gri
             }
             const int cnt = C0 + (int)__reduce_add_sync(0xffffffffu, (unsigned)part);
             const int tgt = target_at2(g, p, tc, y1, cs);
-            const int m = refine_warp2<CIRCLE>(c, cs + r, y1 + r, P0, cnt, tgt);
+            const int m = refine_warp2<SHAPE>(c, cs + r, y1 + r, P0, cnt, tgt);
             if (lane == 0) {
                 if (m < 0) atomicOr(p.status, 1);
                 seedP[gi] = max(m, 0);
@@ -555,7 +578,7 @@ __global__ void __launch_bounds__(512) k2_pair(Geom g, PairParams p, const __gri
     for (int u = tid; u < G * TH; u += blockDim.x) {  // steps 2q -> 2q+1, 2q+1 -> 2q+2 of row gi
         const int gi = u / TH, q = u - gi * TH;
         int P, C0;
-        to_state<CIRCLE>(c, hs, seedP[gi], seedC[gi], cs + r, seed_row(gi) + r, P, C0);
+        to_state<SHAPE>(c, hs, seedP[gi], seedC[gi], cs + r, seed_row(gi) + r, P, C0);
         const uint32_t K = pivot_k(P >> hs, P >> hs);
         const uint32_t b = I_a + 2 * (seed_row(gi) * Sw + 2 * q);
         const uint32_t ge_in = hcount(b, kt.he, p.nhe_even, p.nh, K);
@@ -569,14 +592,14 @@ __global__ void __launch_bounds__(512) k2_pair(Geom g, PairParams p, const __gri
     for (int u = tid; u < G * T; u += blockDim.x) {
         const int gi = u / T, j = u - gi * T, row = seed_row(gi);
         int P, cnt;
-        to_state<CIRCLE>(c, hs, seedP[gi], seedC[gi], cs + r, row + r, P, cnt);
+        to_state<SHAPE>(c, hs, seedP[gi], seedC[gi], cs + r, row + r, P, cnt);
         if (j > cs) {
             for (int i = cs; i < j; i++) cnt += deltas[gi * T + i];
         } else {
             for (int i = j; i < cs; i++) cnt -= deltas[gi * T + i];
         }
         const int tgt = target_at2(g, p, tc, row, j);
-        int m = (j == cs) ? seedP[gi] : refine8<CIRCLE, OMG>(c, j + r, row + r, P, cnt, tgt);
+        int m = (j == cs) ? seedP[gi] : refine8<SHAPE, OMG>(c, j + r, row + r, P, cnt, tgt);
         if (m < 0) {
             atomicOr(p.status, 1);
             m = 0;
@@ -599,8 +622,8 @@ __global__ void __launch_bounds__(512) k2_pair(Geom g, PairParams p, const __gri
         const int j0 = 2 * q, j1 = j0 + 1;
         const int mA0 = st_P[gi * T + j0], mB0 = st_P[gi * T + j1];
         int PA, cA, PB, cB;
-        to_state<CIRCLE>(c, hs, mA0, st_C[gi * T + j0], j0 + r, row0 + r, PA, cA);
-        to_state<CIRCLE>(c, hs, mB0, st_C[gi * T + j1], j1 + r, row0 + r, PB, cB);
+        to_state<SHAPE>(c, hs, mA0, st_C[gi * T + j0], j0 + r, row0 + r, PA, cA);
+        to_state<SHAPE>(c, hs, mB0, st_C[gi * T + j1], j1 + r, row0 + r, PB, cB);
         Pend wa{0, 0, false}, wb{0, 0, false};
         if (down) {
             wa = gather_out(g, tc, om, mA0, row0, j0);
@@ -628,7 +651,7 @@ __global__ void __launch_bounds__(512) k2_pair(Geom g, PairParams p, const __gri
             const int tA = target_at2(g, p, tc, row, j0);
             const int tB = target_at2(g, p, tc, row, j1);
             int mA, mB;
-            refine8x2<CIRCLE, OMG>(c, j0 + r, row + r, PA, cA, tA, PB, cB, tB, mA, mB);
+            refine8x2<SHAPE, OMG>(c, j0 + r, row + r, PA, cA, tA, PB, cB, tB, mA, mB);
             if ((mA | mB) < 0) {
                 atomicOr(p.status, 1);
                 mA = max(mA, 0);
@@ -636,18 +659,23 @@ __global__ void __launch_bounds__(512) k2_pair(Geom g, PairParams p, const __gri
             }
             wa = gather_out(g, tc, om, mA, row, j0);
             wb = gather_out(g, tc, om, mB, row, j1);
-            to_state<CIRCLE>(c, hs, mA, tA, j0 + r, row + r, PA, cA);
-            to_state<CIRCLE>(c, hs, mB, tB, j1 + r, row + r, PB, cB);
+            to_state<SHAPE>(c, hs, mA, tA, j0 + r, row + r, PA, cA);
+            to_state<SHAPE>(c, hs, mB, tB, j1 + r, row + r, PB, cB);
         }
         store_out(g, wa);
         store_out(g, wb);
     }
 }
 
-template __global__ void k2_pair<true, false>(Geom, PairParams, const __grid_constant__ PairTab, const uint16_t*);
-template __global__ void k2_pair<false, false>(Geom, PairParams, const __grid_constant__ PairTab, const uint16_t*);
-template __global__ void k2_pair<true, true>(Geom, PairParams, const __grid_constant__ PairTab, const uint16_t*);
-template __global__ void k2_pair<false, true>(Geom, PairParams, const __grid_constant__ PairTab, const uint16_t*);
+#define IMF_K2P(S, O) \
+    template __global__ void k2_pair<S, O>(Geom, PairParams, const __grid_constant__ PairTab, const uint16_t*);
+IMF_K2P(SH_SPAN, false)
+IMF_K2P(SH_CIRCLE, false)
+IMF_K2P(SH_SQUARE, false)
+IMF_K2P(SH_SPAN, true)
+IMF_K2P(SH_CIRCLE, true)
+IMF_K2P(SH_SQUARE, true)
+#undef IMF_K2P
 
 size_t k2_pair_smem_bytes(int N, int Npad, int NI, int r, int G, int T, int TY, bool omg) {
     const int Ipad = (NI + 15) & ~7;
