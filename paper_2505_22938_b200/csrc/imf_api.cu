@@ -98,7 +98,8 @@ int make_plan(const imf_image* src, const imf_kernel* k, const imf_options* opt,
     // the packed circle test.  Largest such tile.
     // circles and squares have packed membership tests; other shapes (span
     // table per rank) are faster on the general path
-    const bool packed_shape = k->shape_code == IMF_SHAPE_CIRCLE || k->shape_code == IMF_SHAPE_SQUARE;
+    const bool packed_shape = k->shape_code == IMF_SHAPE_CIRCLE || k->shape_code == IMF_SHAPE_SQUARE ||
+                              (k->shape_code == IMF_SHAPE_POLYGON && env_int("IMF_PAIR_POLY", 1));
     if (env_int("IMF_PAIR", 1) && (packed_shape || env_int("IMF_PAIR_ANY", 0))) {
         // columns: even, <= Tmax, packed circle test needs Tw + r <= 128; rows: the
         // tallest tile keeping N = Sw * Sh <= 32768 (ranks < 2^15), at most Tw
@@ -317,6 +318,8 @@ cudaError_t set_attrs() {
     if (!e) e = allow_smem(k2_pair<SH_SPAN, true>, optin);
     if (!e) e = allow_smem(k2_pair<SH_CIRCLE, true>, optin);
     if (!e) e = allow_smem(k2_pair<SH_SQUARE, true>, optin);
+    if (!e) e = allow_smem(k2_pair<SH_POLY, false>, optin);
+    if (!e) e = allow_smem(k2_pair<SH_POLY, true>, optin);
     if (!e) g_attr_done = true;
     return e;
 }
@@ -454,7 +457,7 @@ static int filter_impl(const imf_image* src, imf_image* dsts, int n, const int32
         const bool bytes_ok = p.g.Tw + r <= 128 && p.g.Th + r <= 128;  // |dx|, |dy| <= 127 in a tile
         pp.shape = !bytes_ok ? SH_SPAN
                    : kernel->shape_code == IMF_SHAPE_CIRCLE ? SH_CIRCLE
-                   : kernel->shape_code == IMF_SHAPE_SQUARE ? SH_SQUARE : SH_SPAN;
+                   : kernel->shape_code == IMF_SHAPE_SQUARE ? SH_SQUARE : SH_POLY;
         pp.R2p1 = r * (r + 1) + 1;
         pp.target = targets[0];
         pp.tmap = target_map;
@@ -520,6 +523,8 @@ static int filter_impl(const imf_image* src, imf_image* dsts, int n, const int32
                 case SH_CIRCLE * 2 + 1: IMF_K2P_LAUNCH(SH_CIRCLE, true); break;
                 case SH_SQUARE * 2: IMF_K2P_LAUNCH(SH_SQUARE, false); break;
                 case SH_SQUARE * 2 + 1: IMF_K2P_LAUNCH(SH_SQUARE, true); break;
+                case SH_POLY * 2: IMF_K2P_LAUNCH(SH_POLY, false); break;
+                case SH_POLY * 2 + 1: IMF_K2P_LAUNCH(SH_POLY, true); break;
                 case SH_SPAN * 2 + 1: IMF_K2P_LAUNCH(SH_SPAN, true); break;
                 default: IMF_K2P_LAUNCH(SH_SPAN, false); break;
             }

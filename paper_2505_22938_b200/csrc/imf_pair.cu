@@ -37,6 +37,7 @@ namespace imf {
 constexpr int SH_SPAN = 0;    // any convex kernel: per-row span table (kernels.py:127-182)
 constexpr int SH_CIRCLE = 1;  // 4(dx^2+dy^2) <= (2r+1)^2 (kernels.py:70-71), packed bytes + IDP.4A
 constexpr int SH_SQUARE = 2;  // |dx|, |dy| <= r (kernels.py:72-73), packed 16-bit range tests
+constexpr int SH_POLY = 3;    // any convex kernel, per-row range constants looked up by dy byte
 
 constexpr int PT_MAX = 184;  // >= kernel rows / columns (2r+1) of every pair-path geometry
 
@@ -155,7 +156,14 @@ struct PairCtx {
     const uint16_t* om;   // generic pointer to omega rank 0
     const int* span;      // shared span table (2r+1)
     int N, r, R2p1;
+    uint32_t rowk_a;      // SH_POLY: shared address of the 256-entry per-(dy+128) range table
 };
+
+__device__ __forceinline__ uint32_t lds32c(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
 
 // Membership bits of ranks v0..v0+7 (bit i = rank v0+i) of the window at (cx, cy).
 template <int SHAPE, bool OMG>
@@ -191,6 +199,18 @@ __device__ __forceinline__ uint32_t test8(const PairCtx& c, int v0, uint32_t Kc,
             const uint32_t t0 = (h0 + KA) & ~(h0 + KB) & 0x80008000u;
             m = __funnelshift_l((t1 >> 15) + 0x7ffeffffu, m, 1);
             m = __funnelshift_l((t0 >> 15) + 0x7ffeffffu, m, 1);
+        }
+    } else if (SHAPE == SH_POLY) {
+        // row table T[dy+128] = (0x8000 - (128+xlo)) | (0x8000 - (128+xhi)) << 16
+        // (0 for rows outside the kernel): with the dx byte h in both halves,
+        // bit 15 of h*0x10001 + T is [dx >= xlo] and bit 31 is [dx >= xhi]
+#pragma unroll
+        for (int i = 3; i >= 0; i--) {
+            const uint32_t a = w[i] + Kc;
+            const uint32_t T1 = lds32c(c.rowk_a + 4 * (a >> 24)), T0 = lds32c(c.rowk_a + 4 * ((a >> 8) & 0xffu));
+            const uint32_t d1 = prmt(a, 0u, 0x4242u) + T1, d0 = prmt(a, 0u, 0x4040u) + T0;
+            m = __funnelshift_l((d1 << 16) & ~d1, m, 1);
+            m = __funnelshift_l((d0 << 16) & ~d0, m, 1);
         }
     } else {
 #pragma unroll
@@ -458,6 +478,7 @@ __global__ void __launch_bounds__(512) k2_pair(Geom g, PairParams p, const __gri
     int* seedP = hist + 32;                    // G
     int* seedC = seedP + G;                    // G
     int* span_s = seedC + G;                   // 2r+1
+    uint32_t* rowk = reinterpret_cast<uint32_t*>(span_s + 2 * r + 1);  // 256 (SH_POLY)
 
     // ---- 0. stage omega, build the ordinal image --------------------------
     {
@@ -483,11 +504,24 @@ __global__ void __launch_bounds__(512) k2_pair(Geom g, PairParams p, const __gri
         for (int i = Sw * g.Sh + tid; i < Ipad; i += blockDim.x) I[i] = 0;
         if (tid < 32) hist[tid] = 0;
         for (int i = tid; i < 2 * r + 1; i += blockDim.x) span_s[i] = kt.span[i];
+        if (SHAPE == SH_POLY) {
+            for (int i = tid; i < 256; i += blockDim.x) {
+                const int dy = i - 128;
+                uint32_t v = 0;  // rows outside the kernel: never inside
+                if (dy >= -r && dy <= r) {
+                    const int sp = kt.span[dy + r];
+                    const int xlo = (int)(short)(sp & 0xffff), xhi = xlo + (sp >> 16);
+                    if (sp >> 16) v = (uint32_t)(0x8000 - (128 + xlo)) | ((uint32_t)(0x8000 - (128 + xhi)) << 16);
+                }
+                rowk[i] = v;
+            }
+        }
     }
     __syncthreads();
 
     const uint32_t I_a = (uint32_t)__cvta_generic_to_shared(I);
-    const PairCtx c{OMG ? 0u : (uint32_t)__cvta_generic_to_shared(om_sh), om, span_s, N, r, p.R2p1};
+    const PairCtx c{OMG ? 0u : (uint32_t)__cvta_generic_to_shared(om_sh), om, span_s, N, r, p.R2p1,
+                    (uint32_t)__cvta_generic_to_shared(rowk)};
     const int R = TY / G;
     const int g0 = G >> 1;
     const int cs = (T >> 1) & ~1;  // seed column (even: a pair base)
@@ -675,13 +709,15 @@ IMF_K2P(SH_SQUARE, false)
 IMF_K2P(SH_SPAN, true)
 IMF_K2P(SH_CIRCLE, true)
 IMF_K2P(SH_SQUARE, true)
+IMF_K2P(SH_POLY, false)
+IMF_K2P(SH_POLY, true)
 #undef IMF_K2P
 
 size_t k2_pair_smem_bytes(int N, int Npad, int NI, int r, int G, int T, int TY, bool omg) {
     const int Ipad = (NI + 15) & ~7;
     const int gt = G * T;
     return (omg ? 0 : 2 * (size_t)(Npad + 16)) + 2 * (size_t)Ipad +
-           4 * (size_t)(2 * gt + (gt > TY ? gt : TY) + 32 + 2 * G + 2 * r + 1) + 16;
+           4 * (size_t)(2 * gt + (gt > TY ? gt : TY) + 32 + 2 * G + 2 * r + 1 + 256) + 16;
 }
 
 // Host: build the pair tables for input-tile row stride Sw.  Returns false if

@@ -5,7 +5,8 @@ Paths: pair fast path vs the generic selection kernel (IMF_PAIR), omega in
 shared memory vs in L2 (IMF_PAIR_OMG), rounded-rect footprint on/off
 (IMF_FOOTPRINT), f32 bucket transform vs LSD radix sort (IMF_F32_BUCKET),
 register-resident vs two-pass u16 counting sort (IMF_K1REG), the pair path on
-non-circle kernels (IMF_PAIR_ANY), rectangular pair tiles (IMF_PAIR_RECT),
+generic-span kernels (IMF_PAIR_ANY), polygons on the general path
+(IMF_PAIR_POLY=0), one chunk stream (IMF_LANES), rectangular pair tiles (IMF_PAIR_RECT),
 and tile / seed-row overrides.  Compared against the C oracle, which is itself
 pinned to the reference's golden outputs (tests/test_oracle.py)."""
 import os
@@ -26,6 +27,8 @@ VARIANTS = [
     {"IMF_F32_BUCKET": "0"},
     {"IMF_K1REG": "0"},
     {"IMF_PAIR_ANY": "1"},
+    {"IMF_PAIR_POLY": "0"},
+    {"IMF_LANES": "1"},
     {"IMF_PAIR_RECT": "1", "IMF_TILE": "64"},
     {"IMF_TILE": "40", "IMF_SEED_ROWS": "4"},
     {"IMF_STRIPE_EDGE": "1", "IMF_STRIPE_MID": "5"},
