@@ -466,6 +466,7 @@ static int filter_impl(const imf_image* src, imf_image* dsts, int n, const int32
         pp.tmap = target_map;
         pp.G = p.G;
         pp.hs = p.hs;
+        pp.grouped = p.k2_threads == 64 * p.G && p.g.Tw <= 64 && p.G <= 15 && env_int("IMF_GROUPED", 1);
         pp.status = status;
     }
 

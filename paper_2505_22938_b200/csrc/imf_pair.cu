@@ -59,6 +59,7 @@ struct PairParams {
     int target;
     const int* tmap;
     int G;
+    int grouped;     // phase C+D per seed-row group (named barriers), needs 64 threads per group
     int hs;          // 1: I holds rank >> 1 (tiles with 32768 < N <= 65536), pivots even
     int* status;
 };
@@ -479,6 +480,7 @@ __global__ void __launch_bounds__(512) k2_pair(Geom g, PairParams p, const __gri
     int* seedC = seedP + G;                    // G
     int* span_s = seedC + G;                   // 2r+1
     uint32_t* rowk = reinterpret_cast<uint32_t*>(span_s + 2 * r + 1);  // 256 (SH_POLY)
+    uint32_t* gsc = rowk + 256;                                         // 2 * G * 32 (grouped phase C)
 
     // ---- 0. stage omega, build the ordinal image --------------------------
     {
@@ -608,6 +610,50 @@ __global__ void __launch_bounds__(512) k2_pair(Geom g, PairParams p, const __gri
         __syncthreads();
     }
 
+    // ---- C+D grouped: with one warp pair per seed-row group (T <= 64), each
+    // group does its own seed row and then its sweeps, synchronized by a named
+    // barrier of its 64 threads only -- no CTA-wide wait for the slowest
+    // group's seed-row refines.
+    if (p.grouped) {
+        const int q = lane, rest = wid, gi = rest % G, half = rest / G;  // half 0: down warp
+        const int row = seed_row(gi);
+        auto gbar = [&]() { asm volatile("bar.sync %0, 64;" ::"r"(1 + gi) : "memory"); };
+        int P, C0;
+        to_state<SHAPE>(c, hs, seedP[gi], seedC[gi], cs + r, row + r, P, C0);
+        uint32_t* gin = gsc + gi * 64;  // [0..32): entering counts, [32..64): exiting counts
+        if (q < TH) {  // pair-step (2q, 2q+1): the down warp counts entering, the up warp exiting
+            const uint32_t K = pivot_k(P >> hs, P >> hs);
+            const uint32_t b = I_a + 2 * (row * Sw + 2 * q);
+            gin[half * 32 + q] = half ? hcount(b, kt.hx, p.nhx_even, p.nh, K)
+                                      : hcount(b, kt.he, p.nhe_even, p.nh, K);
+        }
+        gbar();
+        if (half == 0 && q < TH) {
+            int d0, d1;
+            half_diff(gin[32 + q], gin[q], d0, d1);
+            deltas[gi * T + 2 * q] = d0;
+            deltas[gi * T + 2 * q + 1] = d1;
+        }
+        gbar();
+        const int j = half * 32 + q;
+        if (j < T) {
+            int cnt = C0;
+            if (j > cs) {
+                for (int i = cs; i < j; i++) cnt += deltas[gi * T + i];
+            } else {
+                for (int i = j; i < cs; i++) cnt -= deltas[gi * T + i];
+            }
+            const int tgt = target_at2(g, p, tc, row, j);
+            int m = (j == cs) ? seedP[gi] : refine8<SHAPE, OMG>(c, j + r, row + r, P, cnt, tgt);
+            if (m < 0) {
+                atomicOr(p.status, 1);
+                m = 0;
+            }
+            st_P[gi * T + j] = m;
+            st_C[gi * T + j] = tgt;
+        }
+        gbar();
+    } else {
     // ---- C. seed rows: horizontal deltas (pairs of steps) at the row pivot --
     for (int u = tid; u < G * TH; u += blockDim.x) {  // steps 2q -> 2q+1, 2q+1 -> 2q+2 of row gi
         const int gi = u / TH, q = u - gi * TH;
@@ -642,6 +688,7 @@ __global__ void __launch_bounds__(512) k2_pair(Geom g, PairParams p, const __gri
         st_C[u] = tgt;
     }
     __syncthreads();
+    }  // !grouped
 
     // ---- D. vertical sweeps: thread = (direction, group, column pair) ------
     // lanes of a (direction, group) padded to whole warps: every warp sweeps
@@ -717,7 +764,7 @@ size_t k2_pair_smem_bytes(int N, int Npad, int NI, int r, int G, int T, int TY, 
     const int Ipad = (NI + 15) & ~7;
     const int gt = G * T;
     return (omg ? 0 : 2 * (size_t)(Npad + 16)) + 2 * (size_t)Ipad +
-           4 * (size_t)(2 * gt + (gt > TY ? gt : TY) + 32 + 2 * G + 2 * r + 1 + 256) + 16;
+           4 * (size_t)(2 * gt + (gt > TY ? gt : TY) + 32 + 2 * G + 2 * r + 1 + 256 + 64 * G) + 16;
 }
 
 // Host: build the pair tables for input-tile row stride Sw.  Returns false if

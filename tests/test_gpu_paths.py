@@ -29,6 +29,7 @@ VARIANTS = [
     {"IMF_PAIR_ANY": "1"},
     {"IMF_PAIR_POLY": "0"},
     {"IMF_LANES": "1"},
+    {"IMF_GROUPED": "0"},
     {"IMF_PAIR_RECT": "1", "IMF_TILE": "64"},
     {"IMF_TILE": "40", "IMF_SEED_ROWS": "4"},
     {"IMF_STRIPE_EDGE": "1", "IMF_STRIPE_MID": "5"},
