@@ -531,6 +531,8 @@ __global__ void __launch_bounds__(512) k2_pair(Geom g, PairParams p, const __gri
 
     // ---- A. direct seed: 32-bin rank histogram over the window ------------
     const int sh = max(0, 32 - __clz(max(((N - 1) >> hs), 1)) - 5);  // 32 bins over I's range
+    const int ytop = seed_row(0), ybot = seed_row(G - 1);
+    if (!p.grouped) {
     {
         const int cx = cs + r, cy = seed_row(g0) + r;
         unsigned lm[5];
@@ -578,7 +580,6 @@ __global__ void __launch_bounds__(512) k2_pair(Geom g, PairParams p, const __gri
     __syncthreads();
 
     // ---- B. other seed rows' centre windows: vertical deltas at column cs --
-    const int ytop = seed_row(0), ybot = seed_row(G - 1);
     if (G > 1) {
         int P0, C0;
         to_state<SHAPE>(c, hs, seedP[g0], seedC[g0], cs + r, seed_row(g0) + r, P0, C0);
@@ -610,6 +611,8 @@ __global__ void __launch_bounds__(512) k2_pair(Geom g, PairParams p, const __gri
         __syncthreads();
     }
 
+    }  // !grouped (phases A, B)
+
     // ---- C+D grouped: with one warp pair per seed-row group (T <= 64), each
     // group does its own seed row and then its sweeps, synchronized by a named
     // barrier of its 64 threads only -- no CTA-wide wait for the slowest
@@ -618,6 +621,36 @@ __global__ void __launch_bounds__(512) k2_pair(Geom g, PairParams p, const __gri
         const int q = lane, rest = wid, gi = rest % G, half = rest / G;  // half 0: down warp
         const int row = seed_row(gi);
         auto gbar = [&]() { asm volatile("bar.sync %0, 64;" ::"r"(1 + gi) : "memory"); };
+        // this group's seed: the centre window of its seed row, from an exact count
+        // at the even pivot N/2 (the group's two warps split the window rows), then
+        // a warp-collaborative walk (core.py:47-60, :87-146) -- no CTA-wide phase
+        {
+            const int Pg = (N >> 1) & ~1, Pq = Pg >> hs;
+            const int cx = cs + r, cy = row + r;
+            int cntp = 0;
+            for (int dy = half; dy <= 2 * r; dy += 2) {
+                const int sp = span_s[dy];
+                const int w = sp >> 16;
+                const uint16_t* rowp = I + (cy - r + dy) * Sw + cx + (int)(short)(sp & 0xffff);
+                for (int o0 = 0; o0 < w; o0 += 32) {
+                    const int o = o0 + lane;
+                    cntp += __popc(__ballot_sync(0xffffffffu, o < w && (int)rowp[o] < Pq));
+                }
+            }
+            if (lane == 0) gsc[gi * 64 + half] = (uint32_t)cntp;
+            gbar();
+            if (half == 0) {
+                const int cnt = (int)(gsc[gi * 64] + gsc[gi * 64 + 1]);
+                const int tgt = target_at2(g, p, tc, row, cs);
+                const int m = refine_warp2<SHAPE>(c, cx, cy, Pg, cnt, tgt);
+                if (lane == 0) {
+                    if (m < 0) atomicOr(p.status, 1);
+                    seedP[gi] = max(m, 0);
+                    seedC[gi] = tgt;
+                }
+            }
+            gbar();
+        }
         int P, C0;
         to_state<SHAPE>(c, hs, seedP[gi], seedC[gi], cs + r, row + r, P, C0);
         uint32_t* gin = gsc + gi * 64;  // [0..32): entering counts, [32..64): exiting counts
