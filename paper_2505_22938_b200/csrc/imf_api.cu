@@ -61,6 +61,16 @@ int env_int(const char* name, int dflt) {
 
 int dtype_size(int dt) { return dt == IMF_DTYPE_U8 ? 1 : (dt == IMF_DTYPE_U16 ? 2 : 4); }
 
+// Round-up multiplicative inverse for unsigned division by d of n < 2^31:
+// n / d == (n * m) >> (31 + l) with l = ceil(log2 d), m = ceil(2^(31+l) / d)
+// (m <= 2^32 - 1 for d >= 2; m = 2^31 for d = 1; the error term stays < 1/d).
+void set_magic(unsigned d, unsigned& m, int& s) {
+    int l = 0;
+    while ((1ull << l) < d) l++;
+    s = 31 + l;
+    m = (unsigned)(((1ull << (31 + l)) + d - 1) / d);
+}
+
 // Tile geometry: output tile side T (input side S = T + 2r <= 255 so ranks,
 // positions and 16-bit histogram counters fit), seed rows G, and whether omega
 // stays in global memory (OMG).  Among feasible shapes pick the one with the
@@ -186,6 +196,9 @@ int make_plan(const imf_image* src, const imf_kernel* k, const imf_options* opt,
     g.tiles_y = (row1 - row0 + g.Th - 1) / g.Th;
     p.full_out_h = out_h;
     p.total_tiles = (long long)g.tiles_x * g.tiles_y * g.C * g.B;
+    set_magic((unsigned)g.tiles_x, g.mx, g.sx);
+    set_magic((unsigned)g.tiles_y, g.my, g.sy);
+    set_magic((unsigned)g.C, g.mc, g.sc);
     if (p.total_tiles >= (1ll << 31)) return IMF_ERR_UNSUPPORTED;  // tile_coord uses 32-bit indices
 
     p.k1_count = g.dtype != DT_F32 && k1_count_smem_bytes(g.dtype, g.Npad) <= kSmemMax;
@@ -207,7 +220,8 @@ int make_plan(const imf_image* src, const imf_kernel* k, const imf_options* opt,
     // Rounded-rect footprint (pair path, circle kernels, register-resident K1):
     // rank only input pixels within distance^2 r(r+1) of the output rectangle
     // -- the union of the tile's windows -- so omega is shorter and denser.
-    const bool k1reg = p.k1_count && ((g.Sw + 31) >> 5) <= 6 && env_int("IMF_K1REG", 1);
+    const bool k1reg = p.k1_count && ((g.Sw + 31) >> 5) <= 6 && env_int("IMF_K1REG", 1) &&
+                       (long long)(g.H - 1) * g.s_y + (long long)(g.W - 1) * g.s_x < (1ll << 31);
     if (p.pair && k->shape_code == IMF_SHAPE_CIRCLE && k1reg && env_int("IMF_FOOTPRINT", 1)) {
         const int R2 = r * (r + 1);
         int nfp = 0;
@@ -354,7 +368,9 @@ void launch_k1(const Plan& p, const Geom& g, int nblocks, uint16_t* omega, unsig
     }
     if (p.k1_count) {
         const int nk = (g.Sw + 31) >> 5;
-        if (nk <= 6 && env_int("IMF_K1REG", 1)) {
+        // k1_count_reg addresses a plane with 32-bit element offsets
+        const bool plane32 = (long long)(g.H - 1) * g.s_y + (long long)(g.W - 1) * g.s_x < (1ll << 31);
+        if (nk <= 6 && plane32 && env_int("IMF_K1REG", 1)) {
 #define IMF_K1R_LAUNCH(DT)                                                                       \
     switch (nk) {                                                                                \
         case 1: k1_count_reg<DT, 1><<<grid, block, p.k1_smem, s>>>(g, omega); break;             \

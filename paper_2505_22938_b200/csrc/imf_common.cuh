@@ -37,6 +37,8 @@ struct Geom {
     int fp, fpR2;                  // fp: only pixels within dist^2 <= fpR2 of the output rect are ranked
     int tiles_x, tiles_y;
     long long tile_begin;          // first tile of this launch (chunking)
+    unsigned mx, my, mc;           // division magics: n / d == (n * m) >> s for n < 2^31 (host: set_magic)
+    int sx, sy, sc;
 };
 
 // Kernel offset tables, passed by value as a __grid_constant__ kernel parameter
@@ -71,13 +73,13 @@ __device__ __forceinline__ TileCoord tile_coord(const Geom& g, long long t64) {
     // division is a few instructions, the 64-bit one a ~100-instruction call
     unsigned t = (unsigned)t64;
     const unsigned tx = (unsigned)g.tiles_x, ty = (unsigned)g.tiles_y, C = (unsigned)g.C;
-    unsigned q = t / tx;
+    unsigned q = (unsigned)(((unsigned long long)t * g.mx) >> g.sx);  // t / tx (exact for t < 2^31)
     tc.tx = (int)(t - q * tx);
     t = q;
-    q = t / ty;
+    q = (unsigned)(((unsigned long long)t * g.my) >> g.sy);
     tc.ty = (int)(t - q * ty);
     t = q;
-    q = t / C;
+    q = (unsigned)(((unsigned long long)t * g.mc) >> g.sc);
     tc.c = (int)(t - q * C);
     tc.b = (int)q;
     // The last tile of a row / column is shifted back to end at the image edge

@@ -450,26 +450,41 @@ __global__ void __launch_bounds__(1024) k1_count_reg(Geom g, uint16_t* __restric
     uint16_t* om = reinterpret_cast<uint16_t*>(hw + NW);
     uint32_t v[NK][NK];
     {
-        long long xo[NK];
+        // element offsets within one (image, channel) plane fit 32 bits
+        int xo[NK];
 #pragma unroll
         for (int k = 0; k < NK; k++) {
             int x = tc.ox0 + lane + 32 * k - g.r + g.vshift;
             x = x < 0 ? 0 : (x >= g.W ? g.W - 1 : x);
-            xo[k] = (long long)x * g.s_x;
+            xo[k] = x * (int)g.s_x;
         }
 #pragma unroll
         for (int j = 0; j < NK; j++) {
             const int y = wid + 32 * j;
             int yy = tc.oy0 + y - g.r + g.vshift;
             yy = yy < 0 ? 0 : (yy >= g.H ? g.H - 1 : yy);
-            const long long ro = (long long)yy * g.s_y;
+            const int ro = yy * (int)g.s_y;
+            // footprint columns of this row: [flo, fhi] (all columns without one)
+            int flo = 0, fhi = S - 1;
+            if (g.fp) {
+                const int ey = max(0, max(g.r - y, y - (g.r + g.Th - 1)));
+                const int D = g.fpR2 - ey * ey;
+                int w = D < 0 ? -1 : (int)sqrtf((float)D);
+                if (w >= 0) {
+                    while (w * w > D) w--;
+                    while ((w + 1) * (w + 1) <= D) w++;
+                }
+                flo = w < 0 ? S : g.r - w;
+                fhi = g.r + g.Tw - 1 + w;
+            }
 #pragma unroll
             for (int k = 0; k < NK; k++) {
-                const bool ok = y < SH && lane + 32 * k < S && in_footprint(g, lane + 32 * k, y);
+                const int x = lane + 32 * k;
+                const bool ok = y < SH && x < S && x >= flo && x <= fhi;
                 uint32_t val = 0xffffffffu;
                 if (ok) {
-                    val = DT == DT_U8 ? (uint32_t)__ldg((const uint8_t*)tc.src + ro + xo[k])
-                                      : (uint32_t)__ldg((const uint16_t*)tc.src + ro + xo[k]);
+                    val = DT == DT_U8 ? (uint32_t)__ldg((const uint8_t*)tc.src + (ro + xo[k]))
+                                      : (uint32_t)__ldg((const uint16_t*)tc.src + (ro + xo[k]));
                 }
                 v[j][k] = val;
             }
