@@ -93,8 +93,16 @@ int make_plan(const imf_image* src, const imf_kernel* k, const imf_options* opt,
 
     Plan& p = *pl;
     memset(&p, 0, sizeof(p));
-    const int Tmax0 = std::max(1, std::min(opt->tile_size > 0 ? opt->tile_size : env_int("IMF_TILE", 64),
-                                           255 - 2 * r));
+    // Default output tile 64 (sort amortization vs shared memory); 32 when the
+    // window is tiny (r <= 4: walks through a 68^2 rank space are long) or when
+    // 64-tiles would not give the GPU two CTAs per SM (small images).
+    int tdef = env_int("IMF_TILE", 0);
+    if (tdef <= 0) {
+        const long long planes = (long long)src->batch * src->channels;
+        const long long t64 = planes * ((out_h + 63) / 64) * ((out_w + 63) / 64);
+        tdef = (r <= 4 || t64 < 2 * 148) ? 32 : 64;
+    }
+    const int Tmax0 = std::max(1, std::min(opt->tile_size > 0 ? opt->tile_size : tdef, 255 - 2 * r));
     const int G0 = opt->seed_rows > 0 ? opt->seed_rows : env_int("IMF_SEED_ROWS", 4);
     // f32 tiles use the bucket ordinal transform when N <= 23,716 (S <= 154):
     // cap the tile at 154 - 2r while that keeps it >= 48 (r <= 53)
