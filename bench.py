@@ -290,7 +290,7 @@ def run_ours(args):
         qs = ctypes.c_int32()
         L.imf_profile_last(ctypes.byref(a), ctypes.byref(b), ctypes.byref(n), None, None,
                            ctypes.byref(qs))
-        k2_name = {2: "k2_pair", 1: "k2_select (omega in L2)"}.get(qs.value, "k2_select")
+        k2_name = {2: "k2_pair", 1: "k2_select (omega in L2)", 3: "k_direct"}.get(qs.value, "k2_select")
         sort_ms += a.value
         select_ms += b.value
         k2_launches += n.value

@@ -46,6 +46,7 @@ struct Plan {
     bool k1_f32b_g;       // ... with the bucket entries in a global scratch slot per tile
     size_t k1b_smem;
     int full_out_h;
+    bool direct;  // k_direct: per-pixel register sort (window area <= 32)
     int hs;     // k2_pair: ordinal image holds rank >> hs
     bool pair;  // K2 fast path (imf_pair.cu): two windows per thread, 15-bit ranks
     size_t k1_smem, k2_smem, k1_gs_per_tile;
@@ -112,13 +113,24 @@ int make_plan(const imf_image* src, const imf_kernel* k, const imf_options* opt,
         if (tb >= 48) Tmax = std::min(Tmax, tb);
     }
     double best = -1.0;
+    // Tiny windows (area <= 32, e.g. r <= 2): direct per-pixel selection, no ranks.
+    if (k->area <= 32 && env_int("IMF_DIRECT", 1)) {
+        p.direct = true;
+        best = 1.0;
+        p.g.Tw = p.g.Th = 32;
+        p.g.Sw = p.g.Sh = 32 + 2 * r;
+        p.g.N = p.g.Sw * p.g.Sh;
+        p.g.Npad = (p.g.N + 63) & ~63;
+        p.k2_threads = 1024;
+        p.k2_smem = 4 * (size_t)p.g.N;
+    }
     // K2 fast path: tile ranks < 2^15 (S <= 181), even T, and T + r <= 128 for
     // the packed circle test.  Largest such tile.
     // circles and squares have packed membership tests; other shapes (span
     // table per rank) are faster on the general path
     const bool packed_shape = k->shape_code == IMF_SHAPE_CIRCLE || k->shape_code == IMF_SHAPE_SQUARE ||
                               (k->shape_code == IMF_SHAPE_POLYGON && env_int("IMF_PAIR_POLY", 1));
-    if (env_int("IMF_PAIR", 1) && (packed_shape || env_int("IMF_PAIR_ANY", 0))) {
+    if (!p.direct && env_int("IMF_PAIR", 1) && (packed_shape || env_int("IMF_PAIR_ANY", 0))) {
         // columns: even, <= Tmax, packed circle test needs Tw + r <= 128; rows: the
         // tallest tile keeping N = Sw * Sh <= 32768 (ranks < 2^15), at most Tw
         int Tw = std::min(Tmax, 255 - 2 * r);
@@ -161,7 +173,7 @@ int make_plan(const imf_image* src, const imf_kernel* k, const imf_options* opt,
             }
         }
     }
-    for (int T = Tmax; T >= 1 && !p.pair; T--) {
+    for (int T = Tmax; T >= 1 && !p.pair && !p.direct; T--) {
         const int S = T + 2 * r;
         const int N = S * S, Npad = (N + 63) & ~63;
         const int G = std::max(1, std::min(G0, T));
@@ -333,6 +345,9 @@ cudaError_t set_attrs() {
     if (!e) e = allow_smem(k1_f32_bucket<4>, optin);
     if (!e) e = allow_smem(k1_f32_bucket<5>, optin);
     if (!e) e = allow_smem(k1_f32_bucket_g, optin);
+    if (!e) e = allow_smem(k_direct<DT_U8>, optin);
+    if (!e) e = allow_smem(k_direct<DT_U16>, optin);
+    if (!e) e = allow_smem(k_direct<DT_F32>, optin);
     if (!e) e = allow_smem(k2_select<true, false>, optin);
     if (!e) e = allow_smem(k2_select<false, false>, optin);
     if (!e) e = allow_smem(k2_select<true, true>, optin);
@@ -453,6 +468,44 @@ static int filter_impl(const imf_image* src, imf_image* dsts, int n, const int32
     unsigned char* ws = (unsigned char*)workspace;
     int* status = (int*)ws;
     unsigned char* lane_base[2] = {ws + kStatusBytes, ws + kStatusBytes + p.ws_lane};
+
+    if (p.direct) {  // tiny windows: one kernel, no ordinal transform
+        DirectTab dtab;
+        memset(&dtab, 0, sizeof(dtab));
+        dtab.area = 0;
+        for (int i = 0; i < kernel->nrows; i++)
+            for (int x = kernel->row_xlo[i]; x < kernel->row_xhi[i]; x++)
+                dtab.off[dtab.area++] = kernel->row_dy[i] * p.g.Sw + x;
+        if (!(opt->flags & IMF_FLAG_KEEP_STATUS))
+            if (cudaError_t e = cudaMemsetAsync(status, 0, sizeof(int), s)) return cuda_fail(e, "status memset");
+        Geom g = p.g;
+        g.src = src->data;
+        g.tile_begin = 0;
+        const unsigned nb = (unsigned)p.total_tiles;
+        for (int i = 0; i < n; i++) {
+            g.dst = dsts[i].data;
+            g.d_b = dsts[i].stride_b;
+            g.d_y = dsts[i].stride_y;
+            g.d_x = dsts[i].stride_x;
+            g.d_c = dsts[i].stride_c;
+            if (g.dtype == DT_U8)
+                k_direct<DT_U8><<<nb, 1024, p.k2_smem, s>>>(g, dtab, targets[i], target_map);
+            else if (g.dtype == DT_U16)
+                k_direct<DT_U16><<<nb, 1024, p.k2_smem, s>>>(g, dtab, targets[i], target_map);
+            else
+                k_direct<DT_F32><<<nb, 1024, p.k2_smem, s>>>(g, dtab, targets[i], target_map);
+            g_launches += 1;
+        }
+        if (cudaError_t e = cudaGetLastError()) return cuda_fail(e, "kernel launch");
+        if (opt->flags & IMF_FLAG_PROFILE) {
+            cudaStreamSynchronize(s);
+            g_prof = ProfileRec{};
+            g_prof.tiles = p.total_tiles;
+            g_prof.tile = p.g.Tw;
+            g_prof.qs = 3;
+        }
+        return IMF_OK;
+    }
 
     static thread_local KTab kt;
     build_ktab_struct(kernel, p.g.Sw, kt);

@@ -3,5 +3,6 @@
 #include "imf_sort.cu"
 #include "imf_select.cu"
 #include "imf_pair.cu"
+#include "imf_direct.cu"
 #include "imf_api.cu"
 #include "imf_peak.cu"

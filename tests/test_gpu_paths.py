@@ -6,7 +6,8 @@ shared memory vs in L2 (IMF_PAIR_OMG), rounded-rect footprint on/off
 (IMF_FOOTPRINT), f32 bucket transform vs LSD radix sort (IMF_F32_BUCKET),
 register-resident vs two-pass u16 counting sort (IMF_K1REG), the pair path on
 generic-span kernels (IMF_PAIR_ANY), polygons on the general path
-(IMF_PAIR_POLY=0), one chunk stream (IMF_LANES), rectangular pair tiles (IMF_PAIR_RECT),
+(IMF_PAIR_POLY=0), one chunk stream (IMF_LANES), per-group phases (IMF_GROUPED),
+direct selection for tiny windows (IMF_DIRECT), rectangular pair tiles (IMF_PAIR_RECT),
 and tile / seed-row overrides.  Compared against the C oracle, which is itself
 pinned to the reference's golden outputs (tests/test_oracle.py)."""
 import os
@@ -30,6 +31,7 @@ VARIANTS = [
     {"IMF_PAIR_POLY": "0"},
     {"IMF_LANES": "1"},
     {"IMF_GROUPED": "0"},
+    {"IMF_DIRECT": "0"},
     {"IMF_PAIR_RECT": "1", "IMF_TILE": "64"},
     {"IMF_TILE": "40", "IMF_SEED_ROWS": "4"},
     {"IMF_STRIPE_EDGE": "1", "IMF_STRIPE_MID": "5"},
@@ -42,6 +44,9 @@ CASES = [  # (dtype, shape, kernel spec)
     ("float32", (260, 240), ("circle", 60, 0, 0.0)),      # f32 global-entries bucket
     ("uint8", (190, 170, 2), ("regular_polygon", 11, 6, 15.0)),
     ("uint8", (120, 130), ("square", 7, 0, 0.0)),
+    ("float32", (70, 90), ("circle", 2, 0, 0.0)),         # direct selection (area <= 32)
+    ("uint16", (65, 77, 3), ("square", 2, 0, 0.0)),
+    ("uint8", (40, 33), ("regular_polygon", 3, 5, 10.0)),
 ]
 
 
