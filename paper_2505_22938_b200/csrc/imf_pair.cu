@@ -627,19 +627,16 @@ __global__ void __launch_bounds__(512) k2_pair(Geom g, PairParams p, const __gri
         {
             const int Pg = (N >> 1) & ~1, Pq = Pg >> hs;
             const int cx = cs + r, cy = row + r;
-            // rank < pivot over the window, two pixels per 32-bit load (the
-            // pair-packed compare of the slides; the ends of a row segment masked)
-            const uint32_t K = pivot_k(Pq, Pq);
-            uint32_t cntp = 0;
+            int cntp = 0;
             for (int dy = half; dy <= 2 * r; dy += 2) {
                 const int sp = span_s[dy];
-                const int a = (cy - r + dy) * Sw + cx + (int)(short)(sp & 0xffff), b = a + (sp >> 16);
-                for (int pp = (a & ~1) + 2 * lane; pp < b; pp += 64) {
-                    const uint32_t vm = (pp >= a ? 0x8000u : 0u) | (pp + 1 < b ? 0x80000000u : 0u);
-                    cntp += __popc(~(lds32(I_a + 2 * pp) + K) & vm);
+                const int w = sp >> 16;
+                const uint16_t* rowp = I + (cy - r + dy) * Sw + cx + (int)(short)(sp & 0xffff);
+                for (int o0 = 0; o0 < w; o0 += 32) {
+                    const int o = o0 + lane;
+                    cntp += __popc(__ballot_sync(0xffffffffu, o < w && (int)rowp[o] < Pq));
                 }
             }
-            cntp = __reduce_add_sync(0xffffffffu, cntp);
             if (lane == 0) gsc[gi * 64 + half] = cntp;
             gbar();
             if (half == 0) {
