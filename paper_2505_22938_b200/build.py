@@ -16,7 +16,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libisomedian_b200.so")
 SOURCES = ["imf_lib.cu"]
-DEPS = ["imf_api.cu", "imf_sort.cu", "imf_select.cu", "imf_pair.cu", "imf_direct.cu", "imf_peak.cu"]
+DEPS = ["imf_api.cu", "imf_sort.cu", "imf_select.cu", "imf_pair.cu", "imf_direct.cu", "imf_grank.cu", "imf_peak.cu"]
 HEADERS = ["imf_common.cuh", os.path.join("..", "..", "include", "isomedian_b200.h")]
 
 NVCC_FLAGS = [

@@ -51,7 +51,8 @@ struct Plan {
     bool pair;  // K2 fast path (imf_pair.cu): two windows per thread, 15-bit ranks
     size_t k1_smem, k2_smem, k1_gs_per_tile;
     long long total_tiles, chunk_tiles;
-    size_t ws_omega, ws_k1g, ws_flags, ws_lane, ws_total;
+    size_t ws_omega, ws_k1g, ws_flags, ws_lane, ws_gr, ws_total;
+    int gr_y0, gr_rows, gr_shift;  // f32 image ranks (imf_grank.cu): rows and key shift
     int lanes;  // chunk streams (1 or 2)
 };
 
@@ -288,7 +289,25 @@ int make_plan(const imf_image* src, const imf_kernel* k, const imf_options* opt,
     p.ws_k1g = (size_t)chunk * p.k1_gs_per_tile;
     p.ws_flags = p.k1_f32b ? (((size_t)(chunk + 1) * 4 + 255) & ~(size_t)255) : 0;
     p.ws_lane = p.ws_omega + p.ws_k1g + p.ws_flags;
-    p.ws_total = kStatusBytes + p.lanes * p.ws_lane;
+    // f32, opt-in (IMF_GRANK=1): rank the keys of the rows this launch reads,
+    // image-wide, first (bucket sizes <= 64 everywhere; measured slower than the
+    // tile-local buckets on c3 -- the 4-pass global radix sort costs ~1 ms for
+    // 4 Mpixels as written)
+    p.ws_gr = 0;
+    if (g.dtype == DT_F32 && p.k1_f32b && env_int("IMF_GRANK", 0)) {
+        const int y0 = std::max(0, std::min(H, g.oy_base - r + g.vshift));
+        const int y1 = std::max(y0, std::min(H, g.out_h + r + g.vshift));
+        const long long n = (long long)(y1 - y0) * W;
+        if (n > 0 && n < (1ll << 31)) {
+            int bits = 0;
+            while ((1ll << bits) < n) bits++;
+            p.gr_y0 = y0;
+            p.gr_rows = y1 - y0;
+            p.gr_shift = 32 - bits;
+            p.ws_gr = ((4 * (size_t)n * g.B * g.C + 255) & ~(size_t)255) + 4 * gr_scratch_words(n);
+        }
+    }
+    p.ws_total = kStatusBytes + p.lanes * p.ws_lane + p.ws_gr;
     return IMF_OK;
 }
 
@@ -509,11 +528,44 @@ static int filter_impl(const imf_image* src, imf_image* dsts, int n, const int32
 
     static thread_local KTab kt;
     build_ktab_struct(kernel, p.g.Sw, kt);
+    uint32_t* grank = nullptr;
+    float gr_ms = 0.f;
+    cudaEvent_t gr_e0 = nullptr, gr_e1 = nullptr;
+    if (p.ws_gr && (opt->flags & IMF_FLAG_PROFILE)) {
+        cudaEventCreate(&gr_e0);
+        cudaEventCreate(&gr_e1);
+        cudaEventRecord(gr_e0, s);
+    }
+    if (p.ws_gr) {  // f32: image-wide ranks of every plane's rows, before any tile
+        grank = (uint32_t*)(ws + kStatusBytes + p.lanes * p.ws_lane);
+        const long long n = (long long)p.gr_rows * p.g.W;
+        uint32_t* scratch = grank + (((size_t)n * p.g.B * p.g.C * 4 + 255) & ~(size_t)255) / 4;
+        Geom gg = p.g;
+        gg.src = src->data;
+        for (int b = 0; b < p.g.B; b++)
+            for (int c = 0; c < p.g.C; c++)
+                if (cudaError_t e = gr_rank_plane(gg, b, c, p.gr_y0, p.gr_y0 + p.gr_rows,
+                                                  grank + (size_t)(b * p.g.C + c) * n, scratch, s))
+                    return cuda_fail(e, "image ranks");
+    }
+    if (gr_e0) {
+        cudaEventRecord(gr_e1, s);
+        cudaEventSynchronize(gr_e1);
+        cudaEventElapsedTime(&gr_ms, gr_e0, gr_e1);
+        cudaEventDestroy(gr_e0);
+        cudaEventDestroy(gr_e1);
+    }
     if (!(opt->flags & IMF_FLAG_KEEP_STATUS))
         if (cudaError_t e = cudaMemsetAsync(status, 0, sizeof(int), s)) return cuda_fail(e, "status memset");
 
     Geom g = p.g;
     g.src = src->data;
+    if (grank) {
+        g.gr = grank;
+        g.gr_y0 = p.gr_y0;
+        g.gr_rows = p.gr_rows;
+        g.gr_shift = p.gr_shift;
+    }
 
     SelParams sp;
     memset(&sp, 0, sizeof(sp));
@@ -646,6 +698,7 @@ static int filter_impl(const imf_image* src, imf_image* dsts, int n, const int32
             g_prof.launches += 1;
         }
         for (cudaEvent_t e : ev) cudaEventDestroy(e);
+        g_prof.sort_ms += gr_ms;  // image ranks are part of the ordinal transform
         g_prof.tiles = p.total_tiles;
         g_prof.tile = p.g.Tw;
         g_prof.qs = p.pair ? 2 : (p.omg ? 1 : 0);

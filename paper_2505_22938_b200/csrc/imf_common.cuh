@@ -35,6 +35,8 @@ struct Geom {
     int r;
     int Tw, Th, Sw, Sh, N, Npad;   // N: ranked pixels per tile; Npad: N rounded up to a multiple of 64
     int fp, fpR2;                  // fp: only pixels within dist^2 <= fpR2 of the output rect are ranked
+    const uint32_t* gr;            // f32: image-wide ranks (imf_grank.cu) replace the keys, or nullptr
+    int gr_y0, gr_rows, gr_shift;  // rows [gr_y0, gr_y0 + gr_rows) of every plane; key = rank << gr_shift
     int tiles_x, tiles_y;
     long long tile_begin;          // first tile of this launch (chunking)
     unsigned mx, my, mc;           // division magics: n / d == (n * m) >> s for n < 2^31 (host: set_magic)
@@ -119,11 +121,24 @@ __device__ __forceinline__ uint32_t float_key(uint32_t u) {
     return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
 }
 
+// u32 order key of f32 image pixel (yy, xx) (clamped image coordinates): the
+// float key (ordinal.py:109-123), or its image-wide rank when g.gr is set.
+__device__ __forceinline__ uint32_t f32_key(const Geom& g, const TileCoord& tc, int yy, int xx) {
+    if (g.gr)
+        return __ldg(g.gr + ((long long)(tc.b * g.C + tc.c) * g.gr_rows + (yy - g.gr_y0)) * g.W + xx) << g.gr_shift;
+    return float_key(__ldg((const uint32_t*)tc.src + (long long)yy * g.s_y + (long long)xx * g.s_x));
+}
+
 __device__ __forceinline__ uint32_t load_key(const Geom& g, const TileCoord& tc, int ly, int lx) {
+    if (g.dtype == DT_F32) {
+        int y = tc.oy0 + ly - g.r + g.vshift, x = tc.ox0 + lx - g.r + g.vshift;
+        y = y < 0 ? 0 : (y >= g.H ? g.H - 1 : y);
+        x = x < 0 ? 0 : (x >= g.W ? g.W - 1 : x);
+        return f32_key(g, tc, y, x);
+    }
     long long o = src_offset(g, tc, ly, lx);
     if (g.dtype == DT_U8) return __ldg((const uint8_t*)tc.src + o);
-    if (g.dtype == DT_U16) return __ldg((const uint16_t*)tc.src + o);
-    return float_key(__ldg((const uint32_t*)tc.src + o));
+    return __ldg((const uint16_t*)tc.src + o);
 }
 
 // y = i / Sw, x = i % Sw for i < 65536, Sw <= 256, via an exact float reciprocal

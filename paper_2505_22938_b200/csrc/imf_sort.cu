@@ -559,23 +559,21 @@ __global__ void __launch_bounds__(1024) k1_f32_bucket(Geom g, uint16_t* __restri
     uint32_t v[NK][NK];
     unsigned long long okm = 0;  // which of this thread's pixels are ranked
     {
-        long long xo[NK];
+        int xc[NK];
 #pragma unroll
         for (int k = 0; k < NK; k++) {
             int x = tc.ox0 + lane + 32 * k - g.r + g.vshift;
-            x = x < 0 ? 0 : (x >= g.W ? g.W - 1 : x);
-            xo[k] = (long long)x * g.s_x;
+            xc[k] = x < 0 ? 0 : (x >= g.W ? g.W - 1 : x);
         }
 #pragma unroll
         for (int j = 0; j < NK; j++) {
             const int y = wid + 32 * j;
             int yy = tc.oy0 + y - g.r + g.vshift;
             yy = yy < 0 ? 0 : (yy >= g.H ? g.H - 1 : yy);
-            const long long ro = (long long)yy * g.s_y;
 #pragma unroll
             for (int k = 0; k < NK; k++) {
                 const bool ok = y < SH && lane + 32 * k < S && in_footprint(g, lane + 32 * k, y);
-                v[j][k] = ok ? float_key(__ldg((const uint32_t*)tc.src + ro + xo[k])) : 0u;
+                v[j][k] = ok ? f32_key(g, tc, yy, xc[k]) : 0u;
                 okm |= (ok ? 1ull : 0ull) << (j * NK + k);
             }
         }
@@ -661,13 +659,12 @@ __global__ void __launch_bounds__(1024) k1_f32_bucket_g(Geom g, uint16_t* __rest
     for (int y = wid; y < SH; y += nw) {
         int yy = tc.oy0 + y - g.r + g.vshift;
         yy = yy < 0 ? 0 : (yy >= g.H ? g.H - 1 : yy);
-        const char* rp = tc.src + (long long)yy * g.s_y * 4;
         for (int k = 0; k < nk; k++) {
             const int x = lane + 32 * k;
             if (x < S) {
                 int xx = tc.ox0 + x - g.r + g.vshift;
                 xx = xx < 0 ? 0 : (xx >= g.W ? g.W - 1 : xx);
-                const uint32_t h = float_key(__ldg((const uint32_t*)rp + (long long)xx * g.s_x)) >> 16;
+                const uint32_t h = f32_key(g, tc, yy, xx) >> 16;
                 const uint32_t sh = (h & 1) << 4;
                 atomicAdd(&hw[h >> 1], 1u << sh);
             }
@@ -683,13 +680,12 @@ __global__ void __launch_bounds__(1024) k1_f32_bucket_g(Geom g, uint16_t* __rest
     for (int y = wid; y < SH; y += nw) {
         int yy = tc.oy0 + y - g.r + g.vshift;
         yy = yy < 0 ? 0 : (yy >= g.H ? g.H - 1 : yy);
-        const char* rp = tc.src + (long long)yy * g.s_y * 4;
         for (int k = 0; k < nk; k++) {
             const int x = lane + 32 * k;
             if (x < S) {
                 int xx = tc.ox0 + x - g.r + g.vshift;
                 xx = xx < 0 ? 0 : (xx >= g.W ? g.W - 1 : xx);
-                const uint32_t key = float_key(__ldg((const uint32_t*)rp + (long long)xx * g.s_x));
+                const uint32_t key = f32_key(g, tc, yy, xx);
                 const uint32_t h = key >> 16, sh = (h & 1) << 4;
                 const uint32_t old = atomicAdd(&hw[h >> 1], 1u << sh);
                 ent[(old >> sh) & 0xffffu] = (key << 16) | (uint32_t)(x | (y << 8));
