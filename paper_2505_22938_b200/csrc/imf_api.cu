@@ -277,10 +277,13 @@ int make_plan(const imf_image* src, const imf_kernel* k, const imf_options* opt,
     // lanes only when there are >= 4 such chunks' worth of tiles.
     // (The f32 global-entries transform is K1-bound: its chunks overlap even
     // when small.)
-    const long long min_chunk = p.k1_f32b_g ? 148 : 592;
+    const long long min_chunk = p.k1_f32b_g ? 296 : 592;
     p.lanes = (p.total_tiles >= (p.k1_f32b_g ? 2 : 3) * min_chunk && env_int("IMF_LANES", 2) > 1) ? 2 : 1;
     long long chunk = (long long)(kOmegaScratchTarget / p.lanes / per_tile);
-    if (p.lanes == 2) chunk = std::min<long long>(chunk, std::max<long long>(min_chunk, (p.total_tiles + 5) / 6));
+    if (p.lanes == 2) {
+        chunk = std::min<long long>(chunk, std::max<long long>(min_chunk, (p.total_tiles + 5) / 6));
+        chunk = std::max<long long>(148, chunk / 148 * 148);  // whole waves of one-CTA-per-SM K1
+    }
     chunk = std::max<long long>(chunk, 148);
     chunk = std::min<long long>(chunk, p.total_tiles);
     chunk = std::min<long long>(chunk, 65535LL * 1024);
