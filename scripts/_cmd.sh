@@ -1,2 +1,2 @@
 python -c "from paper_2505_22938_b200 import build as b; assert not b.stale(), \"stale .so\"" || exit 3
-timeout 300 python scripts/quick_bench.py c2 c3 c5 | cut -c1-110
+timeout 900 python -m pytest tests/test_gpu_paths.py -x -q 2>&1 | tail -5

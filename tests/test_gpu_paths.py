@@ -79,3 +79,25 @@ def test_variant_bit_exact(variant, monkeypatch):
                 got = filter_image(img, params)
                 want = oracle.fast_filter(img, params.shape, p, boundary)
                 assert got.tobytes() == want.tobytes(), (variant, dt, shape, spec, boundary, p)
+
+
+@pytest.mark.parametrize("dt", ["uint8", "uint16", "float32"])
+def test_direct_selection_maps_bracket_tiny_images(dt):
+    """Direct-selection kernel (window area <= 32): per-pixel percentile maps,
+    valid boundary, the bracket, and images smaller than one 32-pixel tile."""
+    from paper_2505_22938_b200 import FilterParams, ShapeSpec, filter_image, filter_image_bracket
+    rng = np.random.default_rng(99)
+    for shape in ((1, 1), (3, 5), (31, 33, 2), (77, 45)):
+        img = _input(dt, shape, 5)
+        for spec in (ShapeSpec("circle", 2), ShapeSpec("square", 1), ShapeSpec("circle", 0)):
+            pmap = rng.random(shape[:2])
+            got = filter_image(img, FilterParams(shape=spec, percentile=pmap))
+            want = oracle.fast_filter(img, spec, pmap, "replicate")
+            assert got.tobytes() == want.tobytes(), (dt, shape, spec)
+            if min(shape[:2]) > 2 * spec.radius:
+                got = filter_image(img, FilterParams(shape=spec, boundary="valid", percentile=0.7))
+                want = oracle.fast_filter(img, spec, 0.7, "valid")
+                assert got.tobytes() == want.tobytes(), (dt, shape, spec, "valid")
+        outs = filter_image_bracket(img, FilterParams(shape=ShapeSpec("circle", 2)), [0.0, 0.5, 1.0])
+        for out, p in zip(outs, (0.0, 0.5, 1.0)):
+            assert out.tobytes() == oracle.fast_filter(img, ShapeSpec("circle", 2), p).tobytes()
