@@ -44,48 +44,67 @@ __global__ void __launch_bounds__(GR_THREADS) k_gr_hist(const uint32_t* __restri
     for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[(long long)i * gridDim.x + blockIdx.x] = h[i];
 }
 
-// exclusive scan of len entries by one block
-__global__ void __launch_bounds__(1024) k_gr_scan(uint32_t* __restrict__ a, int len) {
-    __shared__ uint32_t wt[32];
-    __shared__ uint32_t carry_s;
+// Exclusive scan of the digit-major block histograms in two levels: one CTA
+// per digit scans that digit's row over the nb blocks (and writes the row
+// total), then one CTA turns the 256 totals into digit bases.
+__device__ __forceinline__ uint32_t block_excl_scan_1024(uint32_t v, uint32_t* wt, uint32_t& total) {
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    if (tid == 0) carry_s = 0;
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += t;
+    }
+    if (lane == 31) wt[wid] = x;
     __syncthreads();
-    for (int base = 0; base < len; base += 1024) {
-        const int i = base + tid;
-        const uint32_t v = i < len ? a[i] : 0u;
-        uint32_t x = v;
+    if (wid == 0) {
+        const uint32_t w = wt[lane];
+        uint32_t y = w;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t t = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= o) x += t;
+            const uint32_t t = __shfl_up_sync(0xffffffffu, y, o);
+            if (lane >= o) y += t;
         }
-        if (lane == 31) wt[wid] = x;
-        __syncthreads();
-        if (wid == 0) {
-            const uint32_t w = wt[lane];
-            uint32_t y = w;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t t = __shfl_up_sync(0xffffffffu, y, o);
-                if (lane >= o) y += t;
-            }
-            wt[lane] = y - w;
-        }
-        __syncthreads();
-        const uint32_t carry = carry_s;
-        if (i < len) a[i] = carry + wt[wid] + x - v;
-        __syncthreads();
-        if (tid == 1023) carry_s = carry + wt[wid] + x;
-        __syncthreads();
+        wt[lane] = y - w;
+        if (lane == 31) wt[32] = y;
     }
+    __syncthreads();
+    total = wt[32];
+    const uint32_t r = wt[wid] + x - v;
+    __syncthreads();
+    return r;
+}
+
+__global__ void __launch_bounds__(1024) k_gr_scan_rows(uint32_t* __restrict__ hist, int nb,
+                                                       uint32_t* __restrict__ totals) {
+    __shared__ uint32_t wt[33];
+    uint32_t* row = hist + (long long)blockIdx.x * nb;
+    uint32_t carry = 0;
+    for (int base = 0; base < nb; base += 1024) {
+        const int i = base + threadIdx.x;
+        const uint32_t v = i < nb ? row[i] : 0u;
+        uint32_t tot;
+        const uint32_t ex = block_excl_scan_1024(v, wt, tot);
+        if (i < nb) row[i] = carry + ex;
+        carry += tot;
+    }
+    if (threadIdx.x == 0) totals[blockIdx.x] = carry;
+}
+
+__global__ void __launch_bounds__(1024) k_gr_scan_totals(uint32_t* __restrict__ totals) {
+    __shared__ uint32_t wt[33];
+    const uint32_t v = threadIdx.x < 256 ? totals[threadIdx.x] : 0u;
+    uint32_t tot;
+    const uint32_t ex = block_excl_scan_1024(v, wt, tot);
+    if (threadIdx.x < 256) totals[threadIdx.x] = ex;
 }
 
 // stable scatter of one block's elements by digit
 __global__ void __launch_bounds__(GR_THREADS) k_gr_scatter(const uint32_t* __restrict__ kin,
                                                            const uint32_t* __restrict__ iin,
                                                            uint32_t* __restrict__ kout, uint32_t* __restrict__ iout,
-                                                           int n, int shift, const uint32_t* __restrict__ hist) {
+                                                           int n, int shift, const uint32_t* __restrict__ hist,
+                                                           const uint32_t* __restrict__ dbase) {
     __shared__ uint32_t cnt[256][33];  // [digit][warp], padded row
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const unsigned lt = lanemask_lt();
@@ -104,7 +123,7 @@ __global__ void __launch_bounds__(GR_THREADS) k_gr_scatter(const uint32_t* __res
     __syncthreads();
     // 2. per digit: global offset of this block + prefix over warps
     if (tid < 256) {
-        uint32_t run = hist[(long long)tid * gridDim.x + blockIdx.x];
+        uint32_t run = dbase[tid] + hist[(long long)tid * gridDim.x + blockIdx.x];
         for (int w = 0; w < 32; w++) {
             const uint32_t c = cnt[tid][w];
             cnt[tid][w] = run;
@@ -137,7 +156,7 @@ __global__ void k_gr_final(const uint32_t* __restrict__ idx_sorted, int n, uint3
 
 // Host: ranks of plane (b, c) rows [y0, y1) into grank (n = (y1-y0)*W entries);
 // scratch: 4 arrays of n u32 + 256 * ceil(n / GR_CH) u32.
-inline size_t gr_scratch_words(long long n) { return 4 * (size_t)n + 256 * (size_t)((n + GR_CH - 1) / GR_CH) + 64; }
+inline size_t gr_scratch_words(long long n) { return 4 * (size_t)n + 256 * (size_t)((n + GR_CH - 1) / GR_CH) + 512; }
 
 inline cudaError_t gr_rank_plane(const Geom& g, int b, int c, int y0, int y1, uint32_t* grank, uint32_t* scratch,
                                  cudaStream_t s) {
@@ -150,11 +169,13 @@ inline cudaError_t gr_rank_plane(const Geom& g, int b, int c, int y0, int y1, ui
     uint32_t* iA = kB + n;
     uint32_t* iB = iA + n;
     uint32_t* hist = iB + n;
+    uint32_t* dbase = hist + 256 * (size_t)nb;
     k_gr_keys<<<std::min(nb * 4, 4096), 1024, 0, s>>>(g, b, c, y0, y1, kA, iA);
     for (int pass = 0; pass < 4; pass++) {
         k_gr_hist<<<nb, GR_THREADS, 0, s>>>(kA, n, 8 * pass, hist);
-        k_gr_scan<<<1, 1024, 0, s>>>(hist, 256 * nb);
-        k_gr_scatter<<<nb, GR_THREADS, 0, s>>>(kA, iA, kB, iB, n, 8 * pass, hist);
+        k_gr_scan_rows<<<256, 1024, 0, s>>>(hist, nb, dbase);
+        k_gr_scan_totals<<<1, 1024, 0, s>>>(dbase);
+        k_gr_scatter<<<nb, GR_THREADS, 0, s>>>(kA, iA, kB, iB, n, 8 * pass, hist, dbase);
         std::swap(kA, kB);
         std::swap(iA, iB);
     }
