@@ -361,11 +361,16 @@ cudaError_t set_attrs() {
     IMF_K1R_ATTR(DT_U8)
     IMF_K1R_ATTR(DT_U16)
 #undef IMF_K1R_ATTR
-    if (!e) e = allow_smem(k1_f32_bucket<1>, optin);
-    if (!e) e = allow_smem(k1_f32_bucket<2>, optin);
-    if (!e) e = allow_smem(k1_f32_bucket<3>, optin);
-    if (!e) e = allow_smem(k1_f32_bucket<4>, optin);
-    if (!e) e = allow_smem(k1_f32_bucket<5>, optin);
+#define IMF_K1F_ATTR(NK)                                               \
+    if (!e) e = allow_smem(k1_f32_bucket<NK, false>, optin);           \
+    if (!e) e = allow_smem(k1_f32_bucket<NK, true>, optin);
+    IMF_K1F_ATTR(1)
+    IMF_K1F_ATTR(2)
+    IMF_K1F_ATTR(3)
+    IMF_K1F_ATTR(4)
+    IMF_K1F_ATTR(5)
+    IMF_K1F_ATTR(6)
+#undef IMF_K1F_ATTR
     if (!e) e = allow_smem(k1_f32_bucket_g, optin);
     if (!e) e = allow_smem(k_direct<DT_U8>, optin);
     if (!e) e = allow_smem(k_direct<DT_U16>, optin);
@@ -393,15 +398,24 @@ void launch_k1(const Plan& p, const Geom& g, int nblocks, uint16_t* omega, unsig
     if (p.k1_f32b) {
         const dim3 b1024(1024);
         cudaMemsetAsync(flags, 0, sizeof(int), s);  // fallback list count
-        if (p.k1_f32b_g)
+        const int nk = (g.Sw + 31) >> 5;
+        if (p.k1_f32b_g && nk > 6) {
             k1_f32_bucket_g<<<grid, b1024, p.k1b_smem, s>>>(g, omega, flags, (uint32_t*)k1g, gs / 4);
-        else
-        switch ((g.Sw + 31) >> 5) {
-            case 1: k1_f32_bucket<1><<<grid, b1024, p.k1b_smem, s>>>(g, omega, flags); break;
-            case 2: k1_f32_bucket<2><<<grid, b1024, p.k1b_smem, s>>>(g, omega, flags); break;
-            case 3: k1_f32_bucket<3><<<grid, b1024, p.k1b_smem, s>>>(g, omega, flags); break;
-            case 4: k1_f32_bucket<4><<<grid, b1024, p.k1b_smem, s>>>(g, omega, flags); break;
-            default: k1_f32_bucket<5><<<grid, b1024, p.k1b_smem, s>>>(g, omega, flags); break;
+        } else {
+#define IMF_K1F_LAUNCH(NK)                                                                                  \
+    if (p.k1_f32b_g)                                                                                         \
+        k1_f32_bucket<NK, true><<<grid, b1024, p.k1b_smem, s>>>(g, omega, flags, (uint32_t*)k1g, gs / 4);    \
+    else                                                                                                     \
+        k1_f32_bucket<NK, false><<<grid, b1024, p.k1b_smem, s>>>(g, omega, flags, nullptr, 0);
+            switch (nk) {
+                case 1: IMF_K1F_LAUNCH(1) break;
+                case 2: IMF_K1F_LAUNCH(2) break;
+                case 3: IMF_K1F_LAUNCH(3) break;
+                case 4: IMF_K1F_LAUNCH(4) break;
+                case 5: IMF_K1F_LAUNCH(5) break;
+                default: IMF_K1F_LAUNCH(6) break;
+            }
+#undef IMF_K1F_LAUNCH
         }
         // tiles with a bucket above kMaxBucket: LSD radix sort over the list
         const dim3 fgrid(std::min(nblocks, 148));

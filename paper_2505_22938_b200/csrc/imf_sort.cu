@@ -543,17 +543,20 @@ IMF_K1R(DT_U16)
 // thread of a 1024-thread CTA) the tile goes to the LSD radix sort instead.
 constexpr unsigned long long kMaxSumSq = 64ull << 20;
 
-template <int NK>
+// GENT: the entries live in the tile's global scratch slot (tiles too large
+// for shared-memory entries); the keys stay in registers either way.
+template <int NK, bool GENT>
 __global__ void __launch_bounds__(1024) k1_f32_bucket(Geom g, uint16_t* __restrict__ omega_out,
-                                                     int* __restrict__ fallback) {
+                                                     int* __restrict__ fallback, uint32_t* __restrict__ gent,
+                                                     long long gent_stride) {
     extern __shared__ __align__(16) unsigned char smem[];
     constexpr int NW = 32768;  // histogram words (65536 16-bit counters)
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const TileCoord tc = tile_coord(g, g.tile_begin + blockIdx.x);
     const int S = g.Sw, SH = g.Sh, N = g.N;
     uint32_t* hw = reinterpret_cast<uint32_t*>(smem);
-    uint32_t* ent = hw + NW;                  // N entries
-    uint32_t* starts = ent + ((N + 3) & ~3);  // bucket-start bitmap, ceil(N/32) words
+    uint32_t* ent = GENT ? gent + blockIdx.x * gent_stride : hw + NW;  // N entries
+    uint32_t* starts = GENT ? hw + NW : ent + ((N + 3) & ~3);        // bucket starts, ceil(N/32) words
     const int nsw = (N + 31) >> 5;
     __shared__ unsigned long long s_sumsq;
     uint32_t v[NK][NK];
@@ -715,11 +718,16 @@ __global__ void __launch_bounds__(1024) k1_f32_bucket_g(Geom g, uint16_t* __rest
 
 size_t k1_f32_bucket_g_smem_bytes(int N) { return 32768 * 4 + 4 * (size_t)((N + 31) >> 5) + 16; }
 
-template __global__ void k1_f32_bucket<1>(Geom, uint16_t*, int*);
-template __global__ void k1_f32_bucket<2>(Geom, uint16_t*, int*);
-template __global__ void k1_f32_bucket<3>(Geom, uint16_t*, int*);
-template __global__ void k1_f32_bucket<4>(Geom, uint16_t*, int*);
-template __global__ void k1_f32_bucket<5>(Geom, uint16_t*, int*);
+#define IMF_K1F(NK)                                                                                  \
+    template __global__ void k1_f32_bucket<NK, false>(Geom, uint16_t*, int*, uint32_t*, long long);  \
+    template __global__ void k1_f32_bucket<NK, true>(Geom, uint16_t*, int*, uint32_t*, long long);
+IMF_K1F(1)
+IMF_K1F(2)
+IMF_K1F(3)
+IMF_K1F(4)
+IMF_K1F(5)
+IMF_K1F(6)
+#undef IMF_K1F
 
 size_t k1_f32_bucket_smem_bytes(int N) {
     return 32768 * 4 + 4 * (size_t)((N + 3) & ~3) + 4 * (size_t)((N + 31) >> 5) + 16;
