@@ -225,7 +225,10 @@ int make_plan(const imf_image* src, const imf_kernel* k, const imf_options* opt,
     p.k1_count = g.dtype != DT_F32 && k1_count_smem_bytes(g.dtype, g.Npad) <= kSmemMax;
     p.k1b_smem = k1_f32_bucket_smem_bytes(g.N);
     p.k1_f32b = g.dtype == DT_F32 && env_int("IMF_F32_BUCKET", 1) && g.Sw <= 160 && p.k1b_smem <= kSmemMax;
-    if (g.dtype == DT_F32 && !p.k1_f32b && env_int("IMF_F32_BUCKET", 1)) {
+    // f32 tiles beyond shared-memory entries, and u16 tiles beyond the 64K-bin
+    // counting sort (S > ~180): the bucket transform with global entries
+    // (u16 keys v << 16: every bucket is one value, ties only)
+    if ((g.dtype == DT_F32 || (g.dtype == DT_U16 && !p.k1_count)) && !p.k1_f32b && env_int("IMF_F32_BUCKET", 1)) {
         p.k1_f32b = p.k1_f32b_g = true;
         p.k1b_smem = k1_f32_bucket_g_smem_bytes(g.N);
     }
@@ -417,12 +420,19 @@ void launch_k1(const Plan& p, const Geom& g, int nblocks, uint16_t* omega, unsig
             }
 #undef IMF_K1F_LAUNCH
         }
-        // tiles with a bucket above kMaxBucket: LSD radix sort over the list
+        // tiles whose buckets are too large (sum of squared sizes above the
+        // limit): LSD radix sort over the list
         const dim3 fgrid(std::min(nblocks, 148));
-        if (p.k1_gmem)
+        if (g.dtype == DT_U16) {
+            if (p.k1_gmem)
+                k1_sort<DT_U16, true><<<fgrid, block, p.k1_smem, s>>>(g, omega, k1g, gs, flags);
+            else
+                k1_sort<DT_U16, false><<<fgrid, block, p.k1_smem, s>>>(g, omega, k1g, gs, flags);
+        } else if (p.k1_gmem) {
             k1_sort<DT_F32, true><<<fgrid, block, p.k1_smem, s>>>(g, omega, k1g, gs, flags);
-        else
+        } else {
             k1_sort<DT_F32, false><<<fgrid, block, p.k1_smem, s>>>(g, omega, k1g, gs, flags);
+        }
         return;
     }
     if (p.k1_count) {

@@ -124,6 +124,8 @@ __device__ __forceinline__ uint32_t float_key(uint32_t u) {
 // u32 order key of f32 image pixel (yy, xx) (clamped image coordinates): the
 // float key (ordinal.py:109-123), or its image-wide rank when g.gr is set.
 __device__ __forceinline__ uint32_t f32_key(const Geom& g, const TileCoord& tc, int yy, int xx) {
+    if (g.dtype == DT_U16)  // bucket transform on u16 tiles: the value in the high half
+        return (uint32_t)__ldg((const uint16_t*)tc.src + (long long)yy * g.s_y + (long long)xx * g.s_x) << 16;
     if (g.gr)
         return __ldg(g.gr + ((long long)(tc.b * g.C + tc.c) * g.gr_rows + (yy - g.gr_y0)) * g.W + xx) << g.gr_shift;
     return float_key(__ldg((const uint32_t*)tc.src + (long long)yy * g.s_y + (long long)xx * g.s_x));

@@ -42,6 +42,7 @@ VARIANTS = [
 CASES = [  # (dtype, shape, kernel spec)
     ("uint16", (211, 301, 3), ("circle", 48, 0, 0.0)),
     ("uint16", (150, 170), ("circle", 62, 0, 0.0)),       # halved ranks (N > 32768)
+    ("uint16", (260, 250), ("circle", 100, 0, 0.0)),      # u16 bucket transform (S = 255)
     ("float32", (180, 200), ("circle", 20, 0, 0.0)),
     ("float32", (260, 240), ("circle", 60, 0, 0.0)),      # f32 global-entries bucket
     ("uint8", (190, 170, 2), ("regular_polygon", 11, 6, 15.0)),
