@@ -70,6 +70,12 @@ __device__ __forceinline__ uint32_t lds32(uint32_t a) {
     return v;
 }
 
+__device__ __forceinline__ uint32_t lds16(uint32_t a) {
+    unsigned short v;
+    asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
+    return v;
+}
+
 __device__ __forceinline__ uint4 lds128(uint32_t a) {
     uint4 q;
     asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
@@ -481,6 +487,7 @@ __global__ void __launch_bounds__(512) k2_pair(Geom g, PairParams p, const __gri
     int* span_s = seedC + G;                   // 2r+1
     uint32_t* rowk = reinterpret_cast<uint32_t*>(span_s + 2 * r + 1);  // 256 (SH_POLY)
     uint32_t* gsc = rowk + 256;                                         // 2 * G * 32 (grouped phase C)
+    int* rowd = reinterpret_cast<int*>(gsc + 64 * G);                   // TY + 1 (grouped seed counts)
 
     // ---- 0. stage omega, build the ordinal image --------------------------
     {
@@ -505,6 +512,7 @@ __global__ void __launch_bounds__(512) k2_pair(Geom g, PairParams p, const __gri
         }
         for (int i = Sw * g.Sh + tid; i < Ipad; i += blockDim.x) I[i] = 0;
         if (tid < 32) hist[tid] = 0;
+        for (int i = tid; i <= TY; i += blockDim.x) rowd[i] = 0;
         for (int i = tid; i < 2 * r + 1; i += blockDim.x) span_s[i] = kt.span[i];
         if (SHAPE == SH_POLY) {
             for (int i = tid; i < 256; i += blockDim.x) {
@@ -621,36 +629,63 @@ __global__ void __launch_bounds__(512) k2_pair(Geom g, PairParams p, const __gri
         const int q = lane, rest = wid, gi = rest % G, half = rest / G;  // half 0: down warp
         const int row = seed_row(gi);
         auto gbar = [&]() { asm volatile("bar.sync %0, 64;" ::"r"(1 + gi) : "memory"); };
-        // this group's seed: the centre window of its seed row, from an exact count
-        // at the even pivot N/2 (the group's two warps split the window rows), then
-        // a warp-collaborative walk (core.py:47-60, :87-146) -- no CTA-wide phase
+        // this group's seed: the centre window of its seed row.  The counts
+        // below the even pivot N/2 of ALL groups' seed windows come from one
+        // CTA-wide pass -- the top group's window in full plus the down-slide
+        // deltas of column cs between the seed rows (rowd[TY], rowd[y]) --
+        // then each group walks warp-collaboratively to its target
+        // (core.py:47-60, :87-146).
+        const int Pg = (N >> 1) & ~1;
         {
-            const int Pg = (N >> 1) & ~1, Pq = Pg >> hs;
-            const int cx = cs + r, cy = row + r;
-            int cntp = 0;
-            for (int dy = half; dy <= 2 * r; dy += 2) {
-                const int sp = span_s[dy];
-                const int w = sp >> 16;
-                const uint16_t* rowp = I + (cy - r + dy) * Sw + cx + (int)(short)(sp & 0xffff);
-                for (int o0 = 0; o0 < w; o0 += 32) {
-                    const int o = o0 + lane;
-                    cntp += __popc(__ballot_sync(0xffffffffu, o < w && (int)rowp[o] < Pq));
+            const int Pq = Pg >> hs;
+            {
+                const int cx = cs + r, cy = ytop + r;
+                int cnt = 0;
+                for (int dy = wid; dy <= 2 * r; dy += nwarps) {
+                    const int sp = span_s[dy];
+                    const int w = sp >> 16;
+                    const uint16_t* rowp = I + (cy - r + dy) * Sw + cx + (int)(short)(sp & 0xffff);
+                    for (int o0 = 0; o0 < w; o0 += 32) {
+                        const int o = o0 + lane;
+                        cnt += __popc(__ballot_sync(0xffffffffu, o < w && (int)rowp[o] < Pq));
+                    }
+                }
+                if (lane == 0 && cnt) atomicAdd(&rowd[TY], cnt);
+            }
+            // down-slide deltas (entering < Pq) - (exiting < Pq) of the column-cs
+            // window from row y to y+1: lanes = rows, warps split the column list
+            const int nr = ybot - ytop;
+            if (nr > 0) {
+                const int nrc = (nr + 31) >> 5, kc_n = max(1, nwarps / nrc);
+                for (int u = wid; u < nrc * kc_n; u += nwarps) {
+                    const int rc = u / kc_n, kc = u - rc * kc_n;
+                    const int y = ytop + rc * 32 + lane;
+                    const int k0 = kc * p.nv / kc_n, k1 = (kc + 1) * p.nv / kc_n;
+                    const uint32_t b = I_a + 2 * (min(y, ybot - 1) * Sw + cs);
+                    int d = 0;
+                    for (int k = k0; k < k1; k++) {
+                        const int2 o = kt.v[k];
+                        const int adj = k >= p.nv_even ? 2 : 0;  // odd entries: the high half of the word
+                        d += ((int)lds16(b + o.x + adj) < Pq) - ((int)lds16(b + o.y + adj) < Pq);
+                    }
+                    if (y < ybot && d) atomicAdd(&rowd[y], d);
                 }
             }
-            if (lane == 0) gsc[gi * 64 + half] = cntp;
-            gbar();
-            if (half == 0) {
-                const int cnt = (int)(gsc[gi * 64] + gsc[gi * 64 + 1]);
-                const int tgt = target_at2(g, p, tc, row, cs);
-                const int m = refine_warp2<SHAPE>(c, cx, cy, Pg, cnt, tgt);
-                if (lane == 0) {
-                    if (m < 0) atomicOr(p.status, 1);
-                    seedP[gi] = max(m, 0);
-                    seedC[gi] = tgt;
-                }
-            }
-            gbar();
         }
+        __syncthreads();
+        if (half == 0) {
+            int part = 0;
+            for (int y = ytop + lane; y < row; y += 32) part += rowd[y];
+            const int cnt = rowd[TY] + (int)__reduce_add_sync(0xffffffffu, (unsigned)part);
+            const int tgt = target_at2(g, p, tc, row, cs);
+            const int m = refine_warp2<SHAPE>(c, cs + r, row + r, Pg, cnt, tgt);
+            if (lane == 0) {
+                if (m < 0) atomicOr(p.status, 1);
+                seedP[gi] = max(m, 0);
+                seedC[gi] = tgt;
+            }
+        }
+        gbar();
         int P, C0;
         to_state<SHAPE>(c, hs, seedP[gi], seedC[gi], cs + r, row + r, P, C0);
         uint32_t* gin = gsc + gi * 64;  // [0..32): entering counts, [32..64): exiting counts
@@ -797,7 +832,7 @@ size_t k2_pair_smem_bytes(int N, int Npad, int NI, int r, int G, int T, int TY, 
     const int Ipad = (NI + 15) & ~7;
     const int gt = G * T;
     return (omg ? 0 : 2 * (size_t)(Npad + 16)) + 2 * (size_t)Ipad +
-           4 * (size_t)(2 * gt + (gt > TY ? gt : TY) + 32 + 2 * G + 2 * r + 1 + 256 + 64 * G) + 16;
+           4 * (size_t)(2 * gt + (gt > TY ? gt : TY) + 32 + 2 * G + 2 * r + 1 + 256 + 64 * G + TY + 1) + 16;
 }
 
 // Host: build the pair tables for input-tile row stride Sw.  Returns false if

@@ -1,3 +1,3 @@
 python -c "from paper_2505_22938_b200 import build as b; assert not b.stale(), \"stale .so\"" || exit 3
 timeout 900 python -m pytest tests -x -q -m gpu 2>&1 | tail -2
-for c in "u16 2048 2048 1 100" "u16 2048 2048 1 90" "f32 2048 2048 1 100"; do timeout 120 python scripts/quick_one.py $c; done
+timeout 300 python scripts/quick_bench.py c2 c3 c4 c5 2>&1 | cut -c1-200
