@@ -401,15 +401,16 @@ void launch_k1(const Plan& p, const Geom& g, int nblocks, uint16_t* omega, unsig
     if (p.k1_f32b) {
         const dim3 b1024(1024);
         cudaMemsetAsync(flags, 0, sizeof(int), s);  // fallback list count
+        static const unsigned long long mss = (unsigned long long)env_int("IMF_MAXSUMSQ_K", 65536) << 10;
         const int nk = (g.Sw + 31) >> 5;
         if (p.k1_f32b_g && nk > 6) {
-            k1_f32_bucket_g<<<grid, b1024, p.k1b_smem, s>>>(g, omega, flags, (uint32_t*)k1g, gs / 4);
+            k1_f32_bucket_g<<<grid, b1024, p.k1b_smem, s>>>(g, omega, flags, (uint32_t*)k1g, gs / 4, mss);
         } else {
 #define IMF_K1F_LAUNCH(NK)                                                                                  \
     if (p.k1_f32b_g)                                                                                         \
-        k1_f32_bucket<NK, true><<<grid, b1024, p.k1b_smem, s>>>(g, omega, flags, (uint32_t*)k1g, gs / 4);    \
+        k1_f32_bucket<NK, true><<<grid, b1024, p.k1b_smem, s>>>(g, omega, flags, (uint32_t*)k1g, gs / 4, mss); \
     else                                                                                                     \
-        k1_f32_bucket<NK, false><<<grid, b1024, p.k1b_smem, s>>>(g, omega, flags, nullptr, 0);
+        k1_f32_bucket<NK, false><<<grid, b1024, p.k1b_smem, s>>>(g, omega, flags, nullptr, 0, mss);
             switch (nk) {
                 case 1: IMF_K1F_LAUNCH(1) break;
                 case 2: IMF_K1F_LAUNCH(2) break;

@@ -543,79 +543,94 @@ IMF_K1R(DT_U16)
 // thread of a 1024-thread CTA) the tile goes to the LSD radix sort instead.
 constexpr unsigned long long kMaxSumSq = 64ull << 20;
 
-// GENT: the entries live in the tile's global scratch slot (tiles too large
-// for shared-memory entries); the keys stay in registers either way.
-template <int NK, bool GENT>
-__global__ void __launch_bounds__(1024) k1_f32_bucket(Geom g, uint16_t* __restrict__ omega_out,
-                                                     int* __restrict__ fallback, uint32_t* __restrict__ gent,
-                                                     long long gent_stride) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    constexpr int NW = 32768;  // histogram words (65536 16-bit counters)
-    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const TileCoord tc = tile_coord(g, g.tile_begin + blockIdx.x);
-    const int S = g.Sw, SH = g.Sh, N = g.N;
-    uint32_t* hw = reinterpret_cast<uint32_t*>(smem);
-    uint32_t* ent = GENT ? gent + blockIdx.x * gent_stride : hw + NW;  // N entries
-    uint32_t* starts = GENT ? hw + NW : ent + ((N + 3) & ~3);        // bucket starts, ceil(N/32) words
-    const int nsw = (N + 31) >> 5;
-    __shared__ unsigned long long s_sumsq;
-    uint32_t v[NK][NK];
-    unsigned long long okm = 0;  // which of this thread's pixels are ranked
-    {
-        int xc[NK];
-#pragma unroll
-        for (int k = 0; k < NK; k++) {
-            int x = tc.ox0 + lane + 32 * k - g.r + g.vshift;
-            xc[k] = x < 0 ? 0 : (x >= g.W ? g.W - 1 : x);
-        }
-#pragma unroll
-        for (int j = 0; j < NK; j++) {
-            const int y = wid + 32 * j;
-            int yy = tc.oy0 + y - g.r + g.vshift;
-            yy = yy < 0 ? 0 : (yy >= g.H ? g.H - 1 : yy);
-#pragma unroll
-            for (int k = 0; k < NK; k++) {
-                const bool ok = y < SH && lane + 32 * k < S && in_footprint(g, lane + 32 * k, y);
-                v[j][k] = ok ? f32_key(g, tc, yy, xc[k]) : 0u;
-                okm |= (ok ? 1ull : 0ull) << (j * NK + k);
-            }
-        }
+// Replicate-boundary copies.  Tile column x reads image column clamp(X0 + x);
+// the columns reading one clamped image column are a contiguous range
+// [first, first + cnt).  (Same for rows.)
+__device__ __forceinline__ void rep_axis(int X0, int x, int S, int W, int& cnt, bool& first) {
+    const int X = X0 + x;
+    if (W == 1) {
+        cnt = S;
+        first = x == 0;
+    } else if (X <= 0) {
+        cnt = min(S, 1 - X0);
+        first = x == 0;
+    } else if (X >= W - 1) {
+        const int f = max(0, W - 1 - X0);
+        cnt = S - f;
+        first = x == f;
+    } else {
+        cnt = 1;
+        first = true;
     }
-    {
-        uint4* h4 = reinterpret_cast<uint4*>(hw);
-        for (int i = tid; i < NW / 4; i += blockDim.x) h4[i] = make_uint4(0, 0, 0, 0);
-        for (int i = tid; i < nsw; i += blockDim.x) starts[i] = 0;
-        if (tid == 0) s_sumsq = 0;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int j = 0; j < NK; j++)
-#pragma unroll
-        for (int k = 0; k < NK; k++)
-            if ((okm >> (j * NK + k)) & 1ull) {
-                const uint32_t h = v[j][k] >> 16, sh = (h & 1) << 4;
-                atomicAdd(&hw[h >> 1], 1u << sh);
-            }
-    __syncthreads();
-    hist16_exclusive_scan(hw, NW, starts, &s_sumsq);
-    __syncthreads();
-    if (s_sumsq > kMaxSumSq) {  // block-uniform: hand the tile to the radix sort
-        if (tid == 0) fallback[1 + atomicAdd(fallback, 1)] = blockIdx.x;
+}
+
+// Weight of a tile pixel in the bucket transform: the copies of one image
+// pixel (replicate boundary, >= kRunMin of them: tile corners and edges) are
+// ranked once, as a RUN of consecutive ranks held by the first copy (weight =
+// copy count, the others 0); ties order arbitrarily (imf_sort.cu header), so
+// the run's internal order is free.  Entries of a run starting at slot s:
+//   ent[s]     = key16 << 16 | 0xffff                  (run head)
+//   ent[s + 1] = pos << 16 | 0xfffe                     (first copy x | y << 8)
+//   ent[s + 2] = (cnt_x | cnt_y << 8) << 16 | 0xfffe    (copy rectangle)
+//   ent[s + 3 ..] = 0xfffe                               (interior)
+// Plain entries are key16 << 16 | pos with pos <= 0xfefe (x, y < 255).
+// Only groups of >= kRunMin copies become runs: ranking a group of m plain
+// copies costs m^2 compares (~1 per thread at m = 32 for a 1024-thread CTA),
+// which only the tile-corner groups, (r+1)^2 copies, make worth the run
+// bookkeeping (measured: edges, r+1 copies, gain nothing even at r = 100).
+constexpr int kRunMin = 1024;
+
+// Largest copy group of a tile (columns [X0, X0 + S) of an image W wide).
+__device__ __forceinline__ int max_copies(int X0, int S, int W) {
+    if (W == 1) return S;
+    const int l = X0 < 0 ? min(S, 1 - X0) : 1;
+    const int r = X0 + S > W ? S - max(0, W - 1 - X0) : 1;
+    return max(l, r);
+}
+
+__device__ __forceinline__ bool has_runs(const Geom& g, const TileCoord& tc) {
+    const int X0 = tc.ox0 - g.r + g.vshift, Y0 = tc.oy0 - g.r + g.vshift;
+    return !g.fp && max_copies(X0, g.Sw, g.W) * max_copies(Y0, g.Sh, g.H) >= kRunMin;
+}
+
+__device__ __forceinline__ int pixel_weight(int cx, bool fx, int cy, bool fy) {
+    const int m = cx * cy;
+    if (m < kRunMin) return 1;
+    return (fx && fy) ? m : 0;
+}
+
+__device__ __forceinline__ void put_entry(uint32_t* ent, int slot, uint32_t key16, int x, int y, int w, int cx,
+                                          int cy) {
+    const uint32_t pos = (uint32_t)(x | (y << 8));
+    if (w == 1) {
+        ent[slot] = (key16 << 16) | pos;
         return;
     }
-#pragma unroll
-    for (int j = 0; j < NK; j++)
-#pragma unroll
-        for (int k = 0; k < NK; k++)
-            if ((okm >> (j * NK + k)) & 1ull) {
-                const uint32_t key = v[j][k], h = key >> 16, sh = (h & 1) << 4;
-                const uint32_t old = atomicAdd(&hw[h >> 1], 1u << sh);
-                ent[(old >> sh) & 0xffffu] = (key << 16) | (uint32_t)((lane + 32 * k) | ((wid + 32 * j) << 8));
-            }
-    __syncthreads();
-    uint16_t* om = reinterpret_cast<uint16_t*>(hw);  // the histogram is dead: omega goes here
-    for (int sp = tid; sp < N; sp += blockDim.x) {
+    ent[slot] = (key16 << 16) | 0xffffu;
+    ent[slot + 1] = (pos << 16) | 0xfffeu;
+    ent[slot + 2] = ((uint32_t)(cx | (cy << 8)) << 16) | 0xfffeu;
+    for (int i = 3; i < w; i++) ent[slot + i] = 0xfffeu;
+}
+
+// Rank every entry within its bucket (starts: bucket-start bitmap) and write
+// omega.  Each scan is bounded (kScanMax steps); a thread past its budget sets
+// *abort and the caller hands the tile to the radix sort (block-uniform after
+// the closing barrier).  Long runs are filled by the whole CTA.
+constexpr int kScanMax = 4096;
+constexpr int kScanBudget = 16384;
+constexpr int kBigRuns = 16;
+
+// RUNS = false (tiles without runs, already bounded by the sum-of-squares
+// estimate): the plain unrolled compare loop.
+template <bool RUNS>
+__device__ void rank_buckets(const uint32_t* ent, const uint32_t* starts, int N, uint16_t* om, int* abort_flag,
+                             int* nbig, uint4* big) {
+    const int nsw = (N + 31) >> 5;
+    int work = 0;
+    for (int sp = threadIdx.x; sp < N; sp += blockDim.x) {
         const uint32_t e = ent[sp];
+        const uint32_t lo = e & 0xffffu;
+        if (RUNS && lo == 0xfffeu) continue;  // inside a run
         int w = sp >> 5;
         uint32_t m = starts[w] & (0xffffffffu >> (31 - (sp & 31)));  // start bits <= sp
         while (!m) m = starts[--w];
@@ -625,12 +640,204 @@ __global__ void __launch_bounds__(1024) k1_f32_bucket(Geom g, uint16_t* __restri
         while (!m && ++w < nsw) m = starts[w];
         const int b1 = m ? (w << 5) + __ffs(m) - 1 : N;
         int rk = b0;
-        for (int q = b0; q < b1; q++) rk += ent[q] < e ? 1 : 0;
-        om[rk] = (uint16_t)(e & 0xffffu);
+        if (!RUNS) {
+            for (int q = b0; q < b1; q++) rk += ent[q] < e ? 1 : 0;
+            om[rk] = (uint16_t)lo;
+            continue;
+        }
+        int q = b0, it = 0;
+        for (; q < b1 && it < kScanMax; it++) {
+            if (q + 4 <= b1) {  // four plain entries at once (no run head among them)
+                const uint32_t v0 = ent[q], v1 = ent[q + 1], v2 = ent[q + 2], v3 = ent[q + 3];
+                const bool h = (v0 & 0xffffu) == 0xffffu || (v1 & 0xffffu) == 0xffffu ||
+                               (v2 & 0xffffu) == 0xffffu || (v3 & 0xffffu) == 0xffffu;
+                if (!h) {
+                    rk += (v0 < e ? 1 : 0) + (v1 < e ? 1 : 0) + (v2 < e ? 1 : 0) + (v3 < e ? 1 : 0);
+                    q += 4;
+                    continue;
+                }
+            }
+            const uint32_t v = ent[q];
+            if ((v & 0xffffu) == 0xffffu) {  // run head: the run orders as a whole
+                const uint32_t d = ent[q + 2] >> 16;
+                const int len = (int)(d & 0xffu) * (int)(d >> 8);
+                rk += (v < e || (v == e && q < sp)) ? len : 0;
+                q += len;
+            } else {
+                rk += v < e ? 1 : 0;
+                q++;
+            }
+        }
+        work += it;
+        if (q < b1 || work > kScanBudget) {
+            *abort_flag = 1;
+            break;
+        }
+        if (lo != 0xffffu) {
+            om[rk] = (uint16_t)lo;
+            continue;
+        }
+        const uint32_t pos = ent[sp + 1] >> 16, d = ent[sp + 2] >> 16;
+        const int cx = (int)(d & 0xffu), cy = (int)(d >> 8), len = cx * cy;
+        if (len > 256) {
+            const int k = atomicAdd(nbig, 1);
+            if (k < kBigRuns) {
+                big[k] = make_uint4((uint32_t)rk, pos, (uint32_t)cx, (uint32_t)cy);
+                continue;
+            }
+        }
+        for (int i = 0; i < len; i++) {
+            const int yy = i / cx, xx = i - yy * cx;
+            om[rk + i] = (uint16_t)(pos + (uint32_t)(xx | (yy << 8)));
+        }
     }
+}
+
+// After the barrier closing rank_buckets: fill the long runs with the CTA.
+__device__ void fill_big_runs(uint16_t* om, int nbig, const uint4* big) {
+    for (int k = 0; k < min(nbig, kBigRuns); k++) {
+        const uint4 b = big[k];
+        const int cx = (int)b.z, len = cx * (int)b.w;
+        for (int i = threadIdx.x; i < len; i += blockDim.x) {
+            const int yy = i / cx, xx = i - yy * cx;
+            om[b.x + i] = (uint16_t)(b.y + (uint32_t)(xx | (yy << 8)));
+        }
+    }
+}
+
+// GENT: the entries live in the tile's global scratch slot (tiles too large
+// for shared-memory entries); the keys stay in registers either way.
+// EDGE: the tile reads clamped (replicated) image pixels; the copies of one
+// pixel are ranked as a run (pixel_weight).  Interior tiles take the EDGE =
+// false instance, which carries none of that.
+template <int NK, bool GENT, bool EDGE>
+__device__ __forceinline__ void f32_bucket_tile(const Geom& g, const TileCoord& tc, uint16_t* __restrict__ omega_out,
+                                                int* __restrict__ fallback, uint32_t* __restrict__ gent,
+                                                long long gent_stride, unsigned long long max_sumsq) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    constexpr int NW = 32768;  // histogram words (65536 16-bit counters)
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int S = g.Sw, SH = g.Sh, N = g.N;
+    uint32_t* hw = reinterpret_cast<uint32_t*>(smem);
+    uint32_t* ent = GENT ? gent + blockIdx.x * gent_stride : hw + NW;  // N entries
+    uint32_t* starts = GENT ? hw + NW : ent + ((N + 3) & ~3);        // bucket starts, ceil(N/32) words
+    const int nsw = (N + 31) >> 5;
+    __shared__ unsigned long long s_sumsq;
+    __shared__ int s_runs, s_abort, s_nbig;
+    __shared__ uint4 s_big[kBigRuns];
+    uint32_t v[NK][NK];
+    unsigned long long okm = 0;  // which of this thread's pixels are ranked (weight > 0)
+    // replicate copies (rep_axis), edge tiles only, recomputed where used
+    // (keeps the 1024-thread register budget for the keys)
+    const int X0 = tc.ox0 - g.r + g.vshift, Y0 = tc.oy0 - g.r + g.vshift;
+    auto weight = [&](int j, int k) {
+        if (!EDGE) return 1;
+        int cx, cy;
+        bool fx, fy;
+        rep_axis(X0, lane + 32 * k, S, g.W, cx, fx);
+        rep_axis(Y0, wid + 32 * j, SH, g.H, cy, fy);
+        return pixel_weight(cx, fx, cy, fy);
+    };
+    auto cnt_x = [&](int k) {
+        int c;
+        bool f;
+        rep_axis(X0, lane + 32 * k, S, g.W, c, f);
+        return c;
+    };
+    auto cnt_y = [&](int j) {
+        int c;
+        bool f;
+        rep_axis(Y0, wid + 32 * j, SH, g.H, c, f);
+        return c;
+    };
+    {
+        int xc[NK];
+#pragma unroll
+        for (int k = 0; k < NK; k++) {
+            int x = X0 + lane + 32 * k;
+            xc[k] = x < 0 ? 0 : (x >= g.W ? g.W - 1 : x);
+        }
+#pragma unroll
+        for (int j = 0; j < NK; j++) {
+            const int y = wid + 32 * j;
+            int yy = Y0 + y;
+            yy = yy < 0 ? 0 : (yy >= g.H ? g.H - 1 : yy);
+#pragma unroll
+            for (int k = 0; k < NK; k++) {
+                const bool ok = y < SH && lane + 32 * k < S && in_footprint(g, lane + 32 * k, y) && weight(j, k) > 0;
+                v[j][k] = ok ? f32_key(g, tc, yy, xc[k]) : 0u;
+                okm |= (ok ? 1ull : 0ull) << (j * NK + k);
+            }
+        }
+    }
+    {
+        uint4* h4 = reinterpret_cast<uint4*>(hw);
+        for (int i = tid; i < NW / 4; i += blockDim.x) h4[i] = make_uint4(0, 0, 0, 0);
+        for (int i = tid; i < nsw; i += blockDim.x) starts[i] = 0;
+        if (tid == 0) {
+            s_sumsq = 0;
+            s_runs = s_abort = s_nbig = 0;
+        }
+    }
+    __syncthreads();
+    bool runs = false;
+#pragma unroll
+    for (int j = 0; j < NK; j++)
+#pragma unroll
+        for (int k = 0; k < NK; k++)
+            if ((okm >> (j * NK + k)) & 1ull) {
+                const uint32_t h = v[j][k] >> 16, sh = (h & 1) << 4;
+                const int wt = weight(j, k);
+                runs |= wt > 1;
+                atomicAdd(&hw[h >> 1], (uint32_t)wt << sh);
+            }
+    if (runs) s_runs = 1;
+    __syncthreads();
+    hist16_exclusive_scan(hw, NW, starts, &s_sumsq);
+    __syncthreads();
+    // tiles with runs skip the estimate (run weights inflate it); their scans
+    // are bounded instead (rank_buckets)
+    if (!s_runs && s_sumsq > max_sumsq) {  // block-uniform: hand the tile to the radix sort
+        if (tid == 0) fallback[1 + atomicAdd(fallback, 1)] = blockIdx.x;
+        return;
+    }
+#pragma unroll
+    for (int j = 0; j < NK; j++)
+#pragma unroll
+        for (int k = 0; k < NK; k++)
+            if ((okm >> (j * NK + k)) & 1ull) {
+                const uint32_t key = v[j][k], h = key >> 16, sh = (h & 1) << 4;
+                const int wt = weight(j, k);
+                const uint32_t old = atomicAdd(&hw[h >> 1], (uint32_t)wt << sh);
+                put_entry(ent, (old >> sh) & 0xffffu, key & 0xffffu, lane + 32 * k, wid + 32 * j, wt, cnt_x(k),
+                          cnt_y(j));
+            }
+    __syncthreads();
+    uint16_t* om = reinterpret_cast<uint16_t*>(hw);  // the histogram is dead: omega goes here
+    if (s_runs)
+        rank_buckets<true>(ent, starts, N, om, &s_abort, &s_nbig, s_big);
+    else
+        rank_buckets<false>(ent, starts, N, om, &s_abort, &s_nbig, s_big);
+    __syncthreads();
+    if (s_abort) {
+        if (tid == 0) fallback[1 + atomicAdd(fallback, 1)] = blockIdx.x;
+        return;
+    }
+    fill_big_runs(om, s_nbig, s_big);
     for (int i = N + tid; i < g.Npad; i += blockDim.x) om[i] = 0xffffu;
     __syncthreads();
     store_omega(g, om, omega_slot(g, omega_out));
+}
+
+template <int NK, bool GENT>
+__global__ void __launch_bounds__(1024) k1_f32_bucket(Geom g, uint16_t* __restrict__ omega_out,
+                                                     int* __restrict__ fallback, uint32_t* __restrict__ gent,
+                                                     long long gent_stride, unsigned long long max_sumsq) {
+    const TileCoord tc = tile_coord(g, g.tile_begin + blockIdx.x);
+    if (has_runs(g, tc))
+        f32_bucket_tile<NK, GENT, true>(g, tc, omega_out, fallback, gent, gent_stride, max_sumsq);
+    else
+        f32_bucket_tile<NK, GENT, false>(g, tc, omega_out, fallback, gent, gent_stride, max_sumsq);
 }
 
 // k1_f32_bucket for tiles too large for shared-memory entries (N > ~23.7K,
@@ -640,7 +847,8 @@ __global__ void __launch_bounds__(1024) k1_f32_bucket(Geom g, uint16_t* __restri
 // histogram (later omega) and the bucket-start bitmap stay in shared memory.
 __global__ void __launch_bounds__(1024) k1_f32_bucket_g(Geom g, uint16_t* __restrict__ omega_out,
                                                        int* __restrict__ fallback,
-                                                       uint32_t* __restrict__ gent, long long gent_stride) {
+                                                       uint32_t* __restrict__ gent, long long gent_stride,
+                                                       unsigned long long max_sumsq) {
     extern __shared__ __align__(16) unsigned char smem[];
     constexpr int NW = 32768;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
@@ -651,66 +859,90 @@ __global__ void __launch_bounds__(1024) k1_f32_bucket_g(Geom g, uint16_t* __rest
     const int nsw = (N + 31) >> 5;
     uint32_t* ent = gent + blockIdx.x * gent_stride;
     __shared__ unsigned long long s_sumsq;
+    __shared__ int s_runs, s_abort, s_nbig;
+    __shared__ uint4 s_big[kBigRuns];
+    const int X0 = tc.ox0 - g.r + g.vshift, Y0 = tc.oy0 - g.r + g.vshift;
+    const bool edge = has_runs(g, tc);
     {
         uint4* h4 = reinterpret_cast<uint4*>(hw);
         for (int i = tid; i < NW / 4; i += blockDim.x) h4[i] = make_uint4(0, 0, 0, 0);
         for (int i = tid; i < nsw; i += blockDim.x) starts[i] = 0;
-        if (tid == 0) s_sumsq = 0;
-    }
-    __syncthreads();
-    const int nk = (S + 31) >> 5;
-    for (int y = wid; y < SH; y += nw) {
-        int yy = tc.oy0 + y - g.r + g.vshift;
-        yy = yy < 0 ? 0 : (yy >= g.H ? g.H - 1 : yy);
-        for (int k = 0; k < nk; k++) {
-            const int x = lane + 32 * k;
-            if (x < S) {
-                int xx = tc.ox0 + x - g.r + g.vshift;
-                xx = xx < 0 ? 0 : (xx >= g.W ? g.W - 1 : xx);
-                const uint32_t h = f32_key(g, tc, yy, xx) >> 16;
-                const uint32_t sh = (h & 1) << 4;
-                atomicAdd(&hw[h >> 1], 1u << sh);
-            }
+        if (tid == 0) {
+            s_sumsq = 0;
+            s_runs = s_abort = s_nbig = 0;
         }
     }
     __syncthreads();
+    const int nk = (S + 31) >> 5;
+    bool runs = false;
+    for (int y = wid; y < SH; y += nw) {
+        int yy = Y0 + y;
+        yy = yy < 0 ? 0 : (yy >= g.H ? g.H - 1 : yy);
+        int cy = 1;
+        bool fy = true;
+        if (edge) rep_axis(Y0, y, SH, g.H, cy, fy);
+        for (int k = 0; k < nk; k++) {
+            const int x = lane + 32 * k;
+            if (x < S) {
+                int xx = X0 + x;
+                xx = xx < 0 ? 0 : (xx >= g.W ? g.W - 1 : xx);
+                int cx = 1;
+                bool fx = true;
+                if (edge) rep_axis(X0, x, S, g.W, cx, fx);
+                const int wt = pixel_weight(cx, fx, cy, fy);
+                if (wt) {
+                    runs |= wt > 1;
+                    const uint32_t h = f32_key(g, tc, yy, xx) >> 16;
+                    const uint32_t sh = (h & 1) << 4;
+                    atomicAdd(&hw[h >> 1], (uint32_t)wt << sh);
+                }
+            }
+        }
+    }
+    if (runs) s_runs = 1;
+    __syncthreads();
     hist16_exclusive_scan(hw, NW, starts, &s_sumsq);
     __syncthreads();
-    if (s_sumsq > kMaxSumSq) {
+    if (!s_runs && s_sumsq > max_sumsq) {
         if (tid == 0) fallback[1 + atomicAdd(fallback, 1)] = blockIdx.x;
         return;
     }
     for (int y = wid; y < SH; y += nw) {
-        int yy = tc.oy0 + y - g.r + g.vshift;
+        int yy = Y0 + y;
         yy = yy < 0 ? 0 : (yy >= g.H ? g.H - 1 : yy);
+        int cy = 1;
+        bool fy = true;
+        if (edge) rep_axis(Y0, y, SH, g.H, cy, fy);
         for (int k = 0; k < nk; k++) {
             const int x = lane + 32 * k;
             if (x < S) {
-                int xx = tc.ox0 + x - g.r + g.vshift;
+                int xx = X0 + x;
                 xx = xx < 0 ? 0 : (xx >= g.W ? g.W - 1 : xx);
-                const uint32_t key = f32_key(g, tc, yy, xx);
-                const uint32_t h = key >> 16, sh = (h & 1) << 4;
-                const uint32_t old = atomicAdd(&hw[h >> 1], 1u << sh);
-                ent[(old >> sh) & 0xffffu] = (key << 16) | (uint32_t)(x | (y << 8));
+                int cx = 1;
+                bool fx = true;
+                if (edge) rep_axis(X0, x, S, g.W, cx, fx);
+                const int wt = pixel_weight(cx, fx, cy, fy);
+                if (wt) {
+                    const uint32_t key = f32_key(g, tc, yy, xx);
+                    const uint32_t h = key >> 16, sh = (h & 1) << 4;
+                    const uint32_t old = atomicAdd(&hw[h >> 1], (uint32_t)wt << sh);
+                    put_entry(ent, (old >> sh) & 0xffffu, key & 0xffffu, x, y, wt, cx, cy);
+                }
             }
         }
     }
     __syncthreads();  // block-scope ordering of the entry stores (global, same CTA)
     uint16_t* om = reinterpret_cast<uint16_t*>(hw);
-    for (int sp = tid; sp < N; sp += blockDim.x) {
-        const uint32_t e = ent[sp];
-        int w = sp >> 5;
-        uint32_t m = starts[w] & (0xffffffffu >> (31 - (sp & 31)));
-        while (!m) m = starts[--w];
-        const int b0 = (w << 5) + 31 - __clz(m);
-        w = sp >> 5;
-        m = (sp & 31) == 31 ? 0u : starts[w] & (0xfffffffeu << (sp & 31));
-        while (!m && ++w < nsw) m = starts[w];
-        const int b1 = m ? (w << 5) + __ffs(m) - 1 : N;
-        int rk = b0;
-        for (int q = b0; q < b1; q++) rk += ent[q] < e ? 1 : 0;
-        om[rk] = (uint16_t)(e & 0xffffu);
+    if (s_runs)
+        rank_buckets<true>(ent, starts, N, om, &s_abort, &s_nbig, s_big);
+    else
+        rank_buckets<false>(ent, starts, N, om, &s_abort, &s_nbig, s_big);
+    __syncthreads();
+    if (s_abort) {
+        if (tid == 0) fallback[1 + atomicAdd(fallback, 1)] = blockIdx.x;
+        return;
     }
+    fill_big_runs(om, s_nbig, s_big);
     for (int i = N + tid; i < g.Npad; i += blockDim.x) om[i] = 0xffffu;
     __syncthreads();
     store_omega(g, om, omega_slot(g, omega_out));
@@ -719,8 +951,10 @@ __global__ void __launch_bounds__(1024) k1_f32_bucket_g(Geom g, uint16_t* __rest
 size_t k1_f32_bucket_g_smem_bytes(int N) { return 32768 * 4 + 4 * (size_t)((N + 31) >> 5) + 16; }
 
 #define IMF_K1F(NK)                                                                                  \
-    template __global__ void k1_f32_bucket<NK, false>(Geom, uint16_t*, int*, uint32_t*, long long);  \
-    template __global__ void k1_f32_bucket<NK, true>(Geom, uint16_t*, int*, uint32_t*, long long);
+    template __global__ void k1_f32_bucket<NK, false>(Geom, uint16_t*, int*, uint32_t*, long long,  \
+                                                      unsigned long long);                          \
+    template __global__ void k1_f32_bucket<NK, true>(Geom, uint16_t*, int*, uint32_t*, long long,   \
+                                                     unsigned long long);
 IMF_K1F(1)
 IMF_K1F(2)
 IMF_K1F(3)
