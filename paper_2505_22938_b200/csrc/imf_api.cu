@@ -223,6 +223,7 @@ int make_plan(const imf_image* src, const imf_kernel* k, const imf_options* opt,
     if (p.total_tiles >= (1ll << 31)) return IMF_ERR_UNSUPPORTED;  // tile_coord uses 32-bit indices
 
     p.k1_count = g.dtype != DT_F32 && k1_count_smem_bytes(g.dtype, g.Npad) <= kSmemMax;
+    g.run_min = std::max(kRunMinFloor, env_int("IMF_RUNMIN", kRunMin));
     p.k1b_smem = k1_f32_bucket_smem_bytes(g.N);
     p.k1_f32b = g.dtype == DT_F32 && env_int("IMF_F32_BUCKET", 1) && g.Sw <= 160 && p.k1b_smem <= kSmemMax;
     // f32 tiles beyond shared-memory entries, and u16 tiles beyond the 64K-bin
@@ -237,9 +238,10 @@ int make_plan(const imf_image* src, const imf_kernel* k, const imf_options* opt,
     p.k1_smem = p.k1_count ? k1_count_smem_bytes(g.dtype, g.Npad)
                            : k1_smem_bytes(g.dtype, g.Npad, p.k1_threads / 32, p.k1_gmem);
     p.k1_gs_per_tile = p.k1_gmem ? k1_gscratch_bytes(g.dtype, g.Npad) : 0;
-    // the global-entries bucket kernel needs 4 B per pixel; the LSD fallback
-    // reuses the same slot (k1_gscratch_bytes(f32) = 6 B per pixel when it needs one)
-    if (p.k1_f32b_g) p.k1_gs_per_tile = std::max(p.k1_gs_per_tile, (size_t)4 * g.Npad);
+    // the global-entries bucket kernels need 6 B per pixel (entries + run
+    // descriptors); the LSD fallback reuses the same slot (k1_gscratch_bytes(f32)
+    // = 6 B per pixel when it needs one)
+    if (p.k1_f32b_g) p.k1_gs_per_tile = std::max(p.k1_gs_per_tile, (size_t)6 * g.Npad);  // + run descriptors
 
     // Rounded-rect footprint (pair path, circle kernels, register-resident K1):
     // rank only input pixels within distance^2 r(r+1) of the output rectangle

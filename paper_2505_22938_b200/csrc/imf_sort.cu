@@ -543,6 +543,52 @@ IMF_K1R(DT_U16)
 // thread of a 1024-thread CTA) the tile goes to the LSD radix sort instead.
 constexpr unsigned long long kMaxSumSq = 64ull << 20;
 
+// Adaptive buckets for f32 keys.  Bucketing on the key's top 16 bits
+// (sign, exponent, 7 mantissa bits) leaves a tile's values in a few hundred
+// buckets of tens of entries each, and the in-bucket ranking costs the sum of
+// squared bucket sizes.  Instead: 4096 coarse bins on key >> 20 are counted
+// first; populated bin c (n_c keys, P populated) gets f_c = 2^l_c fine
+// buckets, f_c = pow2floor(16 + n_c (65536 - 16 P) / N) (>= 16, total <=
+// 65536), splitting it on the next l_c key bits.  A fine bucket then spans
+// <= 2^16 keys (l_c >= 4), so the entry's low 16 key bits still order it, and
+// holds ~2 N / 65536 keys.  tab[c]: coarse count in, base | l_c << 16 out.
+constexpr int kCoarse = 4096;
+// Below this many tile pixels the top-16-bit buckets are already small and the
+// coarse pass (4096-bin atomics, allocation scan) costs more than it saves.
+constexpr int kAdaptiveMinN = 16384;
+
+__device__ void coarse_alloc(uint32_t* tab, int N) {
+    __shared__ int s_pop;
+    const int tid = threadIdx.x, per = kCoarse / 1024;  // 1024-thread CTAs: 4 bins per thread
+    if (tid == 0) s_pop = 0;
+    __syncthreads();
+    int pop = 0;
+    for (int i = 0; i < per; i++) pop += tab[tid * per + i] ? 1 : 0;
+    pop = (int)__reduce_add_sync(0xffffffffu, (unsigned)pop);
+    if ((tid & 31) == 0 && pop) atomicAdd(&s_pop, pop);
+    __syncthreads();
+    const unsigned long long room = 65536ull - 16ull * (unsigned long long)s_pop;
+    uint32_t fv[kCoarse / 1024];
+    for (int i = 0; i < per; i++) {
+        const uint32_t n = tab[tid * per + i];
+        fv[i] = n ? 1u << (31 - __clz(16u + (uint32_t)(n * room / (unsigned long long)N))) : 0u;
+    }
+    __syncthreads();
+    for (int i = 0; i < per; i++) tab[tid * per + i] = fv[i];
+    __syncthreads();
+    block_exclusive_scan(tab, kCoarse);  // ends with a barrier
+    for (int i = 0; i < per; i++) {
+        const int c = tid * per + i;
+        tab[c] = fv[i] ? (tab[c] | ((uint32_t)(31 - __clz(fv[i])) << 16)) : 0u;
+    }
+    __syncthreads();
+}
+
+__device__ __forceinline__ uint32_t fine_bucket(const uint32_t* tab, uint32_t key) {
+    const uint32_t t = tab[key >> 20], l = t >> 16;
+    return (t & 0xffffu) + ((key & 0xfffffu) >> (20 - l));
+}
+
 // Replicate-boundary copies.  Tile column x reads image column clamp(X0 + x);
 // the columns reading one clamped image column are a contiguous range
 // [first, first + cnt).  (Same for rows.)
@@ -565,20 +611,34 @@ __device__ __forceinline__ void rep_axis(int X0, int x, int S, int W, int& cnt, 
 }
 
 // Weight of a tile pixel in the bucket transform: the copies of one image
-// pixel (replicate boundary, >= kRunMin of them: tile corners and edges) are
-// ranked once, as a RUN of consecutive ranks held by the first copy (weight =
-// copy count, the others 0); ties order arbitrarily (imf_sort.cu header), so
-// the run's internal order is free.  Entries of a run starting at slot s:
-//   ent[s]     = key16 << 16 | 0xffff                  (run head)
-//   ent[s + 1] = pos << 16 | 0xfffe                     (first copy x | y << 8)
-//   ent[s + 2] = (cnt_x | cnt_y << 8) << 16 | 0xfffe    (copy rectangle)
-//   ent[s + 3 ..] = 0xfffe                               (interior)
-// Plain entries are key16 << 16 | pos with pos <= 0xfefe (x, y < 255).
-// Only groups of >= kRunMin copies become runs: ranking a group of m plain
-// copies costs m^2 compares (~1 per thread at m = 32 for a 1024-thread CTA),
-// which only the tile-corner groups, (r+1)^2 copies, make worth the run
-// bookkeeping (measured: edges, r+1 copies, gain nothing even at r = 100).
+// pixel (replicate boundary, >= run_min of them) are ranked once, as a RUN of
+// consecutive ranks held by the first copy (weight = copy count, the others
+// 0); ties order arbitrarily (imf_sort.cu header), so the run's internal
+// order is free.  A run of w copies starting at slot s:
+//   ent[s]            = key16 << 16 | 0xffff   (head)
+//   ent[s+1 .. s+w)   = key16 << 16 | 0xfffe   (interior)
+// and a descriptor: first copy x | y << 8 and copy rectangle cx | cy << 8, in
+// the side array d16[s], d16[s+1] (global-entry kernels) or in the CTA's run
+// list (shared-memory entries; a tile with more runs goes to the radix sort).  Plain entries are key16 << 16 | pos, pos <= 0xfefe (x, y <
+// 255).  Ranking orders slots by (entry | 1, slot): the interior of a run then
+// compares exactly like its head, so a bucket scan counts a whole run with
+// plain compares (no data-dependent skip), and only the head's thread ranks it.
 constexpr int kRunMin = 1024;
+constexpr int kRunMinFloor = 2;
+constexpr int kRunList = 64;   // runs per tile without a side array
+// Runs longer than kMarkSelf are LONG: listed (RunList::mark), their interior
+// written by the CTA, and skipped whole by bucket scans (a corner run of
+// (r+1)^2 slots would otherwise be scanned by every entry sharing its bucket).
+constexpr int kMarkSelf = 128;
+constexpr int kBigRuns = 32;   // queued long runs (interior marks, omega fill)
+
+struct RunList {
+    int n, nbig, nmark, abort;
+    uint2 run[kRunList];   // list mode: (slot, pos | cx << 16 | cy << 24)
+    uint2 mark[kBigRuns];  // (slot, key16 << 16 | 0xfffe) of the long runs (kMarkSelf)
+    uint2 mlen[kBigRuns];  // (w, 0)
+    uint4 big[kBigRuns];   // (rank, pos, cx, cy) of heads with more than 256 copies
+};
 
 // Largest copy group of a tile (columns [X0, X0 + S) of an image W wide).
 __device__ __forceinline__ int max_copies(int X0, int S, int W) {
@@ -590,42 +650,88 @@ __device__ __forceinline__ int max_copies(int X0, int S, int W) {
 
 __device__ __forceinline__ bool has_runs(const Geom& g, const TileCoord& tc) {
     const int X0 = tc.ox0 - g.r + g.vshift, Y0 = tc.oy0 - g.r + g.vshift;
-    return !g.fp && max_copies(X0, g.Sw, g.W) * max_copies(Y0, g.Sh, g.H) >= kRunMin;
+    return !g.fp && max_copies(X0, g.Sw, g.W) * max_copies(Y0, g.Sh, g.H) >= g.run_min;
 }
 
-__device__ __forceinline__ int pixel_weight(int cx, bool fx, int cy, bool fy) {
+__device__ __forceinline__ int pixel_weight(int cx, bool fx, int cy, bool fy, int run_min) {
     const int m = cx * cy;
-    if (m < kRunMin) return 1;
+    if (m < run_min) return 1;
     return (fx && fy) ? m : 0;
 }
 
-__device__ __forceinline__ void put_entry(uint32_t* ent, int slot, uint32_t key16, int x, int y, int w, int cx,
-                                          int cy) {
+__device__ __forceinline__ void put_entry(uint32_t* ent, uint16_t* d16, int slot, uint32_t key16, int x, int y,
+                                          int w, int cx, int cy, RunList* rl) {
     const uint32_t pos = (uint32_t)(x | (y << 8));
     if (w == 1) {
         ent[slot] = (key16 << 16) | pos;
         return;
     }
     ent[slot] = (key16 << 16) | 0xffffu;
-    ent[slot + 1] = (pos << 16) | 0xfffeu;
-    ent[slot + 2] = ((uint32_t)(cx | (cy << 8)) << 16) | 0xfffeu;
-    for (int i = 3; i < w; i++) ent[slot + i] = 0xfffeu;
+    if (d16) {
+        d16[slot] = (uint16_t)pos;
+        d16[slot + 1] = (uint16_t)(cx | (cy << 8));
+    } else {
+        const int k = atomicAdd(&rl->n, 1);
+        if (k >= kRunList) {
+            rl->abort = 1;
+            return;
+        }
+        rl->run[k] = make_uint2((uint32_t)slot, pos | ((uint32_t)cx << 16) | ((uint32_t)cy << 24));
+    }
+    const uint32_t mv = (key16 << 16) | 0xfffeu;
+    if (w > kMarkSelf) {
+        const int k = atomicAdd(&rl->nmark, 1);
+        if (k < kBigRuns) {
+            rl->mark[k] = make_uint2((uint32_t)slot, mv);
+            rl->mlen[k] = make_uint2((uint32_t)w, 0u);
+            return;
+        }
+    }
+    for (int i = 1; i < w; i++) ent[slot + i] = mv;
+}
+
+// After the scatter barrier: the interiors of the long runs, by the CTA, then
+// a barrier (block-uniform: rl->nmark is read after one).
+__device__ __forceinline__ void mark_runs(uint32_t* ent, const RunList* rl) {
+    const int n = min(rl->nmark, kBigRuns);
+    if (!n) return;
+    for (int k = 0; k < n; k++) {
+        const uint2 d = rl->mark[k];
+        const int w = (int)rl->mlen[k].x;
+        for (int i = 1 + (int)threadIdx.x; i < w; i += blockDim.x) ent[d.x + i] = d.y;
+    }
+    __syncthreads();
 }
 
 // Rank every entry within its bucket (starts: bucket-start bitmap) and write
-// omega.  Each scan is bounded (kScanMax steps); a thread past its budget sets
-// *abort and the caller hands the tile to the radix sort (block-uniform after
-// the closing barrier).  Long runs are filled by the whole CTA.
-constexpr int kScanMax = 4096;
-constexpr int kScanBudget = 16384;
-constexpr int kBigRuns = 16;
+// omega.  RUNS: the (entry | 1, slot) order above; the head of a run writes
+// its w ranks (long runs: queued for fill_big_runs).
+#ifdef IMF_STATS
+__device__ unsigned long long g_rstats[128];  // [0, 64): bucket span per ranked entry (dev aid)
+// [64 + 2k]: sum, [65 + 2k]: max over CTAs of phase k's clock cycles (thread 0)
+#define PHASE_T0 long long _t0 = clock64()
+#define PHASE(k)                                                              \
+    if (threadIdx.x == 0) {                                                   \
+        const long long _t = clock64();                                       \
+        atomicAdd(&g_rstats[64 + 2 * (k)], (unsigned long long)(_t - _t0));   \
+        atomicMax(&g_rstats[65 + 2 * (k)], (unsigned long long)(_t - _t0));   \
+        _t0 = _t;                                                             \
+    }
+#else
+#define PHASE_T0
+#define PHASE(k)
+#endif
 
-// RUNS = false (tiles without runs, already bounded by the sum-of-squares
-// estimate): the plain unrolled compare loop.
+// Tiles with runs skip the sum-of-squares estimate (run weights inflate it):
+// their scans are bounded by a per-thread budget of scanned slots instead; a
+// thread past it sets rl->abort and the tile goes to the radix sort.
+constexpr int kScanBudget = 32768;
+
 template <bool RUNS>
-__device__ void rank_buckets(const uint32_t* ent, const uint32_t* starts, int N, uint16_t* om, int* abort_flag,
-                             int* nbig, uint4* big) {
+__device__ void rank_buckets(const uint32_t* ent, const uint16_t* d16, const uint32_t* starts, int N, uint16_t* om,
+                             RunList* rl) {
     const int nsw = (N + 31) >> 5;
+    const int nlong = RUNS ? min(rl->nmark, kBigRuns) : 0;
     int work = 0;
     for (int sp = threadIdx.x; sp < N; sp += blockDim.x) {
         const uint32_t e = ent[sp];
@@ -640,49 +746,63 @@ __device__ void rank_buckets(const uint32_t* ent, const uint32_t* starts, int N,
         while (!m && ++w < nsw) m = starts[w];
         const int b1 = m ? (w << 5) + __ffs(m) - 1 : N;
         int rk = b0;
+#ifdef IMF_RSTATS
+        atomicAdd(&g_rstats[min(b1 - b0, 63)], 1ull);
+#endif
         if (!RUNS) {
             for (int q = b0; q < b1; q++) rk += ent[q] < e ? 1 : 0;
             om[rk] = (uint16_t)lo;
             continue;
         }
-        int q = b0, it = 0;
-        for (; q < b1 && it < kScanMax; it++) {
-            if (q + 4 <= b1) {  // four plain entries at once (no run head among them)
-                const uint32_t v0 = ent[q], v1 = ent[q + 1], v2 = ent[q + 2], v3 = ent[q + 3];
-                const bool h = (v0 & 0xffffu) == 0xffffu || (v1 & 0xffffu) == 0xffffu ||
-                               (v2 & 0xffffu) == 0xffffu || (v3 & 0xffffu) == 0xffffu;
-                if (!h) {
-                    rk += (v0 < e ? 1 : 0) + (v1 < e ? 1 : 0) + (v2 < e ? 1 : 0) + (v3 < e ? 1 : 0);
-                    q += 4;
-                    continue;
+        const uint32_t e1 = e | 1u;
+        auto scan = [&](int q0, int q1) {
+            work += q1 - q0;
+            if (work > kScanBudget) {
+                rl->abort = 1;
+                return;
+            }
+            for (int q = q0; q < q1; q++) {
+                const uint32_t v1 = ent[q] | 1u;
+                rk += (v1 < e1 || (v1 == e1 && q < sp)) ? 1 : 0;
+            }
+        };
+        // long runs inside [b0, b1), in slot order: counted whole, not scanned
+        int qa = b0;
+        for (;;) {
+            int kn = -1;
+            uint32_t sn = 0xffffffffu;
+            for (int k = 0; k < nlong; k++) {
+                const uint32_t sk = rl->mark[k].x;
+                if (sk >= (uint32_t)qa && sk < (uint32_t)b1 && sk < sn) {
+                    sn = sk;
+                    kn = k;
                 }
             }
-            const uint32_t v = ent[q];
-            if ((v & 0xffffu) == 0xffffu) {  // run head: the run orders as a whole
-                const uint32_t d = ent[q + 2] >> 16;
-                const int len = (int)(d & 0xffu) * (int)(d >> 8);
-                rk += (v < e || (v == e && q < sp)) ? len : 0;
-                q += len;
-            } else {
-                rk += v < e ? 1 : 0;
-                q++;
-            }
+            if (kn < 0) break;
+            scan(qa, (int)sn);
+            const uint32_t v1 = rl->mark[kn].y | 1u;  // the run's value (| 1: as its head)
+            if (v1 < e1 || (v1 == e1 && (int)sn < sp)) rk += (int)rl->mlen[kn].x;
+            qa = (int)sn + (int)rl->mlen[kn].x;
         }
-        work += it;
-        if (q < b1 || work > kScanBudget) {
-            *abort_flag = 1;
-            break;
-        }
+        scan(qa, b1);
+        if (work > kScanBudget) break;
         if (lo != 0xffffu) {
             om[rk] = (uint16_t)lo;
             continue;
         }
-        const uint32_t pos = ent[sp + 1] >> 16, d = ent[sp + 2] >> 16;
-        const int cx = (int)(d & 0xffu), cy = (int)(d >> 8), len = cx * cy;
-        if (len > 256) {
-            const int k = atomicAdd(nbig, 1);
+        uint32_t d = 0;  // this head's descriptor: pos | cx << 16 | cy << 24
+        if (d16) {
+            d = (uint32_t)d16[sp] | ((uint32_t)d16[sp + 1] << 16);
+        } else {
+            for (int k = 0; k < min(rl->n, kRunList); k++)
+                if (rl->run[k].x == (uint32_t)sp) d = rl->run[k].y;
+        }
+        const int cx = (int)((d >> 16) & 0xffu), len = cx * (int)(d >> 24);
+        const uint32_t pos = d & 0xffffu;
+        if (len > 256) {  // the CTA fills it (fill_big_runs)
+            const int k = atomicAdd(&rl->nbig, 1);
             if (k < kBigRuns) {
-                big[k] = make_uint4((uint32_t)rk, pos, (uint32_t)cx, (uint32_t)cy);
+                rl->big[k] = make_uint4((uint32_t)rk, pos, (uint32_t)cx, (uint32_t)(d >> 24));
                 continue;
             }
         }
@@ -694,13 +814,14 @@ __device__ void rank_buckets(const uint32_t* ent, const uint32_t* starts, int N,
 }
 
 // After the barrier closing rank_buckets: fill the long runs with the CTA.
-__device__ void fill_big_runs(uint16_t* om, int nbig, const uint4* big) {
-    for (int k = 0; k < min(nbig, kBigRuns); k++) {
-        const uint4 b = big[k];
-        const int cx = (int)b.z, len = cx * (int)b.w;
+__device__ void fill_big_runs(uint16_t* om, const RunList* rl) {
+    for (int k = 0; k < min(rl->nbig, kBigRuns); k++) {
+        const uint4 b = rl->big[k];
+        const int rk = (int)b.x, cx = (int)b.z, len = cx * (int)b.w;
+        const uint32_t pos = b.y;
         for (int i = threadIdx.x; i < len; i += blockDim.x) {
             const int yy = i / cx, xx = i - yy * cx;
-            om[b.x + i] = (uint16_t)(b.y + (uint32_t)(xx | (yy << 8)));
+            om[rk + i] = (uint16_t)(pos + (uint32_t)(xx | (yy << 8)));
         }
     }
 }
@@ -720,11 +841,16 @@ __device__ __forceinline__ void f32_bucket_tile(const Geom& g, const TileCoord& 
     const int S = g.Sw, SH = g.Sh, N = g.N;
     uint32_t* hw = reinterpret_cast<uint32_t*>(smem);
     uint32_t* ent = GENT ? gent + blockIdx.x * gent_stride : hw + NW;  // N entries
-    uint32_t* starts = GENT ? hw + NW : ent + ((N + 3) & ~3);        // bucket starts, ceil(N/32) words
+    // bucket starts, ceil(N/32) words; the coarse table (f32) aliases the
+    // shared entries (dead until the scatter) or follows the starts
+    uint32_t* starts = GENT ? hw + NW : ent + max((N + 3) & ~3, kCoarse);
     const int nsw = (N + 31) >> 5;
+    uint32_t* ctab = GENT ? starts + ((nsw + 3) & ~3) : ent;
+    uint16_t* d16 = GENT ? reinterpret_cast<uint16_t*>(ent + N) : nullptr;  // run descriptors (2 B / slot)
+    const bool adaptive = g.dtype == DT_F32 && N > kAdaptiveMinN;
     __shared__ unsigned long long s_sumsq;
-    __shared__ int s_runs, s_abort, s_nbig;
-    __shared__ uint4 s_big[kBigRuns];
+    __shared__ int s_runs;
+    __shared__ RunList s_rl;
     uint32_t v[NK][NK];
     unsigned long long okm = 0;  // which of this thread's pixels are ranked (weight > 0)
     // replicate copies (rep_axis), edge tiles only, recomputed where used
@@ -736,7 +862,7 @@ __device__ __forceinline__ void f32_bucket_tile(const Geom& g, const TileCoord& 
         bool fx, fy;
         rep_axis(X0, lane + 32 * k, S, g.W, cx, fx);
         rep_axis(Y0, wid + 32 * j, SH, g.H, cy, fy);
-        return pixel_weight(cx, fx, cy, fy);
+        return pixel_weight(cx, fx, cy, fy, g.run_min);
     };
     auto cnt_x = [&](int k) {
         int c;
@@ -774,12 +900,27 @@ __device__ __forceinline__ void f32_bucket_tile(const Geom& g, const TileCoord& 
         uint4* h4 = reinterpret_cast<uint4*>(hw);
         for (int i = tid; i < NW / 4; i += blockDim.x) h4[i] = make_uint4(0, 0, 0, 0);
         for (int i = tid; i < nsw; i += blockDim.x) starts[i] = 0;
+        if (adaptive)
+            for (int i = tid; i < kCoarse; i += blockDim.x) ctab[i] = 0;
         if (tid == 0) {
             s_sumsq = 0;
-            s_runs = s_abort = s_nbig = 0;
+            s_runs = s_rl.n = s_rl.nbig = s_rl.nmark = s_rl.abort = 0;
         }
     }
     __syncthreads();
+    if (adaptive) {  // keys -> fine bucket << 16 | low 16 key bits
+#pragma unroll
+        for (int j = 0; j < NK; j++)
+#pragma unroll
+            for (int k = 0; k < NK; k++)
+                if ((okm >> (j * NK + k)) & 1ull) atomicAdd(&ctab[v[j][k] >> 20], (uint32_t)weight(j, k));
+        coarse_alloc(ctab, N);
+#pragma unroll
+        for (int j = 0; j < NK; j++)
+#pragma unroll
+            for (int k = 0; k < NK; k++)
+                if ((okm >> (j * NK + k)) & 1ull) v[j][k] = (fine_bucket(ctab, v[j][k]) << 16) | (v[j][k] & 0xffffu);
+    }
     bool runs = false;
 #pragma unroll
     for (int j = 0; j < NK; j++)
@@ -796,7 +937,7 @@ __device__ __forceinline__ void f32_bucket_tile(const Geom& g, const TileCoord& 
     hist16_exclusive_scan(hw, NW, starts, &s_sumsq);
     __syncthreads();
     // tiles with runs skip the estimate (run weights inflate it); their scans
-    // are bounded instead (rank_buckets)
+    // are budgeted instead (rank_buckets)
     if (!s_runs && s_sumsq > max_sumsq) {  // block-uniform: hand the tile to the radix sort
         if (tid == 0) fallback[1 + atomicAdd(fallback, 1)] = blockIdx.x;
         return;
@@ -809,21 +950,26 @@ __device__ __forceinline__ void f32_bucket_tile(const Geom& g, const TileCoord& 
                 const uint32_t key = v[j][k], h = key >> 16, sh = (h & 1) << 4;
                 const int wt = weight(j, k);
                 const uint32_t old = atomicAdd(&hw[h >> 1], (uint32_t)wt << sh);
-                put_entry(ent, (old >> sh) & 0xffffu, key & 0xffffu, lane + 32 * k, wid + 32 * j, wt, cnt_x(k),
-                          cnt_y(j));
+                put_entry(ent, d16, (old >> sh) & 0xffffu, key & 0xffffu, lane + 32 * k, wid + 32 * j, wt,
+                          cnt_x(k), cnt_y(j), &s_rl);
             }
     __syncthreads();
+    if (EDGE) mark_runs(ent, &s_rl);
     uint16_t* om = reinterpret_cast<uint16_t*>(hw);  // the histogram is dead: omega goes here
-    if (s_runs)
-        rank_buckets<true>(ent, starts, N, om, &s_abort, &s_nbig, s_big);
-    else
-        rank_buckets<false>(ent, starts, N, om, &s_abort, &s_nbig, s_big);
-    __syncthreads();
-    if (s_abort) {
+    if (s_rl.abort) {  // run list overflow (block-uniform after the scatter barrier)
         if (tid == 0) fallback[1 + atomicAdd(fallback, 1)] = blockIdx.x;
         return;
     }
-    fill_big_runs(om, s_nbig, s_big);
+    if (s_runs)
+        rank_buckets<true>(ent, d16, starts, N, om, &s_rl);
+    else
+        rank_buckets<false>(ent, d16, starts, N, om, &s_rl);
+    __syncthreads();
+    if (s_rl.abort) {  // a scan over budget (block-uniform after the barrier)
+        if (tid == 0) fallback[1 + atomicAdd(fallback, 1)] = blockIdx.x;
+        return;
+    }
+    fill_big_runs(om, &s_rl);
     for (int i = N + tid; i < g.Npad; i += blockDim.x) om[i] = 0xffffu;
     __syncthreads();
     store_omega(g, om, omega_slot(g, omega_out));
@@ -853,14 +999,18 @@ __global__ void __launch_bounds__(1024) k1_f32_bucket_g(Geom g, uint16_t* __rest
     constexpr int NW = 32768;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
     const TileCoord tc = tile_coord(g, g.tile_begin + blockIdx.x);
+    PHASE_T0;
     const int S = g.Sw, SH = g.Sh, N = g.N;
     uint32_t* hw = reinterpret_cast<uint32_t*>(smem);
     uint32_t* starts = hw + NW;
     const int nsw = (N + 31) >> 5;
+    uint32_t* ctab = starts + ((nsw + 3) & ~3);  // coarse bins / fine-bucket table (f32)
+    const bool adaptive = g.dtype == DT_F32 && N > kAdaptiveMinN;
     uint32_t* ent = gent + blockIdx.x * gent_stride;
+    uint16_t* d16 = reinterpret_cast<uint16_t*>(ent + N);  // run descriptors (2 B / slot)
     __shared__ unsigned long long s_sumsq;
-    __shared__ int s_runs, s_abort, s_nbig;
-    __shared__ uint4 s_big[kBigRuns];
+    __shared__ int s_runs;
+    __shared__ RunList s_rl;
     const int X0 = tc.ox0 - g.r + g.vshift, Y0 = tc.oy0 - g.r + g.vshift;
     const bool edge = has_runs(g, tc);
     {
@@ -869,86 +1019,104 @@ __global__ void __launch_bounds__(1024) k1_f32_bucket_g(Geom g, uint16_t* __rest
         for (int i = tid; i < nsw; i += blockDim.x) starts[i] = 0;
         if (tid == 0) {
             s_sumsq = 0;
-            s_runs = s_abort = s_nbig = 0;
+            s_runs = s_rl.n = s_rl.nbig = s_rl.nmark = s_rl.abort = 0;
         }
     }
     __syncthreads();
     const int nk = (S + 31) >> 5;
-    bool runs = false;
-    for (int y = wid; y < SH; y += nw) {
-        int yy = Y0 + y;
-        yy = yy < 0 ? 0 : (yy >= g.H ? g.H - 1 : yy);
-        int cy = 1;
-        bool fy = true;
-        if (edge) rep_axis(Y0, y, SH, g.H, cy, fy);
-        for (int k = 0; k < nk; k++) {
-            const int x = lane + 32 * k;
-            if (x < S) {
-                int xx = X0 + x;
-                xx = xx < 0 ? 0 : (xx >= g.W ? g.W - 1 : xx);
-                int cx = 1;
-                bool fx = true;
-                if (edge) rep_axis(X0, x, S, g.W, cx, fx);
-                const int wt = pixel_weight(cx, fx, cy, fy);
-                if (wt) {
-                    runs |= wt > 1;
-                    const uint32_t h = f32_key(g, tc, yy, xx) >> 16;
-                    const uint32_t sh = (h & 1) << 4;
-                    atomicAdd(&hw[h >> 1], (uint32_t)wt << sh);
+    PHASE(0);
+
+    // visit every ranked pixel: fn(x, y, key, weight, cx, cy); a row's keys
+    // (<= 8 per lane, S <= 255) are loaded before any is used
+    auto each_pixel = [&](auto fn) {
+        for (int y = wid; y < SH; y += nw) {
+            int yy = Y0 + y;
+            yy = yy < 0 ? 0 : (yy >= g.H ? g.H - 1 : yy);
+            int cy = 1;
+            bool fy = true;
+            if (edge) rep_axis(Y0, y, SH, g.H, cy, fy);
+            uint32_t kv[8];
+#pragma unroll
+            for (int k = 0; k < 8; k++) {
+                if (k < nk) {
+                    int xx = X0 + min(lane + 32 * k, S - 1);
+                    xx = xx < 0 ? 0 : (xx >= g.W ? g.W - 1 : xx);
+                    kv[k] = f32_key(g, tc, yy, xx);
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < 8; k++) {
+                const int x = lane + 32 * k;
+                if (k < nk && x < S) {
+                    int cx = 1;
+                    bool fx = true;
+                    if (edge) rep_axis(X0, x, S, g.W, cx, fx);
+                    const int wt = pixel_weight(cx, fx, cy, fy, g.run_min);
+                    if (wt) fn(x, y, kv[k], wt, cx, cy);
                 }
             }
         }
+    };
+    // f32: fine bucket << 16 | low 16 key bits (coarse_alloc); u16: the key
+    auto bucket_key = [&](uint32_t key) {
+        return adaptive ? (fine_bucket(ctab, key) << 16) | (key & 0xffffu) : key;
+    };
+    if (adaptive) {
+        for (int i = tid; i < kCoarse; i += blockDim.x) ctab[i] = 0;
+        __syncthreads();
+        each_pixel([&](int, int, uint32_t key, int wt, int, int) { atomicAdd(&ctab[key >> 20], (uint32_t)wt); });
+        coarse_alloc(ctab, N);
+    PHASE(1);
     }
+    bool runs = false;
+    each_pixel([&](int, int, uint32_t key, int wt, int, int) {
+        runs |= wt > 1;
+        const uint32_t h = bucket_key(key) >> 16, sh = (h & 1) << 4;
+        atomicAdd(&hw[h >> 1], (uint32_t)wt << sh);
+    });
     if (runs) s_runs = 1;
     __syncthreads();
     hist16_exclusive_scan(hw, NW, starts, &s_sumsq);
     __syncthreads();
+    PHASE(2);
     if (!s_runs && s_sumsq > max_sumsq) {
         if (tid == 0) fallback[1 + atomicAdd(fallback, 1)] = blockIdx.x;
         return;
     }
-    for (int y = wid; y < SH; y += nw) {
-        int yy = Y0 + y;
-        yy = yy < 0 ? 0 : (yy >= g.H ? g.H - 1 : yy);
-        int cy = 1;
-        bool fy = true;
-        if (edge) rep_axis(Y0, y, SH, g.H, cy, fy);
-        for (int k = 0; k < nk; k++) {
-            const int x = lane + 32 * k;
-            if (x < S) {
-                int xx = X0 + x;
-                xx = xx < 0 ? 0 : (xx >= g.W ? g.W - 1 : xx);
-                int cx = 1;
-                bool fx = true;
-                if (edge) rep_axis(X0, x, S, g.W, cx, fx);
-                const int wt = pixel_weight(cx, fx, cy, fy);
-                if (wt) {
-                    const uint32_t key = f32_key(g, tc, yy, xx);
-                    const uint32_t h = key >> 16, sh = (h & 1) << 4;
-                    const uint32_t old = atomicAdd(&hw[h >> 1], (uint32_t)wt << sh);
-                    put_entry(ent, (old >> sh) & 0xffffu, key & 0xffffu, x, y, wt, cx, cy);
-                }
-            }
-        }
-    }
+    each_pixel([&](int x, int y, uint32_t key, int wt, int cx, int cy) {
+        const uint32_t bk = bucket_key(key), h = bk >> 16, sh = (h & 1) << 4;
+        const uint32_t old = atomicAdd(&hw[h >> 1], (uint32_t)wt << sh);
+        put_entry(ent, d16, (old >> sh) & 0xffffu, bk & 0xffffu, x, y, wt, cx, cy, &s_rl);
+    });
     __syncthreads();  // block-scope ordering of the entry stores (global, same CTA)
+    mark_runs(ent, &s_rl);
+    PHASE(3);
     uint16_t* om = reinterpret_cast<uint16_t*>(hw);
-    if (s_runs)
-        rank_buckets<true>(ent, starts, N, om, &s_abort, &s_nbig, s_big);
-    else
-        rank_buckets<false>(ent, starts, N, om, &s_abort, &s_nbig, s_big);
-    __syncthreads();
-    if (s_abort) {
+    if (s_rl.abort) {  // run list overflow (block-uniform after the scatter barrier)
         if (tid == 0) fallback[1 + atomicAdd(fallback, 1)] = blockIdx.x;
         return;
     }
-    fill_big_runs(om, s_nbig, s_big);
+    if (s_runs)
+        rank_buckets<true>(ent, d16, starts, N, om, &s_rl);
+    else
+        rank_buckets<false>(ent, d16, starts, N, om, &s_rl);
+    __syncthreads();
+    PHASE(4);
+    if (s_rl.abort) {  // a scan over budget (block-uniform after the barrier)
+        if (tid == 0) fallback[1 + atomicAdd(fallback, 1)] = blockIdx.x;
+        return;
+    }
+    fill_big_runs(om, &s_rl);
     for (int i = N + tid; i < g.Npad; i += blockDim.x) om[i] = 0xffffu;
     __syncthreads();
     store_omega(g, om, omega_slot(g, omega_out));
+    PHASE(5);
+
 }
 
-size_t k1_f32_bucket_g_smem_bytes(int N) { return 32768 * 4 + 4 * (size_t)((N + 31) >> 5) + 16; }
+size_t k1_f32_bucket_g_smem_bytes(int N) {
+    return 32768 * 4 + 4 * (size_t)(((N + 31) >> 5) + 3 & ~3) + 4 * (size_t)kCoarse + 16;
+}
 
 #define IMF_K1F(NK)                                                                                  \
     template __global__ void k1_f32_bucket<NK, false>(Geom, uint16_t*, int*, uint32_t*, long long,  \
@@ -964,7 +1132,7 @@ IMF_K1F(6)
 #undef IMF_K1F
 
 size_t k1_f32_bucket_smem_bytes(int N) {
-    return 32768 * 4 + 4 * (size_t)((N + 3) & ~3) + 4 * (size_t)((N + 31) >> 5) + 16;
+    return 32768 * 4 + 4 * (size_t)std::max((N + 3) & ~3, kCoarse) + 4 * (size_t)((N + 31) >> 5) + 16;
 }
 
 template __global__ void k1_count<DT_U8>(Geom, uint16_t*);
@@ -995,3 +1163,14 @@ size_t k1_gscratch_bytes(int dtype, int Npad) {
 }
 
 }  // namespace imf
+
+#ifdef IMF_STATS
+extern "C" int imf_rstats(unsigned long long* out, int reset) {
+    if (cudaMemcpyFromSymbol(out, imf::g_rstats, sizeof(imf::g_rstats))) return 2;
+    if (reset) {
+        static const unsigned long long z[128] = {};
+        cudaMemcpyToSymbol(imf::g_rstats, z, sizeof(z));
+    }
+    return 0;
+}
+#endif
