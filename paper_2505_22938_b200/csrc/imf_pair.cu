@@ -164,6 +164,7 @@ struct PairCtx {
     const int* span;      // shared span table (2r+1)
     int N, r, R2p1;
     uint32_t rowk_a;      // SH_POLY: shared address of the 256-entry per-(dy+128) range table
+    int nR2p1;            // -(r(r+1)+1)
 };
 
 __device__ __forceinline__ uint32_t lds32c(uint32_t a) {
@@ -186,8 +187,8 @@ __device__ __forceinline__ uint32_t test8(const PairCtx& c, int v0, uint32_t Kc,
 #pragma unroll
         for (int i = 3; i >= 0; i--) {
             const int b = (int)((w[i] + Kc) ^ 0x80808080u);
-            const int slo = __dp4a(b, b & 0xffff, -c.R2p1);
-            const int shi = __dp4a(b, (int)((uint32_t)b & 0xffff0000u), -c.R2p1);
+            const int slo = __dp4a(b, b & 0xffff, c.nR2p1);
+            const int shi = __dp4a(b, (int)((uint32_t)b & 0xffff0000u), c.nR2p1);
             m = __funnelshift_l((uint32_t)shi, m, 1);
             m = __funnelshift_l((uint32_t)slo, m, 1);
         }
@@ -235,36 +236,6 @@ __device__ __forceinline__ uint32_t test8(const PairCtx& c, int v0, uint32_t Kc,
     return m;
 }
 
-// t-th smallest rank of the window at (cx, cy) from the exact state (P, cnt):
-// walk omega from P toward the target 8 ranks per step (core.py:87-146 with an
-// exact pivot).  -1 if the walk leaves [0, N) (core.py:31-36).
-template <int SHAPE, bool OMG>
-__device__ int refine8(const PairCtx& c, int cx, int cy, int P, int cnt, int t) {
-    const bool up = cnt <= t;
-    int need = up ? t - cnt : cnt - t - 1;
-    int v0;
-    uint32_t mask;
-    if (up) {
-        v0 = P & ~7;
-        mask = (0xffu << (P - v0)) & 0xffu;
-    } else {
-        if (P <= 0) return -1;
-        v0 = (P - 1) & ~7;
-        mask = (1u << (P - v0)) - 1u;
-    }
-    const int step = up ? 8 : -8;
-    const uint32_t Kc = (uint32_t)((128 - cx) + ((128 - cy) << 8)) * 0x10001u;
-    for (;;) {
-        if (v0 < 0 || v0 >= c.N) return -1;
-        uint32_t m = test8<SHAPE, OMG>(c, v0, Kc, cx, cy) & mask;
-        if (v0 + 8 > c.N) m &= (1u << (c.N - v0)) - 1u;
-        const int pc = __popc(m);
-        if (need < pc) return v0 + nth_bit8(m, up ? need : pc - 1 - need);
-        need -= pc;
-        v0 += step;
-        mask = 0xffu;
-    }
-}
 
 // Both windows of a pair (columns cx and cx+1, same row) walk in the same
 // loop, one 8-rank step of EACH per iteration (independent work, so the two
@@ -275,48 +246,68 @@ __device__ int refine8(const PairCtx& c, int cx, int cy, int P, int cnt, int t) 
 // the span test both place outside every window, so the last block needs no
 // mask; a walk leaving [0, N) (inconsistent state, core.py:31-36) yields -1.
 struct Walk {
-    int v0, need, step, base, k;
-    uint32_t mask, Kc, msk;
+    int v0, need, step;
+    uint32_t Kc, msk;
     bool up, done;
 };
 
-__device__ __forceinline__ void walk_init(Walk& w, int P, int cnt, int t, int cx, int cy) {
+// Returns the first block's mask (ranks on the walk's side of P).
+__device__ __forceinline__ uint32_t walk_init(Walk& w, int P, int cnt, int t, int cx, int cy) {
     w.up = cnt <= t;
     w.need = w.up ? t - cnt : cnt - t - 1;
+    uint32_t mask;
     if (w.up) {
         w.v0 = P & ~7;
-        w.mask = (0xffu << (P - w.v0)) & 0xffu;
+        mask = (0xffu << (P - w.v0)) & 0xffu;
     } else {
         w.v0 = (P - 1) & ~7;  // P == 0: v0 = -8, reported as a defect
-        w.mask = (P > 0) ? (1u << (P - w.v0)) - 1u : 0xffu;
+        mask = (P > 0) ? (1u << (P - w.v0)) - 1u : 0xffu;
     }
     w.step = w.up ? 8 : -8;
     w.Kc = (uint32_t)((128 - cx) + ((128 - cy) << 8)) * 0x10001u;
     w.done = false;
-    w.base = -1;
-    w.k = 0;
     w.msk = 0;
+    return mask;
 }
 
+// One 8-rank step.  A finished walk keeps v0 at its answer's block (msk: that
+// block's membership bits, need: in-window ranks to skip in it); a walk that
+// leaves [0, N) stops with v0 outside it (a defect).
 template <int SHAPE, bool OMG>
-__device__ __forceinline__ void walk_step(const PairCtx& c, Walk& w, int cx, int cy) {
+__device__ __forceinline__ void walk_step(const PairCtx& c, Walk& w, uint32_t mask, int cx, int cy) {
     if (w.done) return;
-    if ((unsigned)w.v0 >= (unsigned)c.N) {  // left [0, N): defect
+    if ((unsigned)w.v0 >= (unsigned)c.N) {
         w.done = true;
         return;
     }
-    const uint32_t m = test8<SHAPE, OMG>(c, w.v0, w.Kc, cx, cy) & w.mask;
+    const uint32_t m = test8<SHAPE, OMG>(c, w.v0, w.Kc, cx, cy) & mask;
     const int pc = __popc(m);
     if (w.need < pc) {
         w.done = true;
-        w.base = w.v0;
         w.msk = m;
-        w.k = w.up ? w.need : pc - 1 - w.need;
     } else {
         w.need -= pc;
         w.v0 += w.step;
-        w.mask = 0xffu;
     }
+}
+
+__device__ __forceinline__ int walk_result(const PairCtx& c, const Walk& w) {
+    if ((unsigned)w.v0 >= (unsigned)c.N) return -1;
+    return w.v0 + nth_bit8(w.msk, w.up ? w.need : __popc(w.msk) - 1 - w.need);
+}
+
+// t-th smallest rank of the window at (cx, cy) from the exact state (P, cnt):
+// walk omega from P toward the target 8 ranks per step (core.py:87-146 with an
+// exact pivot).  -1 if the walk leaves [0, N) (core.py:31-36).
+template <int SHAPE, bool OMG>
+__device__ int refine8(const PairCtx& c, int cx, int cy, int P, int cnt, int t) {
+    Walk w;
+    uint32_t mask = walk_init(w, P, cnt, t, cx, cy);
+    do {
+        walk_step<SHAPE, OMG>(c, w, mask, cx, cy);
+        mask = 0xffu;
+    } while (!w.done);
+    return walk_result(c, w);
 }
 
 #ifdef IMF_STATS
@@ -327,20 +318,23 @@ template <int SHAPE, bool OMG>
 __device__ __forceinline__ void refine8x2(const PairCtx& c, int cx, int cy, int PA, int cntA, int tA, int PB,
                                           int cntB, int tB, int& mA, int& mB) {
     Walk a, b;
-    walk_init(a, PA, cntA, tA, cx, cy);
-    walk_init(b, PB, cntB, tB, cx + 1, cy);
+    const uint32_t ma = walk_init(a, PA, cntA, tA, cx, cy);
+    const uint32_t mb = walk_init(b, PB, cntB, tB, cx + 1, cy);
+    // first blocks (partial masks) peeled; then full blocks
+    walk_step<SHAPE, OMG>(c, a, ma, cx, cy);
+    walk_step<SHAPE, OMG>(c, b, mb, cx + 1, cy);
 #ifdef IMF_STATS
-    int nit = 0;
+    int nit = 1;
 #endif
-    do {
+    while (!(a.done && b.done)) {
 #ifdef IMF_STATS
         nit++;
 #endif
-        walk_step<SHAPE, OMG>(c, a, cx, cy);
-        walk_step<SHAPE, OMG>(c, b, cx + 1, cy);
-    } while (!(a.done && b.done));
-    mA = a.base < 0 ? -1 : a.base + nth_bit8(a.msk, a.k);
-    mB = b.base < 0 ? -1 : b.base + nth_bit8(b.msk, b.k);
+        walk_step<SHAPE, OMG>(c, a, 0xffu, cx, cy);
+        walk_step<SHAPE, OMG>(c, b, 0xffu, cx + 1, cy);
+    }
+    mA = walk_result(c, a);
+    mB = walk_result(c, b);
 #ifdef IMF_STATS
     atomicAdd(&g_stats[min(nit, 63)], 1ull);
     const int mx = __reduce_max_sync(__activemask(), nit);
@@ -530,8 +524,12 @@ __global__ void __launch_bounds__(512) k2_pair(Geom g, PairParams p, const __gri
     __syncthreads();
 
     const uint32_t I_a = (uint32_t)__cvta_generic_to_shared(I);
-    const PairCtx c{OMG ? 0u : (uint32_t)__cvta_generic_to_shared(om_sh), om, span_s, N, r, p.R2p1,
-                    (uint32_t)__cvta_generic_to_shared(rowk)};
+    // omega's shared address and -(r(r+1)+1) held in registers (opaque to the
+    // compiler, which would otherwise rebuild them inside every refine step)
+    uint32_t om_a = OMG ? 0u : (uint32_t)__cvta_generic_to_shared(om_sh);
+    int nR2p1 = -p.R2p1;
+    asm volatile("" : "+r"(om_a), "+r"(nR2p1));
+    const PairCtx c{om_a, om, span_s, N, r, p.R2p1, (uint32_t)__cvta_generic_to_shared(rowk), nR2p1};
     const int R = TY / G;
     const int g0 = G >> 1;
     const int cs = (T >> 1) & ~1;  // seed column (even: a pair base)
