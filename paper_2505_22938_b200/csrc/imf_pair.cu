@@ -291,6 +291,34 @@ __device__ __forceinline__ void walk_step(const PairCtx& c, Walk& w, uint32_t ma
     }
 }
 
+// Two 8-rank blocks per step (v0 and v0 + step): half the trip count of the
+// warp's longest walk for ~1.7x the work of a step (fewer loop / branch
+// overheads per block).  The second block may lie past either end of [0, N):
+// it then reads the sentinel entries (outside every window) next to omega.
+template <int SHAPE, bool OMG>
+__device__ __forceinline__ void walk_step2(const PairCtx& c, Walk& w, uint32_t mask, int cx, int cy) {
+    if (w.done) return;
+    if ((unsigned)w.v0 >= (unsigned)c.N) {
+        w.done = true;
+        return;
+    }
+    const uint32_t m1 = test8<SHAPE, OMG>(c, w.v0, w.Kc, cx, cy) & mask;
+    const uint32_t m2 = test8<SHAPE, OMG>(c, w.v0 + w.step, w.Kc, cx, cy);
+    const int p1 = __popc(m1), p2 = __popc(m2);
+    if (w.need < p1) {
+        w.done = true;
+        w.msk = m1;
+    } else if (w.need < p1 + p2) {
+        w.done = true;
+        w.msk = m2;
+        w.need -= p1;
+        w.v0 += w.step;
+    } else {
+        w.need -= p1 + p2;
+        w.v0 += 2 * w.step;
+    }
+}
+
 __device__ __forceinline__ int walk_result(const PairCtx& c, const Walk& w) {
     if ((unsigned)w.v0 >= (unsigned)c.N) return -1;
     return w.v0 + nth_bit8(w.msk, w.up ? w.need : __popc(w.msk) - 1 - w.need);
@@ -302,11 +330,8 @@ __device__ __forceinline__ int walk_result(const PairCtx& c, const Walk& w) {
 template <int SHAPE, bool OMG>
 __device__ int refine8(const PairCtx& c, int cx, int cy, int P, int cnt, int t) {
     Walk w;
-    uint32_t mask = walk_init(w, P, cnt, t, cx, cy);
-    do {
-        walk_step<SHAPE, OMG>(c, w, mask, cx, cy);
-        mask = 0xffu;
-    } while (!w.done);
+    walk_step<SHAPE, OMG>(c, w, walk_init(w, P, cnt, t, cx, cy), cx, cy);
+    while (!w.done) walk_step2<SHAPE, OMG>(c, w, 0xffu, cx, cy);
     return walk_result(c, w);
 }
 
@@ -330,8 +355,8 @@ __device__ __forceinline__ void refine8x2(const PairCtx& c, int cx, int cy, int 
 #ifdef IMF_STATS
         nit++;
 #endif
-        walk_step<SHAPE, OMG>(c, a, 0xffu, cx, cy);
-        walk_step<SHAPE, OMG>(c, b, 0xffu, cx + 1, cy);
+        walk_step2<SHAPE, OMG>(c, a, 0xffu, cx, cy);
+        walk_step2<SHAPE, OMG>(c, b, 0xffu, cx + 1, cy);
     }
     mA = walk_result(c, a);
     mB = walk_result(c, b);
