@@ -278,6 +278,7 @@ __device__ __forceinline__ void hist16_exclusive_scan(uint32_t* hw, const int NW
         }
         __syncthreads();
         uint32_t carry = wt[wid];  // plain (unpacked) count before this chunk row
+        unsigned long long sqacc = 0;  // this lane's sum of squared counters (sumsq)
         for (int i0 = 0; i0 < nch; i0 += 32) {
             uint4 q = wb[i0 + lane];
             const uint32_t p1 = q.x, p2 = p1 + q.y, p3 = p2 + q.z, tot = p3 + q.w;  // packed prefixes
@@ -292,20 +293,17 @@ __device__ __forceinline__ void hist16_exclusive_scan(uint32_t* hw, const int NW
             // counters before word k: base + flat(packed prefix of words < k)
             const uint32_t b0 = base, b1 = base + (p1 & 0xffffu) + (p1 >> 16);
             const uint32_t b2 = base + (p2 & 0xffffu) + (p2 >> 16), b3 = base + (p3 & 0xffffu) + (p3 >> 16);
-            if (starts) {  // bit at every non-empty counter's first position (bucket starts)
+            if (starts || sumsq) {
                 const uint32_t cw[4] = {q.x, q.y, q.z, q.w}, bw[4] = {b0, b1, b2, b3};
-                unsigned long long sq = 0;
 #pragma unroll
                 for (int k = 0; k < 4; k++) {
                     const uint32_t lo = cw[k] & 0xffffu, hi = cw[k] >> 16, e0 = bw[k], e1 = bw[k] + lo;
-                    if (lo) atomicOr(&starts[e0 >> 5], 1u << (e0 & 31));
-                    if (hi) atomicOr(&starts[e1 >> 5], 1u << (e1 & 31));
-                    sq += (unsigned long long)(lo * lo) + (unsigned long long)(hi * hi);
+                    if (starts) {  // bit at every non-empty counter's first position (bucket starts)
+                        if (lo) atomicOr(&starts[e0 >> 5], 1u << (e0 & 31));
+                        if (hi) atomicOr(&starts[e1 >> 5], 1u << (e1 & 31));
+                    }
+                    sqacc += (unsigned long long)(lo * lo) + (unsigned long long)(hi * hi);
                 }
-                // clamp per lane at 2^26 (> kMaxSumSq: the tile falls back anyway) so
-                // the 32-bit warp sum cannot wrap
-                const unsigned wsq = __reduce_add_sync(0xffffffffu, (unsigned)min(sq, 1ull << 26));
-                if (lane == 0 && wsq) atomicAdd(sumsq, (unsigned long long)wsq);
             }
             q.x = b0 | ((b0 + (q.x & 0xffffu)) << 16);
             q.y = b1 | ((b1 + (q.y & 0xffffu)) << 16);
@@ -314,6 +312,12 @@ __device__ __forceinline__ void hist16_exclusive_scan(uint32_t* hw, const int NW
             wb[i0 + lane] = q;
             const uint32_t last = __shfl_sync(0xffffffffu, incl, 31);
             carry += (last & 0xffffu) + (last >> 16);
+        }
+        if (sumsq) {
+            // clamp per lane at 2^26 (> kMaxSumSq: the tile falls back anyway) so
+            // the 32-bit warp sum cannot wrap
+            const unsigned wsq = __reduce_add_sync(0xffffffffu, (unsigned)min(sqacc, 1ull << 26));
+            if (lane == 0 && wsq) atomicAdd(sumsq, (unsigned long long)wsq);
         }
         return;
     }
@@ -848,6 +852,10 @@ __device__ __forceinline__ void f32_bucket_tile(const Geom& g, const TileCoord& 
     uint32_t* ctab = GENT ? starts + ((nsw + 3) & ~3) : ent;
     uint16_t* d16 = GENT ? reinterpret_cast<uint16_t*>(ent + N) : nullptr;  // run descriptors (2 B / slot)
     const bool adaptive = g.dtype == DT_F32 && N > kAdaptiveMinN;
+    // interior tiles with adaptive (~2-key) buckets rank their own register
+    // pixels (lanes in different buckets: fine while buckets are that small;
+    // NK = 6 would spill); others rank slot-parallel over a start bitmap
+    const bool own_rank = !EDGE && NK <= 5 && adaptive;
     __shared__ unsigned long long s_sumsq;
     __shared__ int s_runs;
     __shared__ RunList s_rl;
@@ -899,7 +907,8 @@ __device__ __forceinline__ void f32_bucket_tile(const Geom& g, const TileCoord& 
     {
         uint4* h4 = reinterpret_cast<uint4*>(hw);
         for (int i = tid; i < NW / 4; i += blockDim.x) h4[i] = make_uint4(0, 0, 0, 0);
-        for (int i = tid; i < nsw; i += blockDim.x) starts[i] = 0;
+        if (!own_rank)
+            for (int i = tid; i < nsw; i += blockDim.x) starts[i] = 0;
         if (adaptive)
             for (int i = tid; i < kCoarse; i += blockDim.x) ctab[i] = 0;
         if (tid == 0) {
@@ -934,7 +943,7 @@ __device__ __forceinline__ void f32_bucket_tile(const Geom& g, const TileCoord& 
             }
     if (runs) s_runs = 1;
     __syncthreads();
-    hist16_exclusive_scan(hw, NW, starts, &s_sumsq);
+    hist16_exclusive_scan(hw, NW, own_rank ? nullptr : starts, &s_sumsq);
     __syncthreads();
     // tiles with runs skip the estimate (run weights inflate it); their scans
     // are budgeted instead (rank_buckets)
@@ -954,8 +963,35 @@ __device__ __forceinline__ void f32_bucket_tile(const Geom& g, const TileCoord& 
                           cnt_x(k), cnt_y(j), &s_rl);
             }
     __syncthreads();
-    if (EDGE) mark_runs(ent, &s_rl);
     uint16_t* om = reinterpret_cast<uint16_t*>(hw);  // the histogram is dead: omega goes here
+    if (own_rank) {
+        // each thread ranks its own pixels: the counters now hold every bucket's
+        // end, so bucket id spans [end(id - 1), end(id)) -- no start bitmap
+#pragma unroll
+        for (int j = 0; j < NK; j++)
+#pragma unroll
+            for (int k = 0; k < NK; k++)
+                if ((okm >> (j * NK + k)) & 1ull) {
+                    const uint32_t id = v[j][k] >> 16;
+                    const uint32_t e = (v[j][k] << 16) | (uint32_t)((lane + 32 * k) | ((wid + 32 * j) << 8));
+                    const int b1 = (int)((hw[id >> 1] >> ((id & 1u) << 4)) & 0xffffu);
+                    const int b0 = id ? (int)((hw[(id - 1) >> 1] >> (((id - 1) & 1u) << 4)) & 0xffffu) : 0;
+                    int rk = b0;
+                    for (int q = b0; q < b1; q++) rk += ent[q] < e ? 1 : 0;
+                    v[j][k] = (uint32_t)rk;
+                }
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < NK; j++)
+#pragma unroll
+            for (int k = 0; k < NK; k++)
+                if ((okm >> (j * NK + k)) & 1ull) om[v[j][k]] = (uint16_t)((lane + 32 * k) | ((wid + 32 * j) << 8));
+        for (int i = N + tid; i < g.Npad; i += blockDim.x) om[i] = 0xffffu;
+        __syncthreads();
+        store_omega(g, om, omega_slot(g, omega_out));
+        return;
+    }
+    mark_runs(ent, &s_rl);
     if (s_rl.abort) {  // run list overflow (block-uniform after the scatter barrier)
         if (tid == 0) fallback[1 + atomicAdd(fallback, 1)] = blockIdx.x;
         return;
