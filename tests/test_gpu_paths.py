@@ -37,6 +37,8 @@ VARIANTS = [
     {"IMF_PAIR_RECT": "1", "IMF_TILE": "64"},
     {"IMF_TILE": "40", "IMF_SEED_ROWS": "4"},
     {"IMF_STRIPE_EDGE": "1", "IMF_STRIPE_MID": "5"},
+    {"IMF_RUNMIN": "2"},    # every replicate-copy group ranked as a run (bucket K1)
+    {"IMF_RUNMIN": "64"},   # edge groups as runs at large r
 ]
 
 CASES = [  # (dtype, shape, kernel spec)
@@ -45,6 +47,8 @@ CASES = [  # (dtype, shape, kernel spec)
     ("uint16", (260, 250), ("circle", 100, 0, 0.0)),      # u16 bucket transform (S = 255)
     ("float32", (180, 200), ("circle", 20, 0, 0.0)),
     ("float32", (260, 240), ("circle", 60, 0, 0.0)),      # f32 global-entries bucket
+    ("float32", (230, 250), ("circle", 40, 0, 0.0)),      # f32 adaptive buckets, own-pixel ranking
+    ("float32", (300, 280), ("circle", 100, 0, 0.0)),     # f32 r=100: corner runs (bucket_g)
     ("uint8", (190, 170, 2), ("regular_polygon", 11, 6, 15.0)),
     ("uint8", (120, 130), ("square", 7, 0, 0.0)),
     ("float32", (70, 90), ("circle", 2, 0, 0.0)),         # direct selection (area <= 32)
