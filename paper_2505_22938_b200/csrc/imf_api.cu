@@ -134,16 +134,21 @@ int make_plan(const imf_image* src, const imf_kernel* k, const imf_options* opt,
     if (!p.direct && env_int("IMF_PAIR", 1) && (packed_shape || env_int("IMF_PAIR_ANY", 0))) {
         // columns: even, <= Tmax, packed circle test needs Tw + r <= 128; rows: the
         // tallest tile keeping N = Sw * Sh <= 32768 (ranks < 2^15), at most Tw
+        // the packed byte tests need T + r <= 128; circles whose T would drop
+        // below the default take a full tile with the wide test (SH_CIRCLEW)
+        const bool wide = k->shape_code == IMF_SHAPE_CIRCLE && 128 - r < std::min(Tmax, 64) &&
+                          env_int("IMF_PAIR_WIDE", 1);
+        const bool packed_fit = packed_shape && !wide;
         int Tw = std::min(Tmax, 255 - 2 * r);
-        if (packed_shape) Tw = std::min(Tw, 128 - r);
+        if (packed_fit) Tw = std::min(Tw, 128 - r);
         Tw &= ~1;
         const int Sw = Tw + 2 * r;
         int Th = std::min(Tw, 65536 / std::max(Sw, 1) - 2 * r);
-        if (packed_shape) Th = std::min(Th, 128 - r);
+        if (packed_fit) Th = std::min(Th, 128 - r);
         // rectangular tiles (Th < Tw) measured slower than the generic path
         // (short sweeps, more seed rows per output row): square tiles only, and
         // no smaller than the default 64 (small tiles sort too much per output)
-        const bool shape_ok = Tw >= std::min(Tmax, 64) &&
+        const bool shape_ok = Tw >= (std::min(Tmax, 64) & ~1) &&
                               Th >= (env_int("IMF_PAIR_RECT", 0) ? std::max(2, Tw / 4) : Tw);
         if (Tw >= 2 && shape_ok) {
             const int Sh = Th + 2 * r;
@@ -392,6 +397,8 @@ cudaError_t set_attrs() {
     if (!e) e = allow_smem(k2_pair<SH_SQUARE, true>, optin);
     if (!e) e = allow_smem(k2_pair<SH_POLY, false>, optin);
     if (!e) e = allow_smem(k2_pair<SH_POLY, true>, optin);
+    if (!e) e = allow_smem(k2_pair<SH_CIRCLEW, false>, optin);
+    if (!e) e = allow_smem(k2_pair<SH_CIRCLEW, true>, optin);
     if (!e) g_attr_done = true;
     return e;
 }
@@ -617,7 +624,7 @@ static int filter_impl(const imf_image* src, imf_image* dsts, int n, const int32
                             kernel->col_ytop, kernel->col_ybot, kernel->ncols, r, p.g.Sw, ptab, pp))
             return IMF_ERR_UNSUPPORTED;
         const bool bytes_ok = p.g.Tw + r <= 128 && p.g.Th + r <= 128;  // |dx|, |dy| <= 127 in a tile
-        pp.shape = !bytes_ok ? SH_SPAN
+        pp.shape = !bytes_ok ? (kernel->shape_code == IMF_SHAPE_CIRCLE ? SH_CIRCLEW : SH_SPAN)
                    : kernel->shape_code == IMF_SHAPE_CIRCLE ? SH_CIRCLE
                    : kernel->shape_code == IMF_SHAPE_SQUARE ? SH_SQUARE : SH_POLY;
         pp.R2p1 = r * (r + 1) + 1;
@@ -688,6 +695,8 @@ static int filter_impl(const imf_image* src, imf_image* dsts, int n, const int32
                 case SH_SQUARE * 2 + 1: IMF_K2P_LAUNCH(SH_SQUARE, true); break;
                 case SH_POLY * 2: IMF_K2P_LAUNCH(SH_POLY, false); break;
                 case SH_POLY * 2 + 1: IMF_K2P_LAUNCH(SH_POLY, true); break;
+                case SH_CIRCLEW * 2: IMF_K2P_LAUNCH(SH_CIRCLEW, false); break;
+                case SH_CIRCLEW * 2 + 1: IMF_K2P_LAUNCH(SH_CIRCLEW, true); break;
                 case SH_SPAN * 2 + 1: IMF_K2P_LAUNCH(SH_SPAN, true); break;
                 default: IMF_K2P_LAUNCH(SH_SPAN, false); break;
             }

@@ -38,8 +38,9 @@ constexpr int SH_SPAN = 0;    // any convex kernel: per-row span table (kernels.
 constexpr int SH_CIRCLE = 1;  // 4(dx^2+dy^2) <= (2r+1)^2 (kernels.py:70-71), packed bytes + IDP.4A
 constexpr int SH_SQUARE = 2;  // |dx|, |dy| <= r (kernels.py:72-73), packed 16-bit range tests
 constexpr int SH_POLY = 3;    // any convex kernel, per-row range constants looked up by dy byte
+constexpr int SH_CIRCLEW = 4; // circle, any tile (T + r > 128): unsigned-byte IDP.4A on x, y (see test8)
 
-constexpr int PT_MAX = 184;  // >= kernel rows / columns (2r+1) of every pair-path geometry
+constexpr int PT_MAX = 250;  // >= kernel rows / columns (2r+1, r <= 124)
 
 // Byte offsets into I relative to a window pair's base 2*(row*Sw + 2q), in
 // the constant bank.  Every list holds its 4-byte-aligned entries first; the
@@ -192,6 +193,21 @@ __device__ __forceinline__ uint32_t test8(const PairCtx& c, int v0, uint32_t Kc,
             m = __funnelshift_l((uint32_t)shi, m, 1);
             m = __funnelshift_l((uint32_t)slo, m, 1);
         }
+    } else if (SHAPE == SH_CIRCLEW) {
+        // Wide tiles: dx may exceed a signed byte, so expand instead
+        //   (x-cx)^2 + (y-cy)^2 - r(r+1) - 1 = (x^2 + y^2 + Kw) - 2 (x cx + y cy)
+        // with unsigned-byte dot products on the raw entry x | y << 8 (Kc holds
+        // cx | cy << 8): 2 IDP.4A + 1 IMAD per rank; the sign bit is membership.
+        const int Kw = cx * cx + cy * cy + c.nR2p1;
+        const uint32_t Clo = Kc, Chi = Kc << 16;
+#pragma unroll
+        for (int i = 3; i >= 0; i--) {
+            const uint32_t q = w[i];
+            const int slo = __dp4a(q, q & 0xffffu, (unsigned)Kw), shi = __dp4a(q, q & 0xffff0000u, (unsigned)Kw);
+            const int tlo = slo - 2 * (int)__dp4a(q, Clo, 0u), thi = shi - 2 * (int)__dp4a(q, Chi, 0u);
+            m = __funnelshift_l((uint32_t)thi, m, 1);
+            m = __funnelshift_l((uint32_t)tlo, m, 1);
+        }
     } else if (SHAPE == SH_SQUARE) {
         // bytes (dx+128, dy+128) of two ranks; per rank spread into 16-bit halves,
         // bit 15 of h + (0x8000 - (128 - r)) is [d >= -r] and of h + (0x8000 - (129 + r))
@@ -270,6 +286,14 @@ __device__ __forceinline__ uint32_t walk_init(Walk& w, int P, int cnt, int t, in
     return mask;
 }
 
+// Per-window constant of the membership test (walk_init's packed form, or
+// cx | cy << 8 for SH_CIRCLEW).
+template <int SHAPE>
+__device__ __forceinline__ uint32_t window_key(int cx, int cy) {
+    if (SHAPE == SH_CIRCLEW) return (uint32_t)cx | ((uint32_t)cy << 8);
+    return (uint32_t)((128 - cx) + ((128 - cy) << 8)) * 0x10001u;
+}
+
 // One 8-rank step.  A finished walk keeps v0 at its answer's block (msk: that
 // block's membership bits, need: in-window ranks to skip in it); a walk that
 // leaves [0, N) stops with v0 outside it (a defect).
@@ -330,7 +354,9 @@ __device__ __forceinline__ int walk_result(const PairCtx& c, const Walk& w) {
 template <int SHAPE, bool OMG>
 __device__ int refine8(const PairCtx& c, int cx, int cy, int P, int cnt, int t) {
     Walk w;
-    walk_step<SHAPE, OMG>(c, w, walk_init(w, P, cnt, t, cx, cy), cx, cy);
+    const uint32_t mask = walk_init(w, P, cnt, t, cx, cy);
+    w.Kc = window_key<SHAPE>(cx, cy);
+    walk_step<SHAPE, OMG>(c, w, mask, cx, cy);
     while (!w.done) walk_step2<SHAPE, OMG>(c, w, 0xffu, cx, cy);
     return walk_result(c, w);
 }
@@ -345,6 +371,8 @@ __device__ __forceinline__ void refine8x2(const PairCtx& c, int cx, int cy, int 
     Walk a, b;
     const uint32_t ma = walk_init(a, PA, cntA, tA, cx, cy);
     const uint32_t mb = walk_init(b, PB, cntB, tB, cx + 1, cy);
+    a.Kc = window_key<SHAPE>(cx, cy);
+    b.Kc = window_key<SHAPE>(cx + 1, cy);
     // first blocks (partial masks) peeled; then full blocks
     walk_step<SHAPE, OMG>(c, a, ma, cx, cy);
     walk_step<SHAPE, OMG>(c, b, mb, cx + 1, cy);
@@ -426,7 +454,7 @@ __device__ int refine_warp2(const PairCtx& c, int cx, int cy, int P, int cnt, in
         if (v < 0 || v >= c.N) return false;
         const uint32_t e = c.om[v];
         const int dx = (int)(e & 0xffu) - cx, dyr = (int)(e >> 8) - cy;
-        if (SHAPE == SH_CIRCLE) return dx * dx + dyr * dyr <= R2;
+        if (SHAPE == SH_CIRCLE || SHAPE == SH_CIRCLEW) return dx * dx + dyr * dyr <= R2;
         if (SHAPE == SH_SQUARE) return max(abs(dx), abs(dyr)) <= c.r;
         const int dy = dyr + c.r;
         if ((unsigned)dy > (unsigned)(2 * c.r)) return false;
@@ -458,7 +486,7 @@ template <int SHAPE>
 __device__ __forceinline__ bool inside1(const PairCtx& c, int v, int cx, int cy) {
     const uint32_t e = c.om[v];
     const int dx = (int)(e & 0xffu) - cx, dyr = (int)(e >> 8) - cy;
-    if (SHAPE == SH_CIRCLE) return dx * dx + dyr * dyr <= c.R2p1 - 1;
+    if (SHAPE == SH_CIRCLE || SHAPE == SH_CIRCLEW) return dx * dx + dyr * dyr <= c.R2p1 - 1;
     if (SHAPE == SH_SQUARE) return max(abs(dx), abs(dyr)) <= c.r;
     const int dy = dyr + c.r;
     if ((unsigned)dy > (unsigned)(2 * c.r)) return false;
@@ -849,6 +877,8 @@ IMF_K2P(SH_CIRCLE, true)
 IMF_K2P(SH_SQUARE, true)
 IMF_K2P(SH_POLY, false)
 IMF_K2P(SH_POLY, true)
+IMF_K2P(SH_CIRCLEW, false)
+IMF_K2P(SH_CIRCLEW, true)
 #undef IMF_K2P
 
 size_t k2_pair_smem_bytes(int N, int Npad, int NI, int r, int G, int T, int TY, bool omg) {

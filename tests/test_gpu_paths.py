@@ -39,6 +39,7 @@ VARIANTS = [
     {"IMF_STRIPE_EDGE": "1", "IMF_STRIPE_MID": "5"},
     {"IMF_RUNMIN": "2"},    # every replicate-copy group ranked as a run (bucket K1)
     {"IMF_RUNMIN": "64"},   # edge groups as runs at large r
+    {"IMF_PAIR_WIDE": "0"},  # r > 64 circles on the general select path
 ]
 
 CASES = [  # (dtype, shape, kernel spec)
@@ -48,7 +49,8 @@ CASES = [  # (dtype, shape, kernel spec)
     ("float32", (180, 200), ("circle", 20, 0, 0.0)),
     ("float32", (260, 240), ("circle", 60, 0, 0.0)),      # f32 global-entries bucket
     ("float32", (230, 250), ("circle", 40, 0, 0.0)),      # f32 adaptive buckets, own-pixel ranking
-    ("float32", (300, 280), ("circle", 100, 0, 0.0)),     # f32 r=100: corner runs (bucket_g)
+    ("float32", (300, 280), ("circle", 100, 0, 0.0)),     # f32 r=100: corner runs (bucket_g), wide pair K2
+    ("uint8", (230, 210, 2), ("circle", 75, 0, 0.0)),     # wide pair K2 (T + r > 128), u8
     ("uint8", (190, 170, 2), ("regular_polygon", 11, 6, 15.0)),
     ("uint8", (120, 130), ("square", 7, 0, 0.0)),
     ("float32", (70, 90), ("circle", 2, 0, 0.0)),         # direct selection (area <= 32)
