@@ -103,43 +103,69 @@ __device__ __forceinline__ uint32_t pivot_k(int PA, int PB) {
     return (uint32_t)(0x8000 - PA) | ((uint32_t)(0x8000 - PB) << 16);
 }
 
+// Two test words at once: bits 15 / 31 of d1 and d2 (the [I >= P] answers of
+// windows A / B) are the top bits of bytes 1 / 3; PRMT gathers them into one
+// word as bytes [A1, A2, B1, B2] and acc += (x & 0x80808080) >> 7 counts all
+// four in byte lanes (LOP3 + LEA.HI): 5 instructions per 4 tests instead of 6.
+__device__ __forceinline__ void acc_ge4(uint32_t& acc, uint32_t d1, uint32_t d2) {
+    const uint32_t x = prmt(d1, d2, 0x7351);
+    asm("{\n\t.reg .u32 t;\n\tand.b32 t, %1, 0x80808080;\n\tshr.u32 t, t, 7;\n\tadd.u32 %0, %0, t;\n\t}"
+        : "+r"(acc)
+        : "r"(x));
+}
+
+// Byte-lane counters [A1, A2, B1, B2] -> packed (A | B << 16).
+__device__ __forceinline__ uint32_t unpack4(uint32_t acc) {
+    return (acc & 0x00ff00ffu) + ((acc >> 8) & 0x00ff00ffu);
+}
+
 // Packed counts of [I >= P] over the vertical list at window-pair base `b`
-// (two accumulators per list so the LEA.HI chains interleave).
+// (entering and exiting lists; byte-lane accumulators, <= 2 * 124 + 1 columns).
 __device__ __forceinline__ void vcount(uint32_t b, const int2* __restrict__ v, int ne, int n, uint32_t K,
                                        uint32_t& ge_in, uint32_t& ge_out) {
-    uint32_t ai0 = 0, ao0 = 0, ai1 = 0, ao1 = 0;
+    uint32_t ai = 0, ao = 0, ri = 0, ro = 0;
     int k = 0;
 #pragma unroll 2
     for (; k + 1 < ne; k += 2) {
         const int2 o0 = v[k], o1 = v[k + 1];
-        acc_ge2(ai0, lds32(b + o0.x) + K);
-        acc_ge2(ao0, lds32(b + o0.y) + K);
-        acc_ge2(ai1, lds32(b + o1.x) + K);
-        acc_ge2(ao1, lds32(b + o1.y) + K);
+        acc_ge4(ai, lds32(b + o0.x) + K, lds32(b + o1.x) + K);
+        acc_ge4(ao, lds32(b + o0.y) + K, lds32(b + o1.y) + K);
     }
     if (k < ne) {
         const int2 o = v[k];
-        acc_ge2(ai0, lds32(b + o.x) + K);
-        acc_ge2(ao0, lds32(b + o.y) + K);
+        acc_ge2(ri, lds32(b + o.x) + K);
+        acc_ge2(ro, lds32(b + o.y) + K);
     }
 #pragma unroll 2
-    for (k = ne; k < n; k++) {
-        const int2 o = v[k];
-        acc_ge2(ai1, prmt(lds32(b + o.x), lds32(b + o.x + 4), 0x5432) + K);
-        acc_ge2(ao1, prmt(lds32(b + o.y), lds32(b + o.y + 4), 0x5432) + K);
+    for (k = ne; k + 1 < n; k += 2) {
+        const int2 o0 = v[k], o1 = v[k + 1];
+        acc_ge4(ai, prmt(lds32(b + o0.x), lds32(b + o0.x + 4), 0x5432) + K,
+                prmt(lds32(b + o1.x), lds32(b + o1.x + 4), 0x5432) + K);
+        acc_ge4(ao, prmt(lds32(b + o0.y), lds32(b + o0.y + 4), 0x5432) + K,
+                prmt(lds32(b + o1.y), lds32(b + o1.y + 4), 0x5432) + K);
     }
-    ge_in = ai0 + ai1;
-    ge_out = ao0 + ao1;
+    if (k < n) {
+        const int2 o = v[k];
+        acc_ge2(ri, prmt(lds32(b + o.x), lds32(b + o.x + 4), 0x5432) + K);
+        acc_ge2(ro, prmt(lds32(b + o.y), lds32(b + o.y + 4), 0x5432) + K);
+    }
+    ge_in = unpack4(ai) + ri;
+    ge_out = unpack4(ao) + ro;
 }
 
 // Packed count of [I >= P] over one horizontal list.
 __device__ __forceinline__ uint32_t hcount(uint32_t b, const int* __restrict__ h, int ne, int n, uint32_t K) {
-    uint32_t a = 0;
-#pragma unroll 4
-    for (int k = 0; k < ne; k++) acc_ge2(a, lds32(b + h[k]) + K);
+    uint32_t a = 0, rr = 0;
+    int k = 0;
 #pragma unroll 2
-    for (int k = ne; k < n; k++) acc_ge2(a, prmt(lds32(b + h[k]), lds32(b + h[k] + 4), 0x5432) + K);
-    return a;
+    for (; k + 1 < ne; k += 2) acc_ge4(a, lds32(b + h[k]) + K, lds32(b + h[k + 1]) + K);
+    if (k < ne) acc_ge2(rr, lds32(b + h[k]) + K);
+#pragma unroll 2
+    for (k = ne; k + 1 < n; k += 2)
+        acc_ge4(a, prmt(lds32(b + h[k]), lds32(b + h[k] + 4), 0x5432) + K,
+                prmt(lds32(b + h[k + 1]), lds32(b + h[k + 1] + 4), 0x5432) + K);
+    if (k < n) acc_ge2(rr, prmt(lds32(b + h[k]), lds32(b + h[k] + 4), 0x5432) + K);
+    return unpack4(a) + rr;
 }
 
 // Per-half difference lo(a) - lo(b), hi(a) - hi(b).
