@@ -499,11 +499,18 @@ __global__ void __launch_bounds__(1024) k1_count_reg(Geom g, uint16_t* __restric
         for (int i = tid; i < NW / 4; i += blockDim.x) h4[i] = make_uint4(0, 0, 0, 0);
     }
     __syncthreads();
+    // counting pass: the count a pixel's atomic returns is its index among the
+    // tile's equal values, kept in the key's high half, so rank = prefix(value)
+    // + that index -- the scatter needs a load, not a second atomic
 #pragma unroll
     for (int j = 0; j < NK; j++)
 #pragma unroll
         for (int k = 0; k < NK; k++)
-            if (v[j][k] != 0xffffffffu) atomicAdd(&hw[v[j][k] >> 1], 1u << ((v[j][k] & 1) << 4));
+            if (v[j][k] != 0xffffffffu) {
+                const uint32_t sh = (v[j][k] & 1) << 4;
+                const uint32_t old = atomicAdd(&hw[v[j][k] >> 1], 1u << sh);
+                v[j][k] |= ((old >> sh) & 0xffffu) << 16;
+            }
     __syncthreads();
     hist16_exclusive_scan(hw, NW);
     __syncthreads();
@@ -514,8 +521,8 @@ __global__ void __launch_bounds__(1024) k1_count_reg(Geom g, uint16_t* __restric
             const uint32_t val = v[j][k];
             if (val != 0xffffffffu) {
                 const uint32_t sh = (val & 1) << 4;
-                const uint32_t old = atomicAdd(&hw[val >> 1], 1u << sh);
-                om[(old >> sh) & 0xffffu] = (uint16_t)((lane + 32 * k) | ((wid + 32 * j) << 8));
+                const uint32_t rank = ((hw[(val & 0xffffu) >> 1] >> sh) & 0xffffu) + (val >> 16);
+                om[rank] = (uint16_t)((lane + 32 * k) | ((wid + 32 * j) << 8));
             }
         }
     for (int i = g.N + tid; i < g.Npad; i += blockDim.x) om[i] = 0xffffu;
