@@ -352,6 +352,8 @@ def run_ours(args):
     k2_ops = chp_rank * 1e6 * W * args.steps  # per rank
     achieved = k2_ops / (select_max * 1e-3)
     traffic, tsrc = load_ncu_traffic()
+    if args.workload != "c2" or args.radius is not None:  # the committed capture is of c2
+        traffic, tsrc = None, "no ncu capture committed for this workload (profiles/ holds c2's)"
     im0 = images[0]
     line = {
         "metric": "megapixels/sec circular median (r=8..100, 8/16-bit/f32)",

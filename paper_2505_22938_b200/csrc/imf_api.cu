@@ -857,7 +857,16 @@ int imf_filter_host(const imf_image* src, imf_image* dst, const imf_kernel* kern
     // two compute lanes (stripes alternate between them, each with its own
     // workspace) so one stripe's K1 fills the tail of the previous stripe's K2
     const bool two = env_int("IMF_STRIPE_LANES", 2) > 1;
-    if (cudaMallocAsync(&dsrc, sb, s) || cudaMallocAsync(&ddst, db, s) || cudaMallocAsync(&dws, p.ws_total, s) ||
+    const int OH0 = p.full_out_h;
+    const bool pipe0 = rows_outermost(src) && rows_outermost(dst) && OH0 > 2 * p.g.Th;
+    // batches stream through a ring of two device image slots (image b in slot
+    // b % 2, reused once image b - 2 is downloaded): device memory and the
+    // per-call allocation stay two images deep however long the batch
+    const bool ring = pipe0 && src->batch > 2 && env_int("IMF_RING", 1);
+    const int nslot = ring ? 2 : src->batch;
+    const size_t sbA = ring ? (size_t)nslot * src->stride_b * dsz : sb;
+    const size_t dbA = ring ? (size_t)nslot * dst->stride_b * dsz : db;
+    if (cudaMallocAsync(&dsrc, sbA, s) || cudaMallocAsync(&ddst, dbA, s) || cudaMallocAsync(&dws, p.ws_total, s) ||
         (two && cudaMallocAsync(&dws2, p.ws_total, s)) || (tb && cudaMallocAsync(&dtm, tb, s)))
         rc = cuda_fail(cudaGetLastError(), "cudaMallocAsync");
     if (!rc && tb && cudaMemcpyAsync(dtm, target_map, tb, cudaMemcpyHostToDevice, s))
@@ -868,8 +877,8 @@ int imf_filter_host(const imf_image* src, imf_image* dst, const imf_kernel* kern
     ds.data = dsrc;
     dd.data = ddst;
     const int r = kernel->radius, vshift = opt->boundary == IMF_BOUNDARY_VALID ? r : 0;
-    const int H = src->height, OH = p.full_out_h;
-    const bool pipe = rows_outermost(src) && rows_outermost(dst) && OH > 2 * p.g.Th;
+    const int H = src->height, OH = OH0;
+    const bool pipe = pipe0;
     // Stripes of whole tile rows: a one-tile-row first stripe (the filter starts
     // after a small upload), a one-tile-row last stripe (little left to download
     // after the last filter), and 8 middle stripes; consecutive stripes run on
@@ -897,8 +906,13 @@ int imf_filter_host(const imf_image* src, imf_image* dst, const imf_kernel* kern
     if (!rc) {
         cudaStreamWaitEvent(g_hs.up, e_alloc, 0);
         if (two) cudaStreamWaitEvent(g_hs.comp2, e_alloc, 0);
+        std::vector<cudaEvent_t> slot_free(nslot, nullptr);  // ring: last download of the slot's image
         for (int bi = 0; bi < src->batch && !rc; bi++) {
+            // host offsets of image bi; device offsets of its slot
             const long long sbase = (long long)bi * src->stride_b, dbase = (long long)bi * dst->stride_b;
+            const int slot = ring ? bi % nslot : bi;
+            const long long sdev = (long long)slot * src->stride_b, ddev = (long long)slot * dst->stride_b;
+            if (ring && slot_free[slot]) cudaStreamWaitEvent(g_hs.up, slot_free[slot], 0);
             int up_hi = 0;  // input rows [0, up_hi) of image bi are uploaded
             for (size_t si = 0; si + 1 < cuts.size() && !rc; si++) {
                 const int y0 = cuts[si], y1 = cuts[si + 1];
@@ -906,9 +920,10 @@ int imf_filter_host(const imf_image* src, imf_image* dst, const imf_kernel* kern
                     const int need = std::min(H, y1 - 1 + r + vshift + 1);
                     if (need > up_hi) {
                         const size_t off = (size_t)(sbase + (long long)up_hi * src->stride_y) * dsz;
+                        const size_t doff = (size_t)(sdev + (long long)up_hi * src->stride_y) * dsz;
                         const size_t len = (size_t)((long long)(need - up_hi) * src->stride_y) * dsz;
-                        const size_t cap = sb - off;
-                        if (cudaMemcpyAsync((char*)dsrc + off, (const char*)src->data + off, std::min(len, cap),
+                        const size_t cap = std::min(sb - off, sbA - doff);
+                        if (cudaMemcpyAsync((char*)dsrc + doff, (const char*)src->data + off, std::min(len, cap),
                                             cudaMemcpyHostToDevice, g_hs.up))
                             rc = cuda_fail(cudaGetLastError(), "stripe upload");
                         up_hi = need;
@@ -931,8 +946,8 @@ int imf_filter_host(const imf_image* src, imf_image* dst, const imf_kernel* kern
                 o.row_end = y1;
                 imf_image dsi = ds, ddi = dd;
                 if (pipe) {  // one image of the batch per launch sequence
-                    dsi.data = (char*)dsrc + (size_t)sbase * dsz;
-                    ddi.data = (char*)ddst + (size_t)dbase * dsz;
+                    dsi.data = (char*)dsrc + (size_t)sdev * dsz;
+                    ddi.data = (char*)ddst + (size_t)ddev * dsz;
                     dsi.batch = ddi.batch = 1;
                 } else {
                     o.row_begin = o.row_end = 0;
@@ -946,8 +961,10 @@ int imf_filter_host(const imf_image* src, imf_image* dst, const imf_kernel* kern
                 if (!rc) {
                     if (pipe) {
                         const size_t off = (size_t)(dbase + (long long)y0 * dst->stride_y) * dsz;
-                        const size_t len = std::min((size_t)((long long)(y1 - y0) * dst->stride_y) * dsz, db - off);
-                        if (cudaMemcpyAsync((char*)dst->data + off, (char*)ddst + off, len, cudaMemcpyDeviceToHost,
+                        const size_t doff = (size_t)(ddev + (long long)y0 * dst->stride_y) * dsz;
+                        const size_t len = std::min({(size_t)((long long)(y1 - y0) * dst->stride_y) * dsz, db - off,
+                                                     dbA - doff});
+                        if (cudaMemcpyAsync((char*)dst->data + off, (char*)ddst + doff, len, cudaMemcpyDeviceToHost,
                                             g_hs.down))
                             rc = cuda_fail(cudaGetLastError(), "stripe download");
                     } else if (cudaMemcpyAsync(dst->data, ddst, db, cudaMemcpyDeviceToHost, g_hs.down)) {
@@ -955,6 +972,10 @@ int imf_filter_host(const imf_image* src, imf_image* dst, const imf_kernel* kern
                     }
                 }
                 if (!pipe) break;
+            }
+            if (ring) {
+                slot_free[slot] = event();
+                cudaEventRecord(slot_free[slot], g_hs.down);
             }
             if (!pipe) break;
         }

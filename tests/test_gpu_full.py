@@ -208,6 +208,20 @@ def test_host_pipeline_stripes(boundary):
         assert np.array_equal(got[b], want), b
 
 
+def test_host_pipeline_ring_batch():
+    """Batches longer than two images stream through a ring of two device image
+    slots (image b reuses slot b % 2 after image b - 2 is downloaded)."""
+    from paper_2505_22938_b200 import FilterParams, ShapeSpec
+    from paper_2505_22938_b200.tiling import run_host
+    rng = np.random.default_rng(23)
+    src = rng.integers(0, 256, (5, 290, 270), dtype=np.uint8)
+    params = FilterParams(shape=ShapeSpec("circle", 9), percentile=0.3)
+    got = run_host(src, params, batched=True)
+    for b in range(5):
+        want = oracle.fast_filter(src[b], params.shape, 0.3, "replicate")
+        assert np.array_equal(got[b], want), b
+
+
 def test_device_row_range_stripes_assemble():
     """imf_options.row_begin/row_end: disjoint output stripes written by separate
     calls assemble to the whole-image result."""
