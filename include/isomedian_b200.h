@@ -127,8 +127,10 @@ int imf_workspace_status(void* workspace, void* stream);
  * whose rows are outermost within each plane group (HW, HWC, NHWC) are
  * pipelined in output-row stripes: the upload of stripe i+1, the filter of
  * stripe i and the download of stripe i-1 run concurrently (three streams,
- * event-ordered).  Device buffers come from the stream-ordered pool
- * (cudaMallocAsync).  Host buffers should be pinned for full copy bandwidth.
+ * event-ordered); batches of more than two such images reuse two device
+ * image slots (image b in slot b % 2).  Device buffers come from the
+ * stream-ordered pool (cudaMallocAsync).  Host buffers should be pinned for
+ * full copy bandwidth.
  */
 int imf_filter_host(const imf_image* src, imf_image* dst, const imf_kernel* kernel, int32_t target,
                     const int32_t* target_map, int32_t tmin, int32_t tmax, const imf_options* opt,
