@@ -291,7 +291,8 @@ int make_plan(const imf_image* src, const imf_kernel* k, const imf_options* opt,
     p.lanes = (p.total_tiles >= (p.k1_f32b_g ? 2 : 3) * min_chunk && env_int("IMF_LANES", 2) > 1) ? 2 : 1;
     long long chunk = (long long)(kOmegaScratchTarget / p.lanes / per_tile);
     if (p.lanes == 2) {
-        chunk = std::min<long long>(chunk, std::max<long long>(min_chunk, (p.total_tiles + 5) / 6));
+        const int nch = std::max(2, env_int("IMF_CHUNKS", 4));
+        chunk = std::min<long long>(chunk, std::max<long long>(min_chunk, (p.total_tiles + nch - 1) / nch));
         chunk = std::max<long long>(148, chunk / 148 * 148);  // whole waves of one-CTA-per-SM K1
     }
     chunk = std::max<long long>(chunk, 148);

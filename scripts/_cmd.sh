@@ -1,3 +1,3 @@
-mkdir -p gpurun_out
-timeout 1200 python bench.py --workload c5 --steps 3 --warmup 3 > gpurun_out/bench_c5.json 2> gpurun_out/bench_c5.err; echo rc=$?
-tail -2 gpurun_out/bench_c5.err
+python -c "from paper_2505_22938_b200 import build as b; assert not b.stale(), \"stale .so\"" || exit 3
+timeout 900 python -m pytest tests -x -q -m gpu 2>&1 | tail -2
+timeout 300 python scripts/quick_bench.py c1 c2 c3 c4 c5 2>&1 | cut -c1-100
