@@ -51,7 +51,8 @@ struct Plan {
     bool pair;  // K2 fast path (imf_pair.cu): two windows per thread, 15-bit ranks
     size_t k1_smem, k2_smem, k1_gs_per_tile;
     long long total_tiles, chunk_tiles;
-    size_t ws_omega, ws_k1g, ws_flags, ws_lane, ws_gr, ws_total;
+    size_t ws_omega, ws_k1g, ws_flags, ws_lane, ws_gr, ws_ctab, ws_total;
+    int ct_y0, ct_y1;  // rows of every plane the call reads (call-wide coarse table)
     int gr_y0, gr_rows, gr_shift;  // f32 image ranks (imf_grank.cu): rows and key shift
     int lanes;  // chunk streams (1 or 2)
 };
@@ -321,7 +322,19 @@ int make_plan(const imf_image* src, const imf_kernel* k, const imf_options* opt,
             p.ws_gr = ((4 * (size_t)n * g.B * g.C + 255) & ~(size_t)255) + 4 * gr_scratch_words(n);
         }
     }
-    p.ws_total = kStatusBytes + p.lanes * p.ws_lane + p.ws_gr;
+    // f32 adaptive buckets on the largest tiles (global entries, N > 40K):
+    // one call-wide coarse table instead of a coarse pass per tile.  The
+    // pre-pass over the image is serial; below ~40K-pixel tiles it costs more
+    // than the tiles' coarse passes (c3 r64: +6 %, r100: -4 %).  IMF_GCOARSE:
+    // 0 off, 1 auto, 2 for every adaptive tile.
+    p.ws_ctab = 0;
+    const int gco = env_int("IMF_GCOARSE", 1);
+    if (g.dtype == DT_F32 && p.k1_f32b && g.N > kAdaptiveMinN && (gco == 2 || (gco == 1 && g.N > 40000))) {
+        p.ct_y0 = std::max(0, std::min(H, g.oy_base - r + g.vshift));
+        p.ct_y1 = std::max(p.ct_y0, std::min(H, g.out_h + r + g.vshift));
+        p.ws_ctab = 4 * (size_t)kCoarse;
+    }
+    p.ws_total = kStatusBytes + p.lanes * p.ws_lane + p.ws_gr + p.ws_ctab;
     return IMF_OK;
 }
 
@@ -598,6 +611,17 @@ static int filter_impl(const imf_image* src, imf_image* dsts, int n, const int32
 
     Geom g = p.g;
     g.src = src->data;
+    g.ctab_g = nullptr;
+    if (p.ws_ctab && p.ct_y1 > p.ct_y0) {
+        uint32_t* ct = (uint32_t*)(ws + kStatusBytes + p.lanes * p.ws_lane + p.ws_gr);
+        if (cudaError_t e = cudaMemsetAsync(ct, 0, p.ws_ctab, s)) return cuda_fail(e, "coarse table memset");
+        const long long rows = (long long)(p.ct_y1 - p.ct_y0) * g.B * g.C;
+        const int cgrid = (int)std::min<long long>(296, (rows + 31) / 32);
+        k_coarse_hist<<<cgrid, 1024, 0, s>>>(g, p.ct_y0, p.ct_y1, ct);
+        k_coarse_alloc<<<1, 1024, 0, s>>>(ct);
+        g_launches += 2;
+        g.ctab_g = ct;
+    }
     if (grank) {
         g.gr = grank;
         g.gr_y0 = p.gr_y0;

@@ -36,6 +36,7 @@ struct Geom {
     int Tw, Th, Sw, Sh, N, Npad;   // N: ranked pixels per tile; Npad: N rounded up to a multiple of 64
     int fp, fpR2;                  // fp: only pixels within dist^2 <= fpR2 of the output rect are ranked
     int run_min;                   // bucket K1: copy groups (replicate boundary) this large rank as one run
+    const uint32_t* ctab_g;        // f32 bucket K1: call-wide fine-bucket table (k_coarse_*), or nullptr
     const uint32_t* gr;            // f32: image-wide ranks (imf_grank.cu) replace the keys, or nullptr
     int gr_y0, gr_rows, gr_shift;  // rows [gr_y0, gr_y0 + gr_rows) of every plane; key = rank << gr_shift
     int tiles_x, tiles_y;

@@ -595,6 +595,50 @@ __device__ void coarse_alloc(uint32_t* tab, int N) {
     __syncthreads();
 }
 
+// Call-wide fine-bucket table (f32): the coarse histogram of every pixel the
+// call reads (rows [y0, y1) of every plane), allocated once by coarse_alloc;
+// tiles then skip their own coarse pass.  Every key of every tile lies in a
+// populated coarse bin of this superset, so the table is valid for each tile
+// (f_c >= 16: fine buckets still span <= 2^16 keys); a tile whose values
+// cluster differently only sees larger buckets (sum-of-squares check).
+__global__ void __launch_bounds__(1024) k_coarse_hist(Geom g, int y0, int y1, uint32_t* __restrict__ counts) {
+    __shared__ uint32_t h[kCoarse];
+    for (int i = threadIdx.x; i < kCoarse; i += blockDim.x) h[i] = 0;
+    __syncthreads();
+    const long long rows = (long long)(y1 - y0) * g.B * g.C;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (long long rr = (long long)blockIdx.x * nw + wid; rr < rows; rr += (long long)gridDim.x * nw) {
+        const int y = y0 + (int)(rr % (y1 - y0));
+        const long long pc = rr / (y1 - y0);
+        TileCoord tc;
+        tc.b = (int)(pc / g.C);
+        tc.c = (int)(pc % g.C);
+        tc.src = (const char*)g.src + (tc.b * g.s_b + tc.c * g.s_c) * 4;
+        for (int x = lane; x < g.W; x += 32) atomicAdd(&h[f32_key(g, tc, y, x) >> 20], 1u);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < kCoarse; i += blockDim.x)
+        if (h[i]) atomicAdd(&counts[i], h[i]);
+}
+
+__global__ void __launch_bounds__(1024) k_coarse_alloc(uint32_t* __restrict__ tab) {
+    __shared__ uint32_t t[kCoarse];
+    __shared__ unsigned long long s_n;
+    if (threadIdx.x == 0) s_n = 0;
+    __syncthreads();
+    unsigned long long n = 0;
+    for (int i = threadIdx.x; i < kCoarse; i += blockDim.x) {
+        t[i] = tab[i];
+        n += t[i];
+    }
+    atomicAdd(&s_n, n);
+    __syncthreads();
+    // counts above 2^32 / 65536 would overflow coarse_alloc's 32-bit products
+    // only through n * room; it divides in 64 bits, but N is an int
+    coarse_alloc(t, (int)min(s_n, (unsigned long long)0x7fffffff));
+    for (int i = threadIdx.x; i < kCoarse; i += blockDim.x) tab[i] = t[i];
+}
+
 __device__ __forceinline__ uint32_t fine_bucket(const uint32_t* tab, uint32_t key) {
     const uint32_t t = tab[key >> 20], l = t >> 16;
     return (t & 0xffffu) + ((key & 0xfffffu) >> (20 - l));
@@ -917,7 +961,7 @@ __device__ __forceinline__ void f32_bucket_tile(const Geom& g, const TileCoord& 
         if (!own_rank)
             for (int i = tid; i < nsw; i += blockDim.x) starts[i] = 0;
         if (adaptive)
-            for (int i = tid; i < kCoarse; i += blockDim.x) ctab[i] = 0;
+            for (int i = tid; i < kCoarse; i += blockDim.x) ctab[i] = g.ctab_g ? g.ctab_g[i] : 0u;
         if (tid == 0) {
             s_sumsq = 0;
             s_runs = s_rl.n = s_rl.nbig = s_rl.nmark = s_rl.abort = 0;
@@ -925,12 +969,14 @@ __device__ __forceinline__ void f32_bucket_tile(const Geom& g, const TileCoord& 
     }
     __syncthreads();
     if (adaptive) {  // keys -> fine bucket << 16 | low 16 key bits
+        if (!g.ctab_g) {  // no call-wide table: this tile's own coarse pass
 #pragma unroll
-        for (int j = 0; j < NK; j++)
+            for (int j = 0; j < NK; j++)
 #pragma unroll
-            for (int k = 0; k < NK; k++)
-                if ((okm >> (j * NK + k)) & 1ull) atomicAdd(&ctab[v[j][k] >> 20], (uint32_t)weight(j, k));
-        coarse_alloc(ctab, N);
+                for (int k = 0; k < NK; k++)
+                    if ((okm >> (j * NK + k)) & 1ull) atomicAdd(&ctab[v[j][k] >> 20], (uint32_t)weight(j, k));
+            coarse_alloc(ctab, N);
+        }
 #pragma unroll
         for (int j = 0; j < NK; j++)
 #pragma unroll
@@ -1105,11 +1151,13 @@ __global__ void __launch_bounds__(1024) k1_f32_bucket_g(Geom g, uint16_t* __rest
         return adaptive ? (fine_bucket(ctab, key) << 16) | (key & 0xffffu) : key;
     };
     if (adaptive) {
-        for (int i = tid; i < kCoarse; i += blockDim.x) ctab[i] = 0;
+        for (int i = tid; i < kCoarse; i += blockDim.x) ctab[i] = g.ctab_g ? g.ctab_g[i] : 0u;
         __syncthreads();
-        each_pixel([&](int, int, uint32_t key, int wt, int, int) { atomicAdd(&ctab[key >> 20], (uint32_t)wt); });
-        coarse_alloc(ctab, N);
-    PHASE(1);
+        if (!g.ctab_g) {  // no call-wide table: this tile's own coarse pass
+            each_pixel([&](int, int, uint32_t key, int wt, int, int) { atomicAdd(&ctab[key >> 20], (uint32_t)wt); });
+            coarse_alloc(ctab, N);
+        }
+        PHASE(1);
     }
     bool runs = false;
     each_pixel([&](int, int, uint32_t key, int wt, int, int) {

@@ -40,6 +40,8 @@ VARIANTS = [
     {"IMF_RUNMIN": "2"},    # every replicate-copy group ranked as a run (bucket K1)
     {"IMF_RUNMIN": "64"},   # edge groups as runs at large r
     {"IMF_PAIR_WIDE": "0"},  # r > 64 circles on the general select path
+    {"IMF_GCOARSE": "2"},    # call-wide coarse bucket table for every adaptive f32 tile
+    {"IMF_GCOARSE": "0"},    # per-tile coarse passes only
 ]
 
 CASES = [  # (dtype, shape, kernel spec)
