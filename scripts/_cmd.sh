@@ -1,4 +1,3 @@
 python -c "from paper_2505_22938_b200 import build as b; assert not b.stale(), \"stale .so\"" || exit 3
-timeout 900 python -m pytest tests -x -q -m gpu 2>&1 | tail -2
-IMF_GCOARSE=2 timeout 900 python -m pytest tests/test_gpu_paths.py -x -q -m gpu 2>&1 | tail -2
-timeout 300 python scripts/quick_bench.py c3 2>&1 | cut -c1-100,200-215
+timeout 900 python -m pytest tests/test_gpu_paths.py -x -q -m gpu 2>&1 | tail -2
+timeout 300 python scripts/quick_bench.py c4 2>&1 | cut -c1-110
