@@ -45,6 +45,7 @@ struct Plan {
     bool k1_f32b;         // f32 bucket ordinal transform (+ k1_sort fallback on flagged tiles)
     bool k1_f32b_g;       // ... with the bucket entries in a global scratch slot per tile
     size_t k1b_smem;
+    bool k1_count_g;  // u16, S > ~180: counting sort scattering omega to global memory
     int full_out_h;
     bool direct;  // k_direct: per-pixel register sort (window area <= 32)
     int hs;     // k2_pair: ordinal image holds rank >> hs
@@ -235,7 +236,10 @@ int make_plan(const imf_image* src, const imf_kernel* k, const imf_options* opt,
     // f32 tiles beyond shared-memory entries, and u16 tiles beyond the 64K-bin
     // counting sort (S > ~180): the bucket transform with global entries
     // (u16 keys v << 16: every bucket is one value, ties only)
-    if ((g.dtype == DT_F32 || (g.dtype == DT_U16 && !p.k1_count)) && !p.k1_f32b && env_int("IMF_F32_BUCKET", 1)) {
+    // u16 tiles beyond it: the counting sort with omega in global memory
+    p.k1_count_g = g.dtype == DT_U16 && !p.k1_count && env_int("IMF_K1_COUNT_G", 1);
+    if ((g.dtype == DT_F32 || (g.dtype == DT_U16 && !p.k1_count && !p.k1_count_g)) && !p.k1_f32b &&
+        env_int("IMF_F32_BUCKET", 1)) {
         p.k1_f32b = p.k1_f32b_g = true;
         p.k1b_smem = k1_f32_bucket_g_smem_bytes(g.N);
     }
@@ -243,7 +247,7 @@ int make_plan(const imf_image* src, const imf_kernel* k, const imf_options* opt,
     p.k1_gmem = !p.k1_count && k1_smem_bytes(g.dtype, g.Npad, p.k1_threads / 32, false) > kSmemMax;
     p.k1_smem = p.k1_count ? k1_count_smem_bytes(g.dtype, g.Npad)
                            : k1_smem_bytes(g.dtype, g.Npad, p.k1_threads / 32, p.k1_gmem);
-    p.k1_gs_per_tile = p.k1_gmem ? k1_gscratch_bytes(g.dtype, g.Npad) : 0;
+    p.k1_gs_per_tile = (p.k1_gmem && !p.k1_count_g) ? k1_gscratch_bytes(g.dtype, g.Npad) : 0;
     // the global-entries bucket kernels need 6 B per pixel (entries + run
     // descriptors); the LSD fallback reuses the same slot (k1_gscratch_bytes(f32)
     // = 6 B per pixel when it needs one)
@@ -375,6 +379,7 @@ cudaError_t set_attrs() {
     if (!e) e = allow_smem(k1_sort<DT_F32, true>, optin);
     if (!e) e = allow_smem(k1_count<DT_U8>, optin);
     if (!e) e = allow_smem(k1_count<DT_U16>, optin);
+    if (!e) e = allow_smem(k1_count_g, optin);
 #define IMF_K1R_ATTR(DT)                                                          \
     if (!e) e = allow_smem(k1_count_reg<DT, 1>, optin);                          \
     if (!e) e = allow_smem(k1_count_reg<DT, 2>, optin);                          \
@@ -457,6 +462,10 @@ void launch_k1(const Plan& p, const Geom& g, int nblocks, uint16_t* omega, unsig
         } else {
             k1_sort<DT_F32, false><<<fgrid, block, p.k1_smem, s>>>(g, omega, k1g, gs, flags);
         }
+        return;
+    }
+    if (p.k1_count_g) {
+        k1_count_g<<<grid, dim3(1024), k1_count_g_smem_bytes(), s>>>(g, omega);
         return;
     }
     if (p.k1_count) {

@@ -1229,6 +1229,51 @@ size_t k1_f32_bucket_smem_bytes(int N) {
 template __global__ void k1_count<DT_U8>(Geom, uint16_t*);
 template __global__ void k1_count<DT_U16>(Geom, uint16_t*);
 
+// u16 tiles too large for the histogram AND omega in shared memory (S > ~180,
+// r > ~85): the same counting sort with omega scattered straight to the tile's
+// global slot (2-byte stores, L2-resident), keys read twice from the image.
+__global__ void __launch_bounds__(1024) k1_count_g(Geom g, uint16_t* __restrict__ omega_out) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    constexpr int NW = 32768;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+    const TileCoord tc = tile_coord(g, g.tile_begin + blockIdx.x);
+    const int S = g.Sw, SH = g.Sh, nk = (S + 31) >> 5;
+    uint32_t* hw = reinterpret_cast<uint32_t*>(smem);
+    uint16_t* om = omega_slot(g, omega_out);
+    {
+        uint4* h4 = reinterpret_cast<uint4*>(hw);
+        for (int i = tid; i < NW / 4; i += blockDim.x) h4[i] = make_uint4(0, 0, 0, 0);
+    }
+    __syncthreads();
+    auto each_pixel = [&](auto fn) {
+        for (int y = wid; y < SH; y += nw) {
+            uint32_t kv[8];
+#pragma unroll
+            for (int k = 0; k < 8; k++)
+                if (k < nk) kv[k] = load_key(g, tc, y, min(lane + 32 * k, S - 1));
+#pragma unroll
+            for (int k = 0; k < 8; k++)
+                if (k < nk && lane + 32 * k < S) fn(lane + 32 * k, y, kv[k]);
+        }
+    };
+    each_pixel([&](int, int, uint32_t v) { atomicAdd(&hw[v >> 1], 1u << ((v & 1) << 4)); });
+    __syncthreads();
+    hist16_exclusive_scan(hw, NW);
+    __syncthreads();
+    each_pixel([&](int x, int y, uint32_t v) {
+        const uint32_t sh = (v & 1) << 4;
+        const uint32_t old = atomicAdd(&hw[v >> 1], 1u << sh);
+        om[(old >> sh) & 0xffffu] = (uint16_t)(x | (y << 8));
+    });
+    for (int i = g.N + tid; i < g.Npad; i += blockDim.x) om[i] = 0xffffu;
+    if (tid < OMEGA_SLOT_PAD) {
+        om[-OMEGA_SLOT_PAD + tid] = 0xffffu;
+        om[g.Npad + tid] = 0xffffu;
+    }
+}
+
+size_t k1_count_g_smem_bytes() { return 32768 * 4 + 16; }
+
 size_t k1_count_smem_bytes(int dtype, int Npad) {
     return (dtype == DT_U8 ? 128 * 4 : 32768 * 4) + 2 * (size_t)Npad;
 }

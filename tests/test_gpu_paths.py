@@ -42,6 +42,7 @@ VARIANTS = [
     {"IMF_PAIR_WIDE": "0"},  # r > 64 circles on the general select path
     {"IMF_GCOARSE": "2"},    # call-wide coarse bucket table for every adaptive f32 tile
     {"IMF_GCOARSE": "0"},    # per-tile coarse passes only
+    {"IMF_K1_COUNT_G": "0"},  # u16 tiles beyond the shared counting sort via the bucket transform
 ]
 
 CASES = [  # (dtype, shape, kernel spec)
