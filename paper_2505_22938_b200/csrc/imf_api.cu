@@ -297,7 +297,8 @@ int make_plan(const imf_image* src, const imf_kernel* k, const imf_options* opt,
     // the L2 budget counts the omega slots only (they carry K1's result to K2);
     // K1's private scratch (entries) is written and read back within one CTA
     const size_t l2_per_tile = env_int("IMF_CHUNK_OMEGA_ONLY", 1) ? slot : per_tile;
-    long long chunk = (long long)(kOmegaScratchTarget / p.lanes / l2_per_tile);
+    const size_t target = (size_t)env_int("IMF_SCRATCH_MB", (int)(kOmegaScratchTarget >> 20)) << 20;
+    long long chunk = (long long)(target / p.lanes / l2_per_tile);
     if (p.lanes == 2) {
         const int nch = std::max(2, env_int("IMF_CHUNKS", 4));
         chunk = std::min<long long>(chunk, std::max<long long>(min_chunk, (p.total_tiles + nch - 1) / nch));
