@@ -536,7 +536,7 @@ __device__ __forceinline__ void to_state(const PairCtx& c, int hs, int m, int t,
 }
 
 template <int SHAPE, bool OMG>
-__global__ void __launch_bounds__(512) k2_pair(Geom g, PairParams p, const __grid_constant__ PairTab kt,
+__global__ void __launch_bounds__(512, 2) k2_pair(Geom g, PairParams p, const __grid_constant__ PairTab kt,
                                                const uint16_t* __restrict__ omega_in) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nwarps = blockDim.x >> 5;

@@ -1,1 +1,2 @@
-for mb in 64 96 128 192; do echo MB=$mb; IMF_SCRATCH_MB=$mb timeout 300 python scripts/quick_bench.py c2 c5 2>&1 | cut -c1-90; for r in 64 100; do IMF_SCRATCH_MB=$mb timeout 120 python scripts/quick_one.py f32 2048 2048 1 $r; done; done
+python -c "from paper_2505_22938_b200 import build as b; assert not b.stale(), \"stale .so\"" || exit 3
+timeout 900 python -m pytest tests -x -q -m gpu 2>&1 | tail -2
