@@ -1,2 +1,2 @@
-python -c "from paper_2505_22938_b200 import build as b; assert not b.stale(), \"stale .so\"" || exit 3
-timeout 900 python -m pytest tests -x -q -m gpu 2>&1 | tail -2
+mkdir -p gpurun_out
+timeout 1200 python bench.py --workload c5 --steps 3 --warmup 3 > gpurun_out/bench_c5.json 2> gpurun_out/bench_c5.err; echo rc=$?
