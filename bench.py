@@ -18,8 +18,15 @@ Contract:
   on the box (imf_int_peak), work W(r) = 4*C(r) + 384 int ops per channel-pixel
   (SURVEY.md 8(d)), K2 time from CUDA events around each K2 launch;
 * `cpu_baseline`: the reference algorithm restated in C (oracle/, all host
-  threads) on the same c2 frame -- rank 0, N = 1 only;
-* `--impl reference`: that CPU reference alone, rank 0 only, same metric.
+  threads) on the same c2 frame, plus the real reference package
+  (`isomedian`, numba, installed under baseline/_ref) on a bounded band of it
+  -- rank 0, N = 1 only;
+* `--impl reference`: the real reference package alone (its own
+  `filter_image`, numba engine, default workers), rank 0 only, same metric;
+  the C restatement when baseline/_ref is missing;
+* `--gpus N` without torchrun re-launches itself under torch.distributed.run
+  (N ranks, 127.0.0.1); `--workload c5` splits the 64-image batch across the
+  ranks (strong scaling), every other workload is one frame per rank (weak).
 """
 
 from __future__ import annotations
@@ -65,7 +72,40 @@ def parse():
     ap.add_argument("--radius", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    # launcher check (tests/test_bench_launch.py): ranks rendezvous over gloo and
+    # report their shard of the workload; no GPU work
+    ap.add_argument("--plan-only", action="store_true", help=argparse.SUPPRESS)
     return ap.parse_args()
+
+
+def maybe_spawn(args):
+    """`python bench.py --gpus N` (N > 1) outside torchrun: re-run this script
+    as N ranks under torch.distributed.run on 127.0.0.1.  Returns the exit
+    code, or None when already inside a launcher (or N == 1)."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return None
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+def host_cpu():
+    """CPU model and logical cores of this host (for the baseline records)."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"model": model, "logical_cores": os.cpu_count()}
 
 
 def dist_env():
@@ -75,13 +115,45 @@ def dist_env():
     return rank, world, local
 
 
+def shard_indices(name, rank, world):
+    """Images of `rank`: c5 splits its 64-image batch round-robin (strong
+    scaling: whole images per GPU); the other workloads give
+    every rank its own frame (weak scaling)."""
+    if name == "c5":
+        return list(range(rank, 64, world))
+    return [0]
+
+
 def workload_inputs(name, rank, world):
     """Per-rank host images (list) and the spec for the workload."""
     spec = WORKLOADS[name]["spec"]
     if name == "c5":
-        idx = list(range(rank, 64, world))
-        return [C.baseline_input("c5", i) for i in idx], spec
+        return [C.baseline_input("c5", i) for i in shard_indices(name, rank, world)], spec
     return [C.baseline_input(name)], spec
+
+
+def run_plan_only(args):
+    """Launcher check on CPU: gloo rendezvous, every rank reports its shard,
+    max-over-ranks reduction of a dummy timing, rank 0 prints one line."""
+    import torch
+    import torch.distributed as dist
+    rank, world, _ = dist_env()
+    if world > 1:
+        dist.init_process_group("gloo")
+    mine = shard_indices(args.workload, rank, world)
+    t = torch.tensor([float(len(mine))])
+    shards = [None] * world
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_gather_object(shards, mine)
+        dist.destroy_process_group()
+    else:
+        shards = [mine]
+    if rank == 0:
+        print(json.dumps({"plan_only": True, "n_gpus": world, "workload": args.workload,
+                          "scaling": "strong" if args.workload == "c5" else "weak",
+                          "shards": shards, "max_images_per_rank": t.item()}), flush=True)
+    return 0
 
 
 def workload_spec(args):
@@ -173,6 +245,44 @@ def load_ncu_traffic():
         return None, None
 
 
+def _import_reference():
+    """The real reference package from baseline/_ref (bench's CPU legs only)."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "isomedian")):
+        return None
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache_imf")
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    try:
+        import isomedian
+        return isomedian
+    except Exception:  # numba missing etc.: the C restatement stands in
+        return None
+
+
+def reference_sample(name, images):
+    """Bounded band of the workload for the numba reference: whole rows of the
+    first image, all tile columns (the reference parallelizes over them)."""
+    im = images[0]
+    rows = {"c1": im.shape[0], "c3": 512, "c5": 256}.get(name, 256)
+    return im[:rows]
+
+
+def numba_reference_run(iso, band, spec, reps=1):
+    """Seconds per pass of isomedian.filter_image (default FilterParams:
+    forwarding on, workers = min(#tile columns, cpu_count), tiling.py:238)."""
+    params = iso.FilterParams(shape=iso.ShapeSpec(*spec))
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        iso.filter_image(band, params)
+    return (time.perf_counter() - t0) / reps
+
+
+def numba_warmup(iso, band, spec):
+    small = band[: min(band.shape[0], 2 * spec[1] + 8), : min(band.shape[1], 2 * spec[1] + 8)]
+    iso.filter_image(small, iso.FilterParams(shape=iso.ShapeSpec(*spec)))  # numba JIT
+
+
 def cpu_reference_run(images, spec, threads):
     import oracle  # CPU baseline leg only (test infrastructure)
     from paper_2505_22938_b200 import ShapeSpec
@@ -188,32 +298,50 @@ def run_reference(args):
     if rank != 0:
         return 0
     spec = workload_spec(args)
-    images, _ = workload_inputs(args.workload, 0, 1)
-    if args.workload == "c5":
-        images = images[:2]  # bounded sample
-    threads = os.cpu_count() or 1
-    for _ in range(args.warmup):
-        cpu_reference_run(images, spec, threads)
-    total = 0.0
-    for _ in range(args.steps):
-        total += cpu_reference_run(images, spec, threads)
-    mp = mp_of(images)
-    value = mp * args.steps / total
+    images, _ = workload_inputs(args.workload, 0, 1) if args.workload != "c5" else \
+        ([C.baseline_input("c5", 0)], None)
+    iso = _import_reference()
     im0 = images[0]
+    cols = -(-im0.shape[1] // min(64, 256 - 2 * spec[1] - 1))
+    if iso is not None:
+        band = reference_sample(args.workload, images)
+        numba_warmup(iso, band, spec)
+        for _ in range(args.warmup):
+            numba_reference_run(iso, band, spec)
+        total = sum(numba_reference_run(iso, band, spec) for _ in range(args.steps))
+        mp = band.shape[0] * band.shape[1] / 1e6
+        cores = min(cols, os.cpu_count() or 1)
+        kind = "reference"
+        sample = (f"rows [0, {band.shape[0]}) x all {band.shape[1]} columns of the {args.workload} "
+                  f"frame per step: the reference package itself (isomedian.filter_image, numba "
+                  f"engine, baseline/_ref), default FilterParams, workers = min({cols} tile "
+                  f"columns, {os.cpu_count()} cpus)")
+    else:
+        if args.workload == "c5":
+            images = images[:1]
+        threads = os.cpu_count() or 1
+        for _ in range(args.warmup):
+            cpu_reference_run(images, spec, threads)
+        total = sum(cpu_reference_run(images, spec, threads) for _ in range(args.steps))
+        mp = mp_of(images)
+        cores = threads
+        kind = "port"
+        sample = (f"{len(images)} full {args.workload} image(s) per step (reference fast engine "
+                  "restated in C, oracle/, pthreads over tile columns, forwarding on; "
+                  "baseline/_ref not installed)")
+    value = mp * args.steps / total
     line = {
         "impl": "reference",
         "metric": "megapixels/sec circular median (r=8..100, 8/16-bit/f32)",
         "value": round(value, 4), "unit": "MP/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(1e3 * total / args.steps, 2),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "higher_is_better": True, "scaling": "strong" if args.workload == "c5" else "weak",
+        "vs_baseline": None,
         "dtype": DT_NAME[im0.dtype], "data": "synthetic (numpy default_rng seeds, SURVEY.md 8(d))",
         "config": {"workload": f"{args.workload}: {WORKLOADS[args.workload]['desc'].format(r=spec[1])}",
-                   "images_per_step": len(images)},
-        "cpu_baseline": {"value": round(value, 4), "unit": "MP/s", "cores": threads,
-                         "kind": "port",
-                         "sample": f"{len(images)} full {args.workload} image(s) per step "
-                                   "(reference fast engine restated in C, oracle/, pthreads "
-                                   "over tile columns, forwarding on)"},
+                   "images_per_step": 1},
+        "cpu_baseline": {"value": round(value, 4), "unit": "MP/s", "cores": cores, "kind": kind,
+                         "sample": sample, "cpu": host_cpu()},
         "e2e": {"value": round(value, 4), "unit": "MP/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -298,9 +426,12 @@ def run_ours(args):
     select_ms *= args.steps / prof_steps
     dev_ms = sum(e0.elapsed_time(e1) for e0, e1 in evs)
     t = torch.tensor([dev_ms, sort_ms, select_ms], dtype=torch.float64, device=dev)
+    work = torch.tensor([mp_of(images), chp_of(images)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(work, op=dist.ReduceOp.SUM)  # MP all ranks filter per step
     dev_ms_max, sort_max, select_max = t.tolist()
+    total_mp, total_chp = work.tolist()
 
     # ---- end-to-end through the public call with host buffers ---------------
     e2e = None
@@ -329,11 +460,30 @@ def run_ours(args):
         raise RuntimeError(f"scan defect / error in timed region: {_lib.strerror(st)}")
 
     # ---- parity spot check of the timed output (c2: golden digest) ----------
+    # (c1, c2, c3 at its radius, c4: golden.json; c5: every image of this rank
+    # against golden_c5.json) -- the e2e pass filled out_pin, the device pass out
     parity = None
-    if rank == 0 and args.workload in ("c1", "c2") and args.radius is None:
-        with open(os.path.join(ROOT, "tests", "golden", "golden.json")) as f:
-            gold = json.load(f)["baseline"][args.workload]
-        parity = C.digest(out_pin[0].numpy()) == gold
+    gdir = os.path.join(ROOT, "tests", "golden")
+    gold = None
+    if args.workload == "c5" and args.radius is None:
+        with open(os.path.join(gdir, "golden_c5.json")) as f:
+            g5 = json.load(f)
+        gold = [g5[str(i)] for i in shard_indices("c5", rank, world)]
+    else:
+        with open(os.path.join(gdir, "golden.json")) as f:
+            gb = json.load(f)["baseline"]
+        key = {"c3": f"c3/r{spec[1]}", "c4": f"c4/{json.dumps(list(spec))}"}.get(args.workload, args.workload)
+        if args.radius is None or args.workload == "c3":
+            gold = [gb.get(key)] if gb.get(key) else None
+    if gold:
+        res = out.cpu() if e2e is None else out_pin
+        ok = all(C.digest(res[i].numpy()) == d for i, d in enumerate(gold))
+        if e2e is not None:
+            ok = ok and all(C.digest(out[i].cpu().numpy()) == d for i, d in enumerate(gold))
+        pt = torch.tensor([0.0 if ok else 1.0], device=dev)
+        if world > 1:
+            dist.all_reduce(pt, op=dist.ReduceOp.MAX)
+        parity = pt.item() == 0.0
 
     peak = ctypes.c_double()
     L.imf_int_peak(ctypes.byref(peak), None)
@@ -343,11 +493,9 @@ def run_ours(args):
     if rank != 0:
         return 0
 
-    mp_rank = mp_of(images)
     chp_rank = chp_of(images)
-    total_mp = mp_rank * world  # weak scaling: every rank filters its own batch
     value = total_mp * args.steps / (dev_ms_max * 1e-3)
-    ch_value = chp_rank * world * args.steps / (dev_ms_max * 1e-3)
+    ch_value = total_chp * args.steps / (dev_ms_max * 1e-3)
     W = work_per_chpx(kernel)
     k2_ops = chp_rank * 1e6 * W * args.steps  # per rank
     achieved = k2_ops / (select_max * 1e-3)
@@ -359,14 +507,17 @@ def run_ours(args):
         "metric": "megapixels/sec circular median (r=8..100, 8/16-bit/f32)",
         "value": round(value, 2), "unit": "MP/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(dev_ms_max / args.steps, 4),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "higher_is_better": True, "scaling": "strong" if args.workload == "c5" else "weak",
+        "vs_baseline": None,
         "dtype": DT_NAME[im0.dtype],
         "data": "synthetic (numpy default_rng seeds per SURVEY.md 8(d); no model weights)",
         "config": {"workload": f"{args.workload}: {WORKLOADS[args.workload]['desc'].format(r=spec[1])}",
                    "images_per_rank": len(images), "channels": int(im0.shape[2]) if im0.ndim == 3 else 1,
                    "kernel_area": kernel.area, "kernel_cols": len(kernel.col_dx),
                    "l2": "flushed between timed steps (256 MiB memset, outside the events)",
-                   "parallelism": f"replicas/shards x{world} (no collective on the path)"},
+                   "parallelism": (f"64-image batch split over {world} rank(s), whole images per "
+                                   "GPU (no collective on the path)" if args.workload == "c5" else
+                                   f"one frame per rank x{world} (no collective on the path)")},
         "ch_mp_per_s": round(ch_value, 2),
         "gpu_launches": int(launches),
         "kernel_ms_per_step": {"sort_k1": round(sort_max / args.steps, 4),
@@ -391,21 +542,48 @@ def run_ours(args):
                        "h2d_bytes_per_step": int(host.numel() * host.element_size()),
                        "d2h_bytes_per_step": int(out_pin.numel() * out_pin.element_size())}
     if world == 1 and not args.no_cpu_baseline:
+        import oracle  # CPU baseline leg only (test infrastructure)
         spec_c = spec
         cpu_imgs = images if args.workload != "c5" else images[:1]
         threads = os.cpu_count() or 1
         secs = cpu_reference_run(cpu_imgs, spec_c, threads)
+        cols = -(-im0.shape[1] // min(64, 256 - 2 * spec[1] - 1))
         line["cpu_baseline"] = {"value": round(mp_of(cpu_imgs) / secs, 4), "unit": "MP/s",
                                 "cores": threads, "kind": "port",
                                 "sample": f"{len(cpu_imgs)} full {args.workload} image(s), one pass "
                                           f"({secs:.2f} s): reference fast engine restated in C "
-                                          "(oracle/), pthreads over tile columns"}
+                                          "(oracle/), pthreads over tile columns",
+                                "cpu": host_cpu(),
+                                "worker_cap": f"min({cols} tile columns, {threads} threads)"}
+        iso = _import_reference()
+        if iso is not None:
+            band = reference_sample(args.workload, cpu_imgs)
+            numba_warmup(iso, band, spec)
+            bs = numba_reference_run(iso, band, spec, reps=2)
+            line["cpu_baseline"]["reference_package"] = {
+                "value": round(band.shape[0] * band.shape[1] / 1e6 / bs, 4), "unit": "MP/s",
+                "cores": min(cols, threads), "kind": "reference",
+                "sample": f"rows [0, {band.shape[0]}) of the frame, mean of 2 passes ({bs:.2f} s): "
+                          "isomedian.filter_image from baseline/_ref (numba), default FilterParams"}
+        # measured S-bar: segments the reference refine scans per
+        # window, on a 512x512 crop of the first plane (single-threaded oracle pass)
+        crop = im0[:512, :512, 0] if im0.ndim == 3 else im0[:512, :512]
+        sbar = oracle.segment_stats(np.ascontiguousarray(crop), ShapeSpec(*spec))
+        ncols = len(kernel.col_dx)
+        line["roofline"]["measured_sbar"] = round(sbar, 4)
+        line["roofline"]["element_tests_E"] = 2 * ncols + 64
+        line["roofline"]["work_per_chpx_at_sbar"] = round(4 * ncols + 384 * sbar, 1)
     print(json.dumps(line), flush=True)
     return 0
 
 
 def main():
     args = parse()
+    rc = maybe_spawn(args)
+    if rc is not None:
+        return rc
+    if args.plan_only:
+        return run_plan_only(args)
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

@@ -90,6 +90,9 @@ typedef struct imf_options {
 
 #define IMF_FLAG_PROFILE 1      /* per-kernel CUDA-event timing, see imf_profile_last */
 #define IMF_FLAG_KEEP_STATUS 2  /* do not clear the workspace status word (stripe 2..n of one job) */
+#define IMF_FLAG_DEBUG_DEFECT 4 /* test hook: corrupt one window's slide count in the first tile so its
+                                   segment scan leaves the rank array and the call reports IMF_ERR_DEFECT
+                                   (reference test_core.py:124-130).  Rank paths only (window area > 32) */
 
 /* Bytes of device workspace imf_filter needs for this problem. */
 size_t imf_workspace_size(const imf_image* src, const imf_kernel* kernel, const imf_options* opt);
@@ -130,7 +133,12 @@ int imf_workspace_status(void* workspace, void* stream);
  * event-ordered); batches of more than two such images reuse two device
  * image slots (image b in slot b % 2).  Device buffers come from the
  * stream-ordered pool (cudaMallocAsync).  Host buffers should be pinned for
- * full copy bandwidth.
+ * full copy bandwidth.  dst must be dense (every byte of its extent belongs
+ * to an element, e.g. C-contiguous: row ranges are copied back as whole byte
+ * ranges), else IMF_ERR_INVALID.  opt->row_begin/row_end select an output
+ * row range: only the input rows it reads are uploaded and only its output
+ * rows of dst are written (one device's stripe of a multi-device job; needs
+ * row-outermost src and dst).
  */
 int imf_filter_host(const imf_image* src, imf_image* dst, const imf_kernel* kernel, int32_t target,
                     const int32_t* target_map, int32_t tmin, int32_t tmax, const imf_options* opt,

@@ -148,6 +148,20 @@ def fast_filter(image, shape, percentile=0.5, boundary="replicate", threads=None
     return _run("fast", image, shape, percentile, boundary, threads, tile_size, forwarding)
 
 
+def segment_stats(image, shape, percentile=0.5, boundary="replicate"):
+    """Measured S-bar: mean 64-rank segments the reference
+    refine scans per window, over one single-threaded fast-engine pass."""
+    lib = _lib()
+    lib.orc_segment_stats.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]
+    lib.orc_segment_stats(1, None, None)
+    try:
+        fast_filter(image, shape, percentile, boundary, threads=1)
+    finally:
+        segs, refines = ctypes.c_longlong(), ctypes.c_longlong()
+        lib.orc_segment_stats(0, ctypes.byref(segs), ctypes.byref(refines))
+    return segs.value / max(refines.value, 1)
+
+
 def brute_filter(image, shape, percentile=0.5, boundary="replicate", threads=None):
     """Reference brute oracle restated in C (oracle.py:88-121)."""
     return _run("brute", image, shape, percentile, boundary, threads)

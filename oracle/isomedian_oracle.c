@@ -200,9 +200,41 @@ static inline int64_t kth_bit(uint64_t mask, int64_t need) {
     return -1;
 }
 
-/* core.py:87-146; returns m (-1 on an inconsistent count) */
+/* Optional segment statistics (bench.py reports the measured S-bar of
+ * 64-rank segments scanned per refined window).  Off by
+ * default; one predictable branch per refine when off. */
+static int g_seg_on = 0;
+static long long g_seg_total = 0, g_refine_total = 0;
+
+void orc_segment_stats(int enable, long long *segments, long long *refines) {
+    if (segments) *segments = __atomic_load_n(&g_seg_total, __ATOMIC_RELAXED);
+    if (refines) *refines = __atomic_load_n(&g_refine_total, __ATOMIC_RELAXED);
+    if (enable >= 0) {
+        g_seg_on = enable;
+        __atomic_store_n(&g_seg_total, 0, __ATOMIC_RELAXED);
+        __atomic_store_n(&g_refine_total, 0, __ATOMIC_RELAXED);
+    }
+}
+
+static int64_t refine_(const orc_tile *ot, int64_t cx, int64_t cy, int64_t pivot, int64_t count,
+                       int64_t target, const orc_kernel *k, int64_t *npiv_out, int64_t *ncnt_out,
+                       long long *segs);
+
 static int64_t refine(const orc_tile *ot, int64_t cx, int64_t cy, int64_t pivot, int64_t count,
                       int64_t target, const orc_kernel *k, int64_t *npiv_out, int64_t *ncnt_out) {
+    long long segs = 0;
+    int64_t m = refine_(ot, cx, cy, pivot, count, target, k, npiv_out, ncnt_out, &segs);
+    if (g_seg_on) {
+        __atomic_add_fetch(&g_seg_total, segs, __ATOMIC_RELAXED);
+        __atomic_add_fetch(&g_refine_total, 1, __ATOMIC_RELAXED);
+    }
+    return m;
+}
+
+/* core.py:87-146; returns m (-1 on an inconsistent count) */
+static int64_t refine_(const orc_tile *ot, int64_t cx, int64_t cy, int64_t pivot, int64_t count,
+                       int64_t target, const orc_kernel *k, int64_t *npiv_out, int64_t *ncnt_out,
+                       long long *segs) {
     int64_t n = ot->n;
     int64_t cap = 64 * ((n - 1) >> 6);
     int64_t s = pivot >> 6, c = count;
@@ -211,6 +243,7 @@ static int64_t refine(const orc_tile *ot, int64_t cx, int64_t cy, int64_t pivot,
         for (;;) {
             if (s * 64 >= n) return -1;
             uint64_t mask = segment_mask(ot, s, cx, cy, k, &pop);
+            (*segs)++;
             if (c + pop > target) {
                 int64_t kb = kth_bit(mask, target - c);
                 int64_t m = kb < 0 ? -1 : s * 64 + kb;
@@ -227,6 +260,7 @@ static int64_t refine(const orc_tile *ot, int64_t cx, int64_t cy, int64_t pivot,
             s--;
             if (s < 0) return -1;
             uint64_t mask = segment_mask(ot, s, cx, cy, k, &pop);
+            (*segs)++;
             int64_t base_c = c - pop;
             if (base_c <= target) {
                 int64_t kb = kth_bit(mask, target - base_c);

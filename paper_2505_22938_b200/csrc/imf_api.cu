@@ -4,12 +4,13 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdio>
+#include <mutex>
 #include <cstdlib>
 #include <cstring>
 #include <vector>
 
 #include "../../include/isomedian_b200.h"
-#include "imf_common.cuh"
+#include "imf_kernels.cuh"
 
 
 using namespace imf;
@@ -52,9 +53,8 @@ struct Plan {
     bool pair;  // K2 fast path (imf_pair.cu): two windows per thread, 15-bit ranks
     size_t k1_smem, k2_smem, k1_gs_per_tile;
     long long total_tiles, chunk_tiles;
-    size_t ws_omega, ws_k1g, ws_flags, ws_lane, ws_gr, ws_ctab, ws_total;
+    size_t ws_omega, ws_k1g, ws_flags, ws_lane, ws_ctab, ws_total;
     int ct_y0, ct_y1;  // rows of every plane the call reads (call-wide coarse table)
-    int gr_y0, gr_rows, gr_shift;  // f32 image ranks (imf_grank.cu): rows and key shift
     int lanes;  // chunk streams (1 or 2)
 };
 
@@ -312,24 +312,6 @@ int make_plan(const imf_image* src, const imf_kernel* k, const imf_options* opt,
     p.ws_k1g = (size_t)chunk * p.k1_gs_per_tile;
     p.ws_flags = p.k1_f32b ? (((size_t)(chunk + 1) * 4 + 255) & ~(size_t)255) : 0;
     p.ws_lane = p.ws_omega + p.ws_k1g + p.ws_flags;
-    // f32, opt-in (IMF_GRANK=1): rank the keys of the rows this launch reads,
-    // image-wide, first (bucket sizes <= 64 everywhere; measured slower than the
-    // tile-local buckets on c3 -- the 4-pass global radix sort costs ~1 ms for
-    // 4 Mpixels as written)
-    p.ws_gr = 0;
-    if (g.dtype == DT_F32 && p.k1_f32b && env_int("IMF_GRANK", 0)) {
-        const int y0 = std::max(0, std::min(H, g.oy_base - r + g.vshift));
-        const int y1 = std::max(y0, std::min(H, g.out_h + r + g.vshift));
-        const long long n = (long long)(y1 - y0) * W;
-        if (n > 0 && n < (1ll << 31)) {
-            int bits = 0;
-            while ((1ll << bits) < n) bits++;
-            p.gr_y0 = y0;
-            p.gr_rows = y1 - y0;
-            p.gr_shift = 32 - bits;
-            p.ws_gr = ((4 * (size_t)n * g.B * g.C + 255) & ~(size_t)255) + 4 * gr_scratch_words(n);
-        }
-    }
     // f32 adaptive buckets on the largest tiles (global entries, N > 40K):
     // one call-wide coarse table instead of a coarse pass per tile.  The
     // pre-pass over the image is serial; below ~40K-pixel tiles it costs more
@@ -342,7 +324,7 @@ int make_plan(const imf_image* src, const imf_kernel* k, const imf_options* opt,
         p.ct_y1 = std::max(p.ct_y0, std::min(H, g.out_h + r + g.vshift));
         p.ws_ctab = 4 * (size_t)kCoarse;
     }
-    p.ws_total = kStatusBytes + p.lanes * p.ws_lane + p.ws_gr + p.ws_ctab;
+    p.ws_total = kStatusBytes + p.lanes * p.ws_lane + p.ws_ctab;
     return IMF_OK;
 }
 
@@ -360,7 +342,11 @@ void build_ktab_struct(const imf_kernel* k, int Sw, KTab& t) {
 }
 
 
-bool g_attr_done = false;
+// cudaFuncSetAttribute (the >48 KB shared-memory opt-in) is per device:
+// one bit per device ordinal, set once under a mutex.
+constexpr int kMaxDev = 64;
+std::atomic<uint64_t> g_attr_mask{0};
+std::mutex g_attr_mu;
 
 template <typename F>
 cudaError_t allow_smem(F* f, int optin) {
@@ -372,10 +358,15 @@ cudaError_t allow_smem(F* f, int optin) {
 }
 
 cudaError_t set_attrs() {
-    if (g_attr_done) return cudaSuccess;
     int dev = 0, optin = 0;
     cudaError_t e = cudaGetDevice(&dev);
-    if (!e) e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    if (e) return e;
+    if (dev >= kMaxDev) return cudaErrorInvalidDevice;
+    const uint64_t bit = 1ull << dev;
+    if (g_attr_mask.load(std::memory_order_acquire) & bit) return cudaSuccess;
+    std::lock_guard<std::mutex> lk(g_attr_mu);
+    if (g_attr_mask.load(std::memory_order_relaxed) & bit) return cudaSuccess;
+    e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     if (!e) e = allow_smem(k1_sort<DT_U8, false>, optin);
     if (!e) e = allow_smem(k1_sort<DT_U16, false>, optin);
     if (!e) e = allow_smem(k1_sort<DT_U16, true>, optin);
@@ -422,7 +413,7 @@ cudaError_t set_attrs() {
     if (!e) e = allow_smem(k2_pair<SH_POLY, true>, optin);
     if (!e) e = allow_smem(k2_pair<SH_CIRCLEW, false>, optin);
     if (!e) e = allow_smem(k2_pair<SH_CIRCLEW, true>, optin);
-    if (!e) g_attr_done = true;
+    if (!e) g_attr_mask.fetch_or(bit, std::memory_order_release);
     return e;
 }
 
@@ -433,7 +424,7 @@ void launch_k1(const Plan& p, const Geom& g, int nblocks, uint16_t* omega, unsig
     if (p.k1_f32b) {
         const dim3 b1024(1024);
         cudaMemsetAsync(flags, 0, sizeof(int), s);  // fallback list count
-        static const unsigned long long mss = (unsigned long long)env_int("IMF_MAXSUMSQ_K", 65536) << 10;
+        const unsigned long long mss = (unsigned long long)env_int("IMF_MAXSUMSQ_K", 65536) << 10;
         const int nk = (g.Sw + 31) >> 5;
         if (p.k1_f32b_g && nk > 6) {
             k1_f32_bucket_g<<<grid, b1024, p.k1b_smem, s>>>(g, omega, flags, (uint32_t*)k1g, gs / 4, mss);
@@ -592,33 +583,6 @@ static int filter_impl(const imf_image* src, imf_image* dsts, int n, const int32
 
     static thread_local KTab kt;
     build_ktab_struct(kernel, p.g.Sw, kt);
-    uint32_t* grank = nullptr;
-    float gr_ms = 0.f;
-    cudaEvent_t gr_e0 = nullptr, gr_e1 = nullptr;
-    if (p.ws_gr && (opt->flags & IMF_FLAG_PROFILE)) {
-        cudaEventCreate(&gr_e0);
-        cudaEventCreate(&gr_e1);
-        cudaEventRecord(gr_e0, s);
-    }
-    if (p.ws_gr) {  // f32: image-wide ranks of every plane's rows, before any tile
-        grank = (uint32_t*)(ws + kStatusBytes + p.lanes * p.ws_lane);
-        const long long n = (long long)p.gr_rows * p.g.W;
-        uint32_t* scratch = grank + (((size_t)n * p.g.B * p.g.C * 4 + 255) & ~(size_t)255) / 4;
-        Geom gg = p.g;
-        gg.src = src->data;
-        for (int b = 0; b < p.g.B; b++)
-            for (int c = 0; c < p.g.C; c++)
-                if (cudaError_t e = gr_rank_plane(gg, b, c, p.gr_y0, p.gr_y0 + p.gr_rows,
-                                                  grank + (size_t)(b * p.g.C + c) * n, scratch, s))
-                    return cuda_fail(e, "image ranks");
-    }
-    if (gr_e0) {
-        cudaEventRecord(gr_e1, s);
-        cudaEventSynchronize(gr_e1);
-        cudaEventElapsedTime(&gr_ms, gr_e0, gr_e1);
-        cudaEventDestroy(gr_e0);
-        cudaEventDestroy(gr_e1);
-    }
     if (!(opt->flags & IMF_FLAG_KEEP_STATUS))
         if (cudaError_t e = cudaMemsetAsync(status, 0, sizeof(int), s)) return cuda_fail(e, "status memset");
 
@@ -626,7 +590,7 @@ static int filter_impl(const imf_image* src, imf_image* dsts, int n, const int32
     g.src = src->data;
     g.ctab_g = nullptr;
     if (p.ws_ctab && p.ct_y1 > p.ct_y0) {
-        uint32_t* ct = (uint32_t*)(ws + kStatusBytes + p.lanes * p.ws_lane + p.ws_gr);
+        uint32_t* ct = (uint32_t*)(ws + kStatusBytes + p.lanes * p.ws_lane);
         if (cudaError_t e = cudaMemsetAsync(ct, 0, p.ws_ctab, s)) return cuda_fail(e, "coarse table memset");
         const long long rows = (long long)(p.ct_y1 - p.ct_y0) * g.B * g.C;
         const int cgrid = (int)std::min<long long>(296, (rows + 31) / 32);
@@ -635,13 +599,6 @@ static int filter_impl(const imf_image* src, imf_image* dsts, int n, const int32
         g_launches += 2;
         g.ctab_g = ct;
     }
-    if (grank) {
-        g.gr = grank;
-        g.gr_y0 = p.gr_y0;
-        g.gr_rows = p.gr_rows;
-        g.gr_shift = p.gr_shift;
-    }
-
     SelParams sp;
     memset(&sp, 0, sizeof(sp));
     sp.circle = kernel->shape_code == IMF_SHAPE_CIRCLE;
@@ -652,6 +609,10 @@ static int filter_impl(const imf_image* src, imf_image* dsts, int n, const int32
     sp.tmap = target_map;
     sp.G = p.G;
     sp.status = status;
+    // test hook: IMF_FLAG_DEBUG_DEFECT, or IMF_DEBUG_DEFECT=1 in the environment
+    // (reaches the hook through every entry point, the CLI included)
+    const int dbg_defect = (opt->flags & IMF_FLAG_DEBUG_DEFECT) || env_int("IMF_DEBUG_DEFECT", 0) ? 1 : 0;
+    sp.debug_defect = dbg_defect;
 
     static thread_local PairTab ptab;
     PairParams pp;
@@ -672,6 +633,7 @@ static int filter_impl(const imf_image* src, imf_image* dsts, int n, const int32
         pp.hs = p.hs;
         pp.grouped = p.k2_threads == 64 * p.G && p.g.Tw <= 64 && p.G <= 15 && env_int("IMF_GROUPED", 1);
         pp.status = status;
+        pp.debug_defect = dbg_defect;
     }
 
     // Optional per-kernel timing (opt->reserved[0] & 1): CUDA events recorded on
@@ -684,16 +646,14 @@ static int filter_impl(const imf_image* src, imf_image* dsts, int n, const int32
     cudaStream_t ls[2] = {s, nullptr};
     cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
     if (lanes == 2) {
-        static thread_local cudaStream_t lane2 = nullptr;
-        static thread_local int lane2_dev = -1;
+        // one lane-2 stream per (thread, device), created once and kept
+        static thread_local cudaStream_t lane2[kMaxDev] = {};
         int dev = 0;
-        cudaGetDevice(&dev);
-        if (lane2_dev != dev) {
-            if (cudaError_t e = cudaStreamCreateWithFlags(&lane2, cudaStreamNonBlocking))
+        if (cudaError_t e = cudaGetDevice(&dev)) return cuda_fail(e, "cudaGetDevice");
+        if (!lane2[dev])
+            if (cudaError_t e = cudaStreamCreateWithFlags(&lane2[dev], cudaStreamNonBlocking))
                 return cuda_fail(e, "lane stream");
-            lane2_dev = dev;
-        }
-        ls[1] = lane2;
+        ls[1] = lane2[dev];
         cudaEventCreateWithFlags(&fork_ev, cudaEventDisableTiming);
         cudaEventCreateWithFlags(&join_ev, cudaEventDisableTiming);
         cudaEventRecord(fork_ev, s);  // after the status memset
@@ -775,7 +735,6 @@ static int filter_impl(const imf_image* src, imf_image* dsts, int n, const int32
             g_prof.launches += 1;
         }
         for (cudaEvent_t e : ev) cudaEventDestroy(e);
-        g_prof.sort_ms += gr_ms;  // image ranks are part of the ordinal transform
         g_prof.tiles = p.total_tiles;
         g_prof.tile = p.g.Tw;
         g_prof.qs = p.pair ? 2 : (p.omg ? 1 : 0);
@@ -847,9 +806,8 @@ static bool rows_outermost(const imf_image* im) {
 namespace {
 struct HostStreams {
     cudaStream_t up = nullptr, down = nullptr, comp2 = nullptr;
-    int dev = -1;
 };
-thread_local HostStreams g_hs;
+thread_local HostStreams g_hs_dev[kMaxDev];  // per (thread, device), created once
 }  // namespace
 
 int imf_filter_host(const imf_image* src, imf_image* dst, const imf_kernel* kernel, int32_t target,
@@ -862,14 +820,20 @@ int imf_filter_host(const imf_image* src, imf_image* dst, const imf_kernel* kern
     int st = make_plan(src, kernel, opt, &p);
     if (st) return st;
     const int dsz = dtype_size(src->dtype);
+    if (src->stride_b < 0 || src->stride_y < 0 || src->stride_x < 0 || src->stride_c < 0 || dst->stride_b < 0 ||
+        dst->stride_y < 0 || dst->stride_x < 0 || dst->stride_c < 0)
+        return IMF_ERR_INVALID;
     const size_t sb = extent_bytes(src), db = extent_bytes(dst);
+    // results come back as whole byte ranges of dst: every byte of dst's extent
+    // must belong to one of its elements (dense layout, e.g. C-contiguous), or
+    // host bytes between elements would be overwritten
+    if ((size_t)dst->batch * dst->height * dst->width * dst->channels * dsz != db) return IMF_ERR_INVALID;
     const size_t tb = target_map ? (size_t)p.full_out_h * p.g.out_w * 4 : 0;
     int dev = 0;
     if (cudaGetDevice(&dev)) return IMF_ERR_CUDA;
-    if (g_hs.dev != dev) {
-        if (g_hs.up) cudaStreamDestroy(g_hs.up);
-        if (g_hs.down) cudaStreamDestroy(g_hs.down);
-        if (g_hs.comp2) cudaStreamDestroy(g_hs.comp2);
+    if (dev >= kMaxDev) return IMF_ERR_INVALID;
+    HostStreams& g_hs = g_hs_dev[dev];
+    if (!g_hs.up) {
         if (cudaStreamCreateWithFlags(&g_hs.up, cudaStreamNonBlocking) ||
             cudaStreamCreateWithFlags(&g_hs.down, cudaStreamNonBlocking) ||
             cudaStreamCreateWithFlags(&g_hs.comp2, cudaStreamNonBlocking))
@@ -881,7 +845,6 @@ int imf_filter_host(const imf_image* src, imf_image* dst, const imf_kernel* kern
             uint64_t thr = 4ull << 30;
             cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
         }
-        g_hs.dev = dev;
     }
     void *dsrc = nullptr, *ddst = nullptr, *dws = nullptr, *dws2 = nullptr, *dtm = nullptr;
     std::vector<cudaEvent_t> evs;
@@ -896,7 +859,12 @@ int imf_filter_host(const imf_image* src, imf_image* dst, const imf_kernel* kern
     // workspace) so one stripe's K1 fills the tail of the previous stripe's K2
     const bool two = env_int("IMF_STRIPE_LANES", 2) > 1;
     const int OH0 = p.full_out_h;
-    const bool pipe0 = rows_outermost(src) && rows_outermost(dst) && OH0 > 2 * p.g.Th;
+    // output rows [R0, R1) (opt->row_begin/row_end: one device's stripe of a
+    // multi-device job; the other rows of dst are left untouched)
+    const bool ranged = opt->row_end > 0;
+    const int R0 = ranged ? opt->row_begin : 0, R1 = ranged ? opt->row_end : OH0;
+    const bool pipe0 = rows_outermost(src) && rows_outermost(dst) && (ranged || OH0 > 2 * p.g.Th);
+    if (ranged && !pipe0) return IMF_ERR_INVALID;  // row ranges need row-outermost layouts
     // batches stream through a ring of two device image slots (image b in slot
     // b % 2, reused once image b - 2 is downloaded): device memory and the
     // per-call allocation stay two images deep however long the batch
@@ -922,9 +890,9 @@ int imf_filter_host(const imf_image* src, imf_image* dst, const imf_kernel* kern
     // after the last filter), and 8 middle stripes; consecutive stripes run on
     // alternating compute streams, so each stripe's K1 fills the previous
     // stripe's K2 tail (c2: 2.60 ms host->host vs 2.53 ms device-resident).
-    std::vector<int> cuts{0};
+    std::vector<int> cuts{0};  // in tile rows from R0, then output rows
     if (pipe) {
-        const int tiles_y = (OH + p.g.Th - 1) / p.g.Th;
+        const int tiles_y = (R1 - R0 + p.g.Th - 1) / p.g.Th;
         const int edge = std::max(1, env_int("IMF_STRIPE_EDGE", 1));
         const int mid = std::max(1, env_int("IMF_STRIPE_MID", 8));
         if (tiles_y <= 2 * edge + 1) {
@@ -935,7 +903,7 @@ int imf_filter_host(const imf_image* src, imf_image* dst, const imf_kernel* kern
             for (int i = 1; i <= mid; i++) cuts.push_back(edge + (int)((long long)body * i / mid));
             cuts.push_back(tiles_y);
         }
-        for (int& c : cuts) c = std::min(OH, c * p.g.Th);
+        for (int& c : cuts) c = std::min(R1, R0 + c * p.g.Th);
         cuts.erase(std::unique(cuts.begin(), cuts.end()), cuts.end());
     } else {
         cuts.push_back(OH);
@@ -951,7 +919,8 @@ int imf_filter_host(const imf_image* src, imf_image* dst, const imf_kernel* kern
             const int slot = ring ? bi % nslot : bi;
             const long long sdev = (long long)slot * src->stride_b, ddev = (long long)slot * dst->stride_b;
             if (ring && slot_free[slot]) cudaStreamWaitEvent(g_hs.up, slot_free[slot], 0);
-            int up_hi = 0;  // input rows [0, up_hi) of image bi are uploaded
+            // input rows [first row the stripe reads, up_hi) of image bi are uploaded
+            int up_hi = std::max(0, std::min(H, R0 + vshift - r));
             for (size_t si = 0; si + 1 < cuts.size() && !rc; si++) {
                 const int y0 = cuts[si], y1 = cuts[si + 1];
                 if (pipe) {

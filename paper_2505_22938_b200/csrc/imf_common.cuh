@@ -37,8 +37,6 @@ struct Geom {
     int fp, fpR2;                  // fp: only pixels within dist^2 <= fpR2 of the output rect are ranked
     int run_min;                   // bucket K1: copy groups (replicate boundary) this large rank as one run
     const uint32_t* ctab_g;        // f32 bucket K1: call-wide fine-bucket table (k_coarse_*), or nullptr
-    const uint32_t* gr;            // f32: image-wide ranks (imf_grank.cu) replace the keys, or nullptr
-    int gr_y0, gr_rows, gr_shift;  // rows [gr_y0, gr_y0 + gr_rows) of every plane; key = rank << gr_shift
     int tiles_x, tiles_y;
     long long tile_begin;          // first tile of this launch (chunking)
     unsigned mx, my, mc;           // division magics: n / d == (n * m) >> s for n < 2^31 (host: set_magic)
@@ -69,6 +67,7 @@ struct SelParams {
     const int* tmap;     // per-pixel target ranks [out_h*out_w] or nullptr
     int G;               // seed rows per tile
     int* status;         // device status word (1 = scan defect)
+    int debug_defect;    // test hook (IMF_FLAG_DEBUG_DEFECT): corrupt one slide count in tile 0
 };
 
 __device__ __forceinline__ TileCoord tile_coord(const Geom& g, long long t64) {
@@ -124,12 +123,10 @@ __device__ __forceinline__ uint32_t float_key(uint32_t u) {
 }
 
 // u32 order key of f32 image pixel (yy, xx) (clamped image coordinates): the
-// float key (ordinal.py:109-123), or its image-wide rank when g.gr is set.
+// float key (ordinal.py:109-123).
 __device__ __forceinline__ uint32_t f32_key(const Geom& g, const TileCoord& tc, int yy, int xx) {
     if (g.dtype == DT_U16)  // bucket transform on u16 tiles: the value in the high half
         return (uint32_t)__ldg((const uint16_t*)tc.src + (long long)yy * g.s_y + (long long)xx * g.s_x) << 16;
-    if (g.gr)
-        return __ldg(g.gr + ((long long)(tc.b * g.C + tc.c) * g.gr_rows + (yy - g.gr_y0)) * g.W + xx) << g.gr_shift;
     return float_key(__ldg((const uint32_t*)tc.src + (long long)yy * g.s_y + (long long)xx * g.s_x));
 }
 

@@ -9,14 +9,10 @@
 // compare-exchanges, padded with 0xffffffff keys that sort last), and outputs
 // the key of rank t decoded back to the value (core.py:366: the t-th smallest
 // of the window multiset -- the definition, oracle.py:88-121).
-#include "imf_common.cuh"
+#include "imf_kernels.cuh"
 
 namespace imf {
 
-struct DirectTab {
-    int area;
-    int off[32];  // window offsets dy * Sw + dx relative to the window centre
-};
 
 __device__ __forceinline__ void cx_swap(uint32_t& a, uint32_t& b, bool up) {
     const uint32_t lo = min(a, b), hi = max(a, b);

@@ -29,41 +29,9 @@
 // Layout (shared memory): omega (rank -> x | y << 8, 8 sentinel entries each
 // side, 16-byte aligned so rank 8k starts a 16-byte chunk), then the ordinal
 // image I (u16 rank per input-tile pixel, row stride Sw), then per-window state.
-#include "imf_common.cuh"
+#include "imf_kernels.cuh"
 
 namespace imf {
-
-// Membership test families of the pair kernel (template parameter SHAPE).
-constexpr int SH_SPAN = 0;    // any convex kernel: per-row span table (kernels.py:127-182)
-constexpr int SH_CIRCLE = 1;  // 4(dx^2+dy^2) <= (2r+1)^2 (kernels.py:70-71), packed bytes + IDP.4A
-constexpr int SH_SQUARE = 2;  // |dx|, |dy| <= r (kernels.py:72-73), packed 16-bit range tests
-constexpr int SH_POLY = 3;    // any convex kernel, per-row range constants looked up by dy byte
-constexpr int SH_CIRCLEW = 4; // circle, any tile (T + r > 128): unsigned-byte IDP.4A on x, y (see test8)
-
-constexpr int PT_MAX = 250;  // >= kernel rows / columns (2r+1, r <= 124)
-
-// Byte offsets into I relative to a window pair's base 2*(row*Sw + 2q), in
-// the constant bank.  Every list holds its 4-byte-aligned entries first; the
-// rest ("odd") store the offset of the aligned word BEFORE the pixel pair.
-struct PairTab {
-    int2 v[PT_MAX];  // per kernel column: (enter, exit) of a down slide
-    int he[PT_MAX];  // per kernel row: pixel entering on a right slide
-    int hx[PT_MAX];  // per kernel row: pixel exiting on a right slide
-    int span[PT_MAX];  // per dy + r: (xlo & 0xffff) | width << 16 (kernels.py:127-182 rows)
-};
-
-struct PairParams {
-    int shape;       // SH_*: membership test family (packed ones require T + r <= 128)
-    int R2p1;        // r(r+1) + 1
-    int nv, nv_even;
-    int nh, nhe_even, nhx_even;
-    int target;
-    const int* tmap;
-    int G;
-    int grouped;     // phase C+D per seed-row group (named barriers), needs 64 threads per group
-    int hs;          // 1: I holds rank >> 1 (tiles with 32768 < N <= 65536), pivots even
-    int* status;
-};
 
 __device__ __forceinline__ uint32_t lds32(uint32_t a) {
     uint32_t v;
@@ -874,6 +842,8 @@ __global__ void __launch_bounds__(512, 2) k2_pair(Geom g, PairParams p, const __
             store_out(g, wb);
             cA += dA;
             cB += dB;
+            // test hook: an inconsistent count (core.py:31-36 defect path)
+            if (p.debug_defect && blockIdx.x == 0 && g.tile_begin == 0 && u == 0 && s == 0) cA += 1 << 20;
             const int tA = target_at2(g, p, tc, row, j0);
             const int tB = target_at2(g, p, tc, row, j1);
             int mA, mB;

@@ -29,7 +29,7 @@
 // The refine walks omega from the pivot toward the target rank testing
 // membership of each rank's pixel in the window (ordinal.py:175-199): eight
 // ranks per step per thread (phase C/D) or sixty-four per warp step (A/B).
-#include "imf_common.cuh"
+#include "imf_kernels.cuh"
 
 namespace imf {
 
@@ -363,6 +363,8 @@ __global__ void __launch_bounds__(512) k2_select(Geom g, SelParams p, const __gr
         for (int step = 0; step < nsteps; step++) {
             if (down) {
                 cnt += slide_delta(Ic + (row + r) * rowB, vtab, p.ncols, P, false);
+                // test hook: an inconsistent count (core.py:31-36 defect path)
+                if (p.debug_defect && blockIdx.x == 0 && g.tile_begin == 0 && u == 0 && step == 0) cnt += 1 << 20;
                 row++;
             } else {
                 cnt += slide_delta(Ic + (row + r - 1) * rowB, vtab, p.ncols, P, true);

@@ -20,7 +20,7 @@
 // per-CTA global scratch slot (L2-resident) -- same code, GMEM=true.
 #include <algorithm>
 
-#include "imf_common.cuh"
+#include "imf_kernels.cuh"
 
 namespace imf {
 
@@ -563,10 +563,8 @@ constexpr unsigned long long kMaxSumSq = 64ull << 20;
 // 65536), splitting it on the next l_c key bits.  A fine bucket then spans
 // <= 2^16 keys (l_c >= 4), so the entry's low 16 key bits still order it, and
 // holds ~2 N / 65536 keys.  tab[c]: coarse count in, base | l_c << 16 out.
-constexpr int kCoarse = 4096;
 // Below this many tile pixels the top-16-bit buckets are already small and the
 // coarse pass (4096-bin atomics, allocation scan) costs more than it saves.
-constexpr int kAdaptiveMinN = 16384;
 
 __device__ void coarse_alloc(uint32_t* tab, int N) {
     __shared__ int s_pop;
@@ -678,8 +676,6 @@ __device__ __forceinline__ void rep_axis(int X0, int x, int S, int W, int& cnt, 
 // 255).  Ranking orders slots by (entry | 1, slot): the interior of a run then
 // compares exactly like its head, so a bucket scan counts a whole run with
 // plain compares (no data-dependent skip), and only the head's thread ranks it.
-constexpr int kRunMin = 1024;
-constexpr int kRunMinFloor = 2;
 constexpr int kRunList = 64;   // runs per tile without a side array
 // Runs longer than kMarkSelf are LONG: listed (RunList::mark), their interior
 // written by the CTA, and skipped whole by bucket scans (a corner run of

@@ -17,7 +17,8 @@ one on the hot path.
 
 from __future__ import annotations
 
-from dataclasses import dataclass
+import threading
+from dataclasses import dataclass, replace
 
 import numpy as np
 
@@ -84,6 +85,13 @@ def filter_stripe(image: np.ndarray, params, stripe: Stripe, filter_fn=None) -> 
             shp[1] -= 2 * params.shape.radius
         return np.empty(shp, image.dtype)
     sub = image[stripe.in_y0:stripe.in_y1]
+    pct = params.percentile
+    if not (np.isscalar(pct) or np.ndim(pct) == 0):
+        # a per-pixel map covers the full output: give the stripe its own rows
+        # (replicate: the sub-image's output rows are input rows in_y0..in_y1;
+        # valid: exactly the stripe's rows)
+        lo, hi = (stripe.y0, stripe.y1) if params.boundary == "valid" else (stripe.in_y0, stripe.in_y1)
+        params = replace(params, percentile=np.asarray(pct)[lo:hi])
     out = filter_fn(sub, params)
     if params.boundary == "valid":
         return out
@@ -95,3 +103,68 @@ def assemble(stripes: list[Stripe], parts: list[np.ndarray]) -> np.ndarray:
     """Concatenate per-rank stripe outputs in row order."""
     order = sorted(range(len(stripes)), key=lambda i: stripes[i].y0)
     return np.concatenate([parts[i] for i in order], axis=0)
+
+
+def filter_multi(images, params, devices=None, *, batched: bool = False, out=None):
+    """Filter host images on several GPUs from ONE process (no collective).
+
+    `images`: a host array (H, W[, C]), or (B, H, W[, C]) with `batched`.
+    Work is split as SURVEY.md 8(e) plans it: whole images per device when the
+    batch has at least as many images as devices (contiguous blocks, zero halo
+    overhead), else output-row stripes of each image, each device uploading
+    only the input rows its stripe reads (imf_filter_host with a row range).
+    One host thread per device drives that device's streams through the C-ABI
+    host entry (the GIL is released inside the call); results land in
+    disjoint parts of one host output.  `devices` defaults to every visible
+    GPU; a device may be listed twice (two pipelines on one GPU).
+    """
+    import torch
+
+    from .tiling import _check_dtype, _validate_plane, run_host
+
+    a = images.numpy() if isinstance(images, torch.Tensor) else np.asarray(images)
+    a = np.ascontiguousarray(a)
+    _check_dtype(a.dtype)
+    plane = a.shape[1:3] if batched else a.shape[:2]
+    kernel, (out_h, out_w) = _validate_plane(tuple(plane), a.dtype,
+                                             lambda: bool(np.isnan(a).any()), params)
+    if devices is None:
+        devices = list(range(torch.cuda.device_count()))
+    devices = list(devices)
+    if not devices:
+        raise RuntimeError("filter_multi needs at least one CUDA device (no CPU fallback)")
+    oshape = list(a.shape)
+    hy = 1 if batched else 0
+    oshape[hy], oshape[hy + 1] = out_h, out_w
+    o = np.empty(oshape, dtype=a.dtype) if out is None else out
+    jobs = [[] for _ in devices]  # per worker (= entry of `devices`): run_host kwargs
+    nb = a.shape[0] if batched else 1
+    if batched and nb >= len(devices):
+        cuts = [nb * i // len(devices) for i in range(len(devices) + 1)]
+        for w, (b0, b1) in enumerate(zip(cuts[:-1], cuts[1:])):
+            jobs[w].append(dict(image=a[b0:b1], out=o[b0:b1], batched=True))
+    else:
+        for w, st in enumerate(stripe_plan(a.shape[hy], params.shape.radius, params.boundary,
+                                           len(devices))):
+            for b in range(nb if st.rows else 0):
+                src, dst = (a[b], o[b]) if batched else (a, o)
+                jobs[w].append(dict(image=src, out=dst, rows=(st.y0, st.y1)))
+    errors = []
+
+    def worker(dev, lst):
+        try:
+            with torch.cuda.device(dev):
+                for kws in lst:
+                    run_host(kws.pop("image"), params, kernel=kernel, **kws)
+                torch.cuda.synchronize()
+        except BaseException as e:  # re-raised in the caller
+            errors.append(e)
+
+    threads = [threading.Thread(target=worker, args=(d, lst)) for d, lst in zip(devices, jobs) if lst]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    if errors:
+        raise errors[0]
+    return o

@@ -64,17 +64,65 @@ class FilterParams:
 
 
 @dataclass(frozen=True)
+class Tile:
+    """One tile of the reference schedule (tiling.py:46-78): an output
+    rectangle and the padded-input rectangle it reads (one extra row above
+    when seeded by the tile above).  The GPU picks its own tiles (output is
+    tile-invariant); this is the reference-facing description."""
+
+    out_x0: int
+    out_y0: int
+    out_w: int
+    out_h: int
+    seeded: bool
+    radius: int
+
+    @property
+    def in_x0(self) -> int:
+        return self.out_x0
+
+    @property
+    def in_y0(self) -> int:
+        return self.out_y0 - int(self.seeded)
+
+    @property
+    def in_w(self) -> int:
+        return self.out_w + 2 * self.radius
+
+    @property
+    def in_h(self) -> int:
+        return self.out_h + 2 * self.radius + int(self.seeded)
+
+
+@dataclass(frozen=True)
 class TileGrid:
-    """Reference-compatible tile grid summary (tiling.py:81-91)."""
+    """Reference tile grid (tiling.py:81-91): columns of tiles, top to bottom."""
 
     out_h: int
     out_w: int
     tile_size: int
+    columns: list
     forwarding: bool
+
+    @property
+    def tiles(self) -> list:
+        return [t for col in self.columns for t in col]
 
 
 def decompose(image_shape: tuple[int, int], params: FilterParams) -> TileGrid:
-    """Validate radius / output size / tile size like tiling.py:94-131."""
+    """The reference's tile grid with its validation (tiling.py:94-131)."""
+    h, w, t = _grid_size(image_shape, params)
+    r = params.shape.radius
+    fw = params.forwarding
+    columns = [[Tile(out_x0=x0, out_y0=y0, out_w=min(t, w - x0), out_h=min(t, h - y0),
+                     seeded=fw and y0 > 0, radius=r) for y0 in range(0, h, t)]
+               for x0 in range(0, w, t)]
+    return TileGrid(out_h=h, out_w=w, tile_size=t, columns=columns, forwarding=fw)
+
+
+def _grid_size(image_shape, params: FilterParams):
+    """(out_h, out_w, tile) after the reference checks (tiling.py:94-131), in
+    its order and with its messages; no Tile objects (host prologue)."""
     r = params.shape.radius
     if r > MAX_RADIUS:
         raise ValueError(
@@ -98,7 +146,7 @@ def decompose(image_shape: tuple[int, int], params: FilterParams) -> TileGrid:
                 f"{MAX_TILE_SIDE}-pixel input tile cap")
     else:
         t = min(DEFAULT_OUTPUT_TILE, MAX_TILE_SIDE - 2 * r - seed_extra)
-    return TileGrid(out_h=h, out_w=w, tile_size=t, forwarding=params.forwarding)
+    return h, w, t
 
 
 def pad_image(image: np.ndarray, r: int, mode: str) -> np.ndarray:
@@ -179,19 +227,29 @@ def _target_spec(area: int, percentile, out_shape, device, host: bool = False):
 
 
 class _Workspace:
-    """Per-device cached workspace (grown on demand)."""
+    """Cached device workspace per (device, stream), grown on demand.
+
+    The workspace holds the omega scratch and the status word of a call, so
+    two calls in flight on different streams must not share one: the cache
+    key includes the stream.  A buffer is allocated on (and only ever used
+    by) its own stream, so the caching allocator's stream tracking is exact.
+    """
 
     def __init__(self):
         self.buf = {}
         self.lock = threading.Lock()
 
-    def get(self, device, nbytes: int):
+    def get(self, device, nbytes: int, stream=None):
         torch = _torch()
-        key = device.index if device.index is not None else torch.cuda.current_device()
+        idx = device.index if device.index is not None else torch.cuda.current_device()
+        if stream is None:
+            stream = torch.cuda.current_stream(idx)
+        key = (idx, stream.cuda_stream)
         with self.lock:
             cur = self.buf.get(key)
             if cur is None or cur.numel() < nbytes:
-                cur = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=device)
+                with torch.cuda.stream(stream):
+                    cur = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=torch.device("cuda", idx))
                 self.buf[key] = cur
             return cur
 
@@ -199,9 +257,10 @@ class _Workspace:
 _WS = _Workspace()
 
 
-def workspace_for(device):
-    """The cached device workspace (holds the status word of the last call)."""
-    return _WS.get(device, 1)
+def workspace_for(device, stream=None):
+    """The cached device workspace of (device, stream) (holds the status word
+    of the last call on that stream)."""
+    return _WS.get(device, 1, stream)
 
 
 def _kernel_struct(kernel):
@@ -238,6 +297,12 @@ def run_device(src, params: FilterParams, out=None, *, batched: bool = False, st
     the target map; this is the device half of :func:`filter_image`.
     """
     torch = _torch()
+    with torch.cuda.device(src.device):  # streams, workspace and launches on src's device
+        return _run_device(src, params, out, batched, stream, check, kernel, profile)
+
+
+def _run_device(src, params, out, batched, stream, check, kernel, profile):
+    torch = _torch()
     L = _lib.lib()
     dt = _np_dtype_of(src)
     dt_code = _DTYPES[dt]
@@ -247,13 +312,25 @@ def run_device(src, params: FilterParams, out=None, *, batched: bool = False, st
     h, w = src.shape[1:3] if batched else src.shape[0:2]
     valid = params.boundary == "valid"
     out_h, out_w = (h - 2 * r, w - 2 * r) if valid else (h, w)
+    hy = 1 if batched else 0
+    oshape = list(src.shape)
+    oshape[hy], oshape[hy + 1] = out_h, out_w
     if out is None:
-        oshape = list(src.shape)
-        hy = 1 if batched else 0
-        oshape[hy], oshape[hy + 1] = out_h, out_w
         out = torch.empty(oshape, dtype=src.dtype, device=src.device)
+    elif out.dtype != src.dtype or list(out.shape) != oshape or out.device != src.device:
+        raise ValueError(f"out must be a {src.dtype} tensor of shape {tuple(oshape)} on {src.device}")
+    cur = torch.cuda.current_stream(src.device)
+    if stream is None:
+        stream = cur
     target, tmap, tmin, tmax = _target_spec(kernel.area, params.percentile, (out_h, out_w),
                                             src.device)
+    if stream.cuda_stream != cur.cuda_stream:
+        # src / out / the target map were produced on the current stream: order
+        # the launch after them, and keep their memory alive until `stream` is done
+        stream.wait_stream(cur)
+        for t in (src, out, tmap):
+            if t is not None:
+                t.record_stream(stream)
     ks, keep = _kernel_struct(kernel)
     simg = _image_struct(src, dt_code, batched, has_c)
     dimg = _image_struct(out, dt_code, batched, has_c)
@@ -263,9 +340,7 @@ def run_device(src, params: FilterParams, out=None, *, batched: bool = False, st
     need = L.imf_workspace_size(ctypes.byref(simg), ctypes.byref(ks), ctypes.byref(opt))
     if need == 0:
         raise ValueError("unsupported filter geometry for the CUDA engine")
-    ws = _WS.get(src.device, need)
-    if stream is None:
-        stream = torch.cuda.current_stream(src.device)
+    ws = _WS.get(src.device, need, stream)
     sptr = ctypes.c_void_p(stream.cuda_stream)
     st = L.imf_filter(ctypes.byref(simg), ctypes.byref(dimg), ctypes.byref(ks), target,
                       None if tmap is None else tmap.data_ptr(), tmin, tmax, ctypes.byref(opt),
@@ -291,16 +366,16 @@ def _validate_plane(shape2d, dt, has_nan, params: FilterParams):
         raise ValueError("image contains NaN; NaN has no rank under the "
                          "total order used by this filter")
     kernel = make_kernel(params.shape)
-    grid = decompose(tuple(shape2d), params)
+    out_h, out_w, _ = _grid_size(tuple(shape2d), params)
     if params.boundary == "valid":
         pad_image_check(shape2d, params.shape.radius)
     if not (np.isscalar(params.percentile) or np.ndim(params.percentile) == 0):
         pshape = tuple(np.shape(params.percentile))
-        if pshape != (grid.out_h, grid.out_w):
+        if pshape != (out_h, out_w):
             raise ValueError(
                 f"percentile map shape {pshape} does not match the output "
-                f"shape {(grid.out_h, grid.out_w)}")
-    return kernel, grid
+                f"shape {(out_h, out_w)}")
+    return kernel, (out_h, out_w)
 
 
 def pad_image_check(shape2d, r):
@@ -355,7 +430,7 @@ def _host_image_struct(a: np.ndarray, dt_code: int, batched: bool):
 
 
 def run_host(image, params: FilterParams, out=None, *, batched: bool = False, kernel=None,
-             stream=None) -> np.ndarray:
+             stream=None, rows=None) -> np.ndarray:
     """Filter a HOST array through the C-ABI host entry point (imf_filter_host).
 
     The extension uploads, filters and downloads in output-row stripes on
@@ -363,6 +438,8 @@ def run_host(image, params: FilterParams, out=None, *, batched: bool = False, ke
     (include/isomedian_b200.h).  `image` may be a numpy array or a CPU torch
     tensor (pinned memory gives full copy bandwidth); the result is a numpy
     array (or `out`, a host array/tensor of the output shape, filled in place).
+    `rows=(y0, y1)` filters output rows [y0, y1) only (the other rows of `out`
+    are left as they are): one device's stripe of a multi-device job.
     """
     torch = _torch()
     L = _lib.lib()
@@ -377,18 +454,32 @@ def run_host(image, params: FilterParams, out=None, *, batched: bool = False, ke
     hy = 1 if batched else 0
     h, w = a.shape[hy], a.shape[hy + 1]
     out_h, out_w = (h - 2 * r, w - 2 * r) if valid else (h, w)
+    oshape = list(a.shape)
+    oshape[hy], oshape[hy + 1] = out_h, out_w
+    stage = None
     if out is None:
-        oshape = list(a.shape)
-        oshape[hy], oshape[hy + 1] = out_h, out_w
         o = np.empty(oshape, dtype=a.dtype)
     else:
         o = out.numpy() if _is_tensor(out) else out
+        if not isinstance(o, np.ndarray) or o.dtype != a.dtype or list(o.shape) != oshape:
+            raise ValueError(f"out must be a {a.dtype} host array of shape {tuple(oshape)}")
+        if not o.flags.c_contiguous:
+            # the C ABI copies results back as whole row ranges (dense dst only):
+            # filter into a dense buffer, then scatter into the caller's view
+            stage, o = o, np.empty(oshape, dtype=a.dtype)
     target, tmap, tmin, tmax = _target_spec(kernel.area, params.percentile, (out_h, out_w), None,
                                             host=True)
     ks, keep = _kernel_struct(kernel)
     simg = _host_image_struct(a, dt_code, batched)
     dimg = _host_image_struct(o, dt_code, batched)
     opt = _lib.ImfOptions(1 if valid else 0, int(params.tile_size or 0), 0, 0)
+    if rows is not None:
+        y0, y1 = int(rows[0]), int(rows[1])
+        if not 0 <= y0 < y1 <= out_h:
+            raise ValueError(f"row range {rows} outside the {out_h} output rows")
+        if stage is not None:  # rows outside the range must keep the caller's values
+            np.copyto(o, stage)
+        opt.row_begin, opt.row_end = y0, y1
     if stream is None:
         stream = torch.cuda.current_stream()
     st = L.imf_filter_host(ctypes.byref(simg), ctypes.byref(dimg), ctypes.byref(ks), target,
@@ -400,6 +491,8 @@ def run_host(image, params: FilterParams, out=None, *, batched: bool = False, ke
                               "pivot/count state was inconsistent")
     if st != _lib.IMF_OK:
         raise RuntimeError(f"imf_filter_host failed: {_lib.strerror(st)}")
+    if stage is not None:
+        np.copyto(stage, o)
     return out if out is not None else o
 
 
@@ -457,11 +550,20 @@ def filter_image_bracket(image, params: FilterParams, percentiles) -> list:
         src = image if image.is_cuda else image.to("cuda")
     else:
         src = torch.from_numpy(np.ascontiguousarray(image)).to("cuda")
+    with torch.cuda.device(src.device):
+        outs = _bracket_device(src, dt, kernel, grid, params, percentiles)
+    if is_t:
+        return outs if image.is_cuda else [o.cpu() for o in outs]
+    return [o.cpu().numpy() for o in outs]
+
+
+def _bracket_device(src, dt, kernel, out_hw, params, percentiles):
+    torch = _torch()
     L = _lib.lib()
     dt_code = _DTYPES[dt]
     has_c = src.dim() == 3
     oshape = list(src.shape)
-    oshape[0], oshape[1] = grid.out_h, grid.out_w
+    oshape[0], oshape[1] = out_hw
     outs = [torch.empty(oshape, dtype=src.dtype, device=src.device) for _ in percentiles]
     targets = (ctypes.c_int32 * len(percentiles))(*[target_rank(kernel.area, float(p))
                                                    for p in percentiles])
@@ -472,8 +574,9 @@ def filter_image_bracket(image, params: FilterParams, percentiles) -> list:
     need = L.imf_workspace_size(ctypes.byref(simg), ctypes.byref(ks), ctypes.byref(opt))
     if need == 0:
         raise ValueError("unsupported filter geometry for the CUDA engine")
-    ws = _WS.get(src.device, need)
-    sptr = ctypes.c_void_p(torch.cuda.current_stream(src.device).cuda_stream)
+    stream = torch.cuda.current_stream(src.device)
+    ws = _WS.get(src.device, need, stream)
+    sptr = ctypes.c_void_p(stream.cuda_stream)
     st = L.imf_filter_bracket(ctypes.byref(simg), dimgs, len(outs), targets, ctypes.byref(ks),
                               ctypes.byref(opt), ws.data_ptr(), ws.numel(), sptr)
     if st != _lib.IMF_OK:
@@ -483,6 +586,4 @@ def filter_image_bracket(image, params: FilterParams, percentiles) -> list:
         raise ScanDefectError("segment scan exhausted while solving tile; "
                               "pivot/count state was inconsistent")
     del keep
-    if is_t:
-        return outs if image.is_cuda else [o.cpu() for o in outs]
-    return [o.cpu().numpy() for o in outs]
+    return outs

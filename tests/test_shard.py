@@ -70,3 +70,52 @@ def test_gloo_world2_stripes():
     for p in procs:
         p.join(timeout=60)
     assert np.array_equal(out, _oracle_fn(img, FilterParams(shape=ShapeSpec("circle", 6))))
+
+
+@pytest.mark.parametrize("boundary", ["replicate", "valid"])
+def test_stripes_with_percentile_map(boundary):
+    """A per-pixel percentile map of the FULL output shape (SPEC Fig. 12) is
+    sliced to each stripe's rows (tiling.py:165-177 map -> targets)."""
+    rng = np.random.default_rng(17)
+    img = rng.integers(0, 256, (45, 31)).astype(np.uint8)
+    r = 3
+    oh = 45 - 2 * r if boundary == "valid" else 45
+    ow = 31 - 2 * r if boundary == "valid" else 31
+    pmap = rng.random((oh, ow))
+    params = FilterParams(shape=ShapeSpec("circle", r), percentile=pmap, boundary=boundary)
+    plan = stripe_plan(img.shape[0], r, boundary, 3)
+    parts = [filter_stripe(img, params, s, _oracle_fn) for s in plan]
+    assert np.array_equal(assemble(plan, parts), _oracle_fn(img, params))
+
+
+def _gpu_worker(rank, world, port, img, q):
+    """One rank of a gloo job filtering its stripe with the CUDA engine."""
+    import torch
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(rank % torch.cuda.device_count())
+    params = FilterParams(shape=ShapeSpec("circle", 7))
+    plan = stripe_plan(img.shape[0], 7, "replicate", world)
+    part = filter_stripe(img, params, plan[rank])  # default: the GPU filter_image
+    parts = [None] * world
+    dist.all_gather_object(parts, part)
+    if rank == 0:
+        q.put(assemble(plan, parts))
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_gloo_world2_gpu_stripes():
+    """Two ranks, each filtering its row stripe on the GPU (cuda:rank mod
+    #devices), stitched on rank 0 == the whole-image reference result."""
+    img = np.random.default_rng(6).integers(0, 65536, (203, 171, 3)).astype(np.uint16)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gpu_worker, args=(r, 2, port, img, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=120)
+    assert np.array_equal(out, _oracle_fn(img, FilterParams(shape=ShapeSpec("circle", 7))))
