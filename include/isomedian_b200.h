@@ -154,6 +154,12 @@ uint64_t imf_launch_count(void);        /* kernels launched by this process (dia
 int imf_profile_last(float* sort_ms, float* select_ms, int32_t* launches, int64_t* tiles,
                      int32_t* tile_side, int32_t* qshift);
 
+/* Kernel paths the last imf_filter / imf_filter_bracket on this thread took
+ * (diagnostic): IMF_FEATURE_K1_TMA = the ordinal transform loaded its tile
+ * boxes with TMA (cp.async.bulk.tensor). */
+#define IMF_FEATURE_K1_TMA 1u
+uint32_t imf_last_features(void);
+
 /* Measured int32 add throughput of the current device (ops/s): the
  * denominator of the selection kernel's integer roofline. */
 int imf_int_peak(double* ops_per_s, double* ms);

@@ -25,7 +25,7 @@ IMF_ERR_UNSUPPORTED = 5
 EXPORTED = ("imf_workspace_size", "imf_filter", "imf_filter_bracket", "imf_workspace_status",
             "imf_filter_host",
             "imf_strerror", "imf_version", "imf_last_error", "imf_launch_count",
-            "imf_profile_last", "imf_int_peak")
+            "imf_profile_last", "imf_int_peak", "imf_last_features")
 
 _i32p = ctypes.POINTER(ctypes.c_int32)
 
@@ -54,6 +54,7 @@ class ImfOptions(ctypes.Structure):
                 ("row_end", ctypes.c_int32), ("reserved", ctypes.c_int32)]
 
 IMF_FLAG_PROFILE = 1
+IMF_FEATURE_K1_TMA = 1
 
 
 _lock = threading.Lock()
@@ -93,6 +94,8 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.imf_profile_last.restype = ctypes.c_int
     lib.imf_int_peak.argtypes = [P(ctypes.c_double), P(ctypes.c_double)]
     lib.imf_int_peak.restype = ctypes.c_int
+    lib.imf_last_features.argtypes = []
+    lib.imf_last_features.restype = ctypes.c_uint32
     return lib
 
 

@@ -20,8 +20,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OBJ = os.path.join(HERE, "build")
 LIB = os.path.join(HERE, "libisomedian_b200.so")
-SOURCES = ["imf_sort.cu", "imf_pair.cu", "imf_select.cu", "imf_direct.cu", "imf_api.cu", "imf_peak.cu"]
-HEADERS = ["imf_common.cuh", "imf_kernels.cuh", os.path.join("..", "..", "include", "isomedian_b200.h")]
+SOURCES = ["imf_sort.cu", "imf_count.cu", "imf_pair.cu", "imf_select.cu", "imf_direct.cu", "imf_api.cu", "imf_peak.cu"]
+HEADERS = ["imf_common.cuh", "imf_kernels.cuh", "imf_k1.cuh", os.path.join("..", "..", "include", "isomedian_b200.h")]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

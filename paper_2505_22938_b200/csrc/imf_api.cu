@@ -25,6 +25,7 @@ struct ProfileRec {
     int tile = 0, qs = 0;
 };
 static thread_local ProfileRec g_prof;
+static thread_local bool g_last_tma = false;  // the last call's K1 loaded its tiles with TMA (diagnostic)
 
 static int cuda_fail(cudaError_t e, const char* where) {
     snprintf(g_err, sizeof(g_err), "%s: %s", where, cudaGetErrorString(e));
@@ -36,7 +37,8 @@ namespace {
 constexpr size_t kSmemMax = 227 * 1024 - 1024;  // B200 opt-in 232448 B minus static smem headroom
 constexpr int kK1Threads = 1024;      // k1_count (latency-bound: more warps)
 constexpr int kK1SortThreads = 512;   // k1_sort (per-warp digit counters)
-constexpr size_t kStatusBytes = 256;
+constexpr size_t kStatusBytes = 2048;    // status word at 0, footprint row table at kFpOffset
+constexpr size_t kFpOffset = 256;        // 256 rows x 4 B
 constexpr size_t kOmegaScratchTarget = 96ull << 20;  // stays mostly L2-resident
 
 struct Plan {
@@ -56,6 +58,8 @@ struct Plan {
     size_t ws_omega, ws_k1g, ws_flags, ws_lane, ws_ctab, ws_total;
     int ct_y0, ct_y1;  // rows of every plane the call reads (call-wide coarse table)
     int lanes;  // chunk streams (1 or 2)
+    uint32_t fprow[256];  // footprint rows (g.fp): lo | hi << 16 per input-tile row
+    bool k1_tma;          // k1_count_reg loads its tile box with TMA (planar layouts)
 };
 
 int env_int(const char* name, int dflt) {
@@ -253,25 +257,37 @@ int make_plan(const imf_image* src, const imf_kernel* k, const imf_options* opt,
     // = 6 B per pixel when it needs one)
     if (p.k1_f32b_g) p.k1_gs_per_tile = std::max(p.k1_gs_per_tile, (size_t)6 * g.Npad);  // + run descriptors
 
-    // Rounded-rect footprint (pair path, circle kernels, register-resident K1):
-    // rank only input pixels within distance^2 r(r+1) of the output rectangle
-    // -- the union of the tile's windows -- so omega is shorter and denser.
+    // Tile footprint (pair path, register-resident K1): rank only the input
+    // pixels some window of the tile contains -- the Minkowski sum of the
+    // output rectangle and the kernel (tiling.py:148-162 _footprint_mask,
+    // PAPER.md:283,294): per input-tile row y, kernel rows dy whose window
+    // centre row y - dy lies in the tile contribute columns [r + xlo, r + Tw - 1
+    // + xhi - 1] (convex kernels: the union is one interval).  Circles give the
+    // rounded rectangle (c2: 25,600 -> 23,616 pixels); squares the whole tile.
     const bool k1reg = p.k1_count && ((g.Sw + 31) >> 5) <= 6 && env_int("IMF_K1REG", 1) &&
                        (long long)(g.H - 1) * g.s_y + (long long)(g.W - 1) * g.s_x < (1ll << 31);
-    if (p.pair && k->shape_code == IMF_SHAPE_CIRCLE && k1reg && env_int("IMF_FOOTPRINT", 1)) {
-        const int R2 = r * (r + 1);
+    if (p.pair && k->shape_code != IMF_SHAPE_SQUARE && k1reg && g.Sh <= 256 && env_int("IMF_FOOTPRINT", 1)) {
         int nfp = 0;
         for (int y = 0; y < g.Sh; y++) {
-            const int ey = std::max(0, std::max(r - y, y - (r + g.Th - 1)));
-            const int D = R2 - ey * ey;
-            if (D < 0) continue;
-            int w = 0;
-            while ((w + 1) * (w + 1) <= D) w++;
-            nfp += std::min(g.Sw - 1, r + g.Tw - 1 + w) - std::max(0, r - w) + 1;
+            int lo = 1 << 30, hi = -1;
+            for (int i = 0; i < k->nrows; i++) {
+                const int cy = y - k->row_dy[i];  // window centre row (input-tile coordinates)
+                if (cy < r || cy > r + g.Th - 1 || k->row_xhi[i] <= k->row_xlo[i]) continue;
+                lo = std::min(lo, r + k->row_xlo[i]);
+                hi = std::max(hi, r + g.Tw - 1 + k->row_xhi[i] - 1);
+            }
+            lo = std::max(lo, 0);
+            hi = std::min(hi, g.Sw - 1);
+            if (lo > hi) {
+                p.fprow[y] = 0xffffffffu;  // lo = hi = 65535: no pixel of this row
+                continue;
+            }
+            p.fprow[y] = (uint32_t)lo | ((uint32_t)hi << 16);
+            nfp += hi - lo + 1;
         }
         const int NI = g.Sw * g.Sh;
         g.fp = 1;
-        g.fpR2 = R2;
+        g.fpR2 = 0;
         g.N = nfp;
         g.Npad = (nfp + 63) & ~63;
         p.hs = nfp > 32768 ? 1 : 0;
@@ -283,6 +299,20 @@ int make_plan(const imf_image* src, const imf_kernel* k, const imf_options* opt,
         p.k1_smem = k1_count_smem_bytes(g.dtype, g.Npad);
     }
 
+    // K1 tile loads through TMA when the plane is pixel-contiguous (s_x == 1):
+    // one 2D box (Sw x Sh, width rounded to 16 B) per tile into the omega area
+    // (imf_count.cu).  Interleaved channels keep the per-lane loads.
+    {
+        const int esz = dtype_size(g.dtype);
+        p.k1_tma = k1reg && g.dtype != DT_F32 && g.s_x == 1 && env_int("IMF_TMA", 1) &&
+                   ((long long)g.s_y * esz) % 16 == 0 && (g.C == 1 || ((long long)g.s_c * esz) % 16 == 0) &&
+                   (g.B == 1 || ((long long)g.s_b * esz) % 16 == 0);
+        if (p.k1_tma) {
+            const int q = 16 / esz;  // box starts 16-byte aligned: up to q - 1 extra columns on the left
+            g.tma_bw = (g.Sw + q - 1 + q - 1) / q * q;
+            p.k1_smem = std::max(p.k1_smem, k1_count_smem_bytes(g.dtype, 0) + (size_t)g.tma_bw * g.Sh * esz);
+        }
+    }
     const size_t slot = 2 * (size_t)(g.Npad + 2 * OMEGA_SLOT_PAD);
     const size_t per_tile = slot + p.k1_gs_per_tile;
     // Two lanes (streams) alternate chunks when there are enough tiles: each
@@ -375,15 +405,17 @@ cudaError_t set_attrs() {
     if (!e) e = allow_smem(k1_count<DT_U8>, optin);
     if (!e) e = allow_smem(k1_count<DT_U16>, optin);
     if (!e) e = allow_smem(k1_count_g, optin);
-#define IMF_K1R_ATTR(DT)                                                          \
-    if (!e) e = allow_smem(k1_count_reg<DT, 1>, optin);                          \
-    if (!e) e = allow_smem(k1_count_reg<DT, 2>, optin);                          \
-    if (!e) e = allow_smem(k1_count_reg<DT, 3>, optin);                          \
-    if (!e) e = allow_smem(k1_count_reg<DT, 4>, optin);                          \
-    if (!e) e = allow_smem(k1_count_reg<DT, 5>, optin);                          \
-    if (!e) e = allow_smem(k1_count_reg<DT, 6>, optin);
-    IMF_K1R_ATTR(DT_U8)
-    IMF_K1R_ATTR(DT_U16)
+#define IMF_K1R_ATTR(DT, TMA)                                                     \
+    if (!e) e = allow_smem(k1_count_reg<DT, 1, TMA>, optin);                     \
+    if (!e) e = allow_smem(k1_count_reg<DT, 2, TMA>, optin);                     \
+    if (!e) e = allow_smem(k1_count_reg<DT, 3, TMA>, optin);                     \
+    if (!e) e = allow_smem(k1_count_reg<DT, 4, TMA>, optin);                     \
+    if (!e) e = allow_smem(k1_count_reg<DT, 5, TMA>, optin);                     \
+    if (!e) e = allow_smem(k1_count_reg<DT, 6, TMA>, optin);
+    IMF_K1R_ATTR(DT_U8, false)
+    IMF_K1R_ATTR(DT_U16, false)
+    IMF_K1R_ATTR(DT_U8, true)
+    IMF_K1R_ATTR(DT_U16, true)
 #undef IMF_K1R_ATTR
 #define IMF_K1F_ATTR(NK)                                               \
     if (!e) e = allow_smem(k1_f32_bucket<NK, false>, optin);           \
@@ -417,8 +449,48 @@ cudaError_t set_attrs() {
     return e;
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_tiled() {
+    static EncodeTiledFn fn = []() -> EncodeTiledFn {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &f, 12000, cudaEnableDefault, &q) !=
+                cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return nullptr;
+        return reinterpret_cast<EncodeTiledFn>(f);
+    }();
+    return fn;
+}
+
+// 4D tensor map (W, H, C, B) of the source planes, box (tma_bw, Sh, 1, 1) for
+// k1_count_reg<.., TMA>.  False when the layout cannot be described (then the
+// per-lane loads run).
+bool make_k1_tmap(const Geom& g, const void* data, CUtensorMap* tm) {
+    EncodeTiledFn enc = encode_tiled();
+    const int esz = g.dtype == DT_U8 ? 1 : 2;
+    if (!enc || ((uintptr_t)data & 15)) return false;
+    const cuuint64_t sy = (cuuint64_t)g.s_y * esz;
+    const cuuint64_t sc = g.C > 1 ? (cuuint64_t)g.s_c * esz : sy * (cuuint64_t)g.H;
+    const cuuint64_t sb = g.B > 1 ? (cuuint64_t)g.s_b * esz : sc * (cuuint64_t)g.C;
+    const cuuint64_t dims[4] = {(cuuint64_t)g.W, (cuuint64_t)g.H, (cuuint64_t)g.C, (cuuint64_t)g.B};
+    const cuuint64_t strides[3] = {sy, sc, sb};
+    const cuuint32_t box[4] = {(cuuint32_t)g.tma_bw, (cuuint32_t)g.Sh, 1, 1};
+    const cuuint32_t estr[4] = {1, 1, 1, 1};
+    for (cuuint64_t st : strides)
+        if (st % 16 || st >= (1ull << 40)) return false;
+    return enc(tm, esz == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_UINT16, 4,
+               const_cast<void*>(data), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+               CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 void launch_k1(const Plan& p, const Geom& g, int nblocks, uint16_t* omega, unsigned char* k1g,
-               int* flags, cudaStream_t s) {
+               int* flags, cudaStream_t s, const CUtensorMap* tm) {
     const dim3 grid(nblocks), block(p.k1_threads);
     const long long gs = (long long)p.k1_gs_per_tile;
     if (p.k1_f32b) {
@@ -468,21 +540,23 @@ void launch_k1(const Plan& p, const Geom& g, int nblocks, uint16_t* omega, unsig
         // k1_count_reg addresses a plane with 32-bit element offsets
         const bool plane32 = (long long)(g.H - 1) * g.s_y + (long long)(g.W - 1) * g.s_x < (1ll << 31);
         if (nk <= 6 && plane32 && env_int("IMF_K1REG", 1)) {
-#define IMF_K1R_LAUNCH(DT)                                                                       \
-    switch (nk) {                                                                                \
-        case 1: k1_count_reg<DT, 1><<<grid, block, p.k1_smem, s>>>(g, omega); break;             \
-        case 2: k1_count_reg<DT, 2><<<grid, block, p.k1_smem, s>>>(g, omega); break;             \
-        case 3: k1_count_reg<DT, 3><<<grid, block, p.k1_smem, s>>>(g, omega); break;             \
-        case 4: k1_count_reg<DT, 4><<<grid, block, p.k1_smem, s>>>(g, omega); break;             \
-        case 5: k1_count_reg<DT, 5><<<grid, block, p.k1_smem, s>>>(g, omega); break;             \
-        default: k1_count_reg<DT, 6><<<grid, block, p.k1_smem, s>>>(g, omega); break;            \
+#define IMF_K1R_CASE(DT, TMA)                                                                      \
+    switch (nk) {                                                                                  \
+        case 1: k1_count_reg<DT, 1, TMA><<<grid, block, p.k1_smem, s>>>(g, omega, tmap); break;  \
+        case 2: k1_count_reg<DT, 2, TMA><<<grid, block, p.k1_smem, s>>>(g, omega, tmap); break;  \
+        case 3: k1_count_reg<DT, 3, TMA><<<grid, block, p.k1_smem, s>>>(g, omega, tmap); break;  \
+        case 4: k1_count_reg<DT, 4, TMA><<<grid, block, p.k1_smem, s>>>(g, omega, tmap); break;  \
+        case 5: k1_count_reg<DT, 5, TMA><<<grid, block, p.k1_smem, s>>>(g, omega, tmap); break;  \
+        default: k1_count_reg<DT, 6, TMA><<<grid, block, p.k1_smem, s>>>(g, omega, tmap); break; \
     }
+            const bool tma = tm != nullptr;
+            const CUtensorMap tmap = tma ? *tm : CUtensorMap{};
             if (g.dtype == DT_U8) {
-                IMF_K1R_LAUNCH(DT_U8)
+                if (tma) { IMF_K1R_CASE(DT_U8, true) } else { IMF_K1R_CASE(DT_U8, false) }
             } else {
-                IMF_K1R_LAUNCH(DT_U16)
+                if (tma) { IMF_K1R_CASE(DT_U16, true) } else { IMF_K1R_CASE(DT_U16, false) }
             }
-#undef IMF_K1R_LAUNCH
+#undef IMF_K1R_CASE
             return;
         }
         if (g.dtype == DT_U8)
@@ -589,6 +663,13 @@ static int filter_impl(const imf_image* src, imf_image* dsts, int n, const int32
     Geom g = p.g;
     g.src = src->data;
     g.ctab_g = nullptr;
+    g.fprow = nullptr;
+    if (g.fp) {  // footprint rows into the workspace (the copy is staged at call time)
+        uint32_t* d = (uint32_t*)(ws + kFpOffset);
+        if (cudaError_t e = cudaMemcpyAsync(d, p.fprow, 4 * (size_t)g.Sh, cudaMemcpyHostToDevice, s))
+            return cuda_fail(e, "footprint table upload");
+        g.fprow = d;
+    }
     if (p.ws_ctab && p.ct_y1 > p.ct_y0) {
         uint32_t* ct = (uint32_t*)(ws + kStatusBytes + p.lanes * p.ws_lane);
         if (cudaError_t e = cudaMemsetAsync(ct, 0, p.ws_ctab, s)) return cuda_fail(e, "coarse table memset");
@@ -599,6 +680,10 @@ static int filter_impl(const imf_image* src, imf_image* dsts, int n, const int32
         g_launches += 2;
         g.ctab_g = ct;
     }
+    CUtensorMap k1_tmap;
+    const bool use_tma = p.k1_tma && make_k1_tmap(g, src->data, &k1_tmap);
+    g_last_tma = use_tma;
+
     SelParams sp;
     memset(&sp, 0, sizeof(sp));
     sp.circle = kernel->shape_code == IMF_SHAPE_CIRCLE;
@@ -634,6 +719,7 @@ static int filter_impl(const imf_image* src, imf_image* dsts, int n, const int32
         pp.grouped = p.k2_threads == 64 * p.G && p.g.Tw <= 64 && p.G <= 15 && env_int("IMF_GROUPED", 1);
         pp.status = status;
         pp.debug_defect = dbg_defect;
+        pp.refine_mode = env_int("IMF_REFINE", 1);
     }
 
     // Optional per-kernel timing (opt->reserved[0] & 1): CUDA events recorded on
@@ -675,7 +761,7 @@ static int filter_impl(const imf_image* src, imf_image* dsts, int n, const int32
             cudaEventCreate(&e2);
             cudaEventRecord(e0, s);
         }
-        launch_k1(p, g, nb, omega, k1g, k1flags, s);
+        launch_k1(p, g, nb, omega, k1g, k1flags, s, use_tma ? &k1_tmap : nullptr);
         if (prof) cudaEventRecord(e1, s);
         for (int i = 0; i < n; i++) {
         g.dst = dsts[i].data;
@@ -777,13 +863,14 @@ int imf_profile_last(float* sort_ms, float* select_ms, int32_t* launches, int64_
     return IMF_OK;
 }
 
+uint32_t imf_last_features(void) { return g_last_tma ? IMF_FEATURE_K1_TMA : 0u; }
+
 int imf_workspace_status(void* workspace, void* stream) {
     int h = 0;
     if (!workspace) return IMF_ERR_INVALID;
-    if (cudaMemcpyAsync(&h, workspace, sizeof(int), cudaMemcpyDeviceToHost, (cudaStream_t)stream) !=
-        cudaSuccess)
-        return IMF_ERR_CUDA;
-    if (cudaStreamSynchronize((cudaStream_t)stream) != cudaSuccess) return IMF_ERR_CUDA;
+    if (cudaError_t e = cudaMemcpyAsync(&h, workspace, sizeof(int), cudaMemcpyDeviceToHost, (cudaStream_t)stream))
+        return cuda_fail(e, "status read");
+    if (cudaError_t e = cudaStreamSynchronize((cudaStream_t)stream)) return cuda_fail(e, "stream synchronize");
     return h ? IMF_ERR_DEFECT : IMF_OK;
 }
 

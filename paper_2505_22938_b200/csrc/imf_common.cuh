@@ -34,7 +34,10 @@ struct Geom {
     int vshift;                    // r in valid mode, 0 in replicate mode
     int r;
     int Tw, Th, Sw, Sh, N, Npad;   // N: ranked pixels per tile; Npad: N rounded up to a multiple of 64
-    int fp, fpR2;                  // fp: only pixels within dist^2 <= fpR2 of the output rect are ranked
+    int fp, fpR2;                  // fp: only footprint pixels are ranked (fprow; fpR2: circle radius^2 test)
+    const uint32_t* fprow;         // footprint rows: input-tile row y ranks columns [lo, hi], lo | hi << 16
+                                   // (lo > hi: none); device memory (workspace), nullptr = whole tile
+    int tma_bw;                    // K1 TMA box width (elements per box row) when the launch uses TMA
     int run_min;                   // bucket K1: copy groups (replicate boundary) this large rank as one run
     const uint32_t* ctab_g;        // f32 bucket K1: call-wide fine-bucket table (k_coarse_*), or nullptr
     int tiles_x, tiles_y;

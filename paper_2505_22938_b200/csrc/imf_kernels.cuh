@@ -4,6 +4,8 @@
 // (separate .o, no -rdc: only host launch stubs cross translation units) and
 // explicitly instantiates the template kernels the planner launches.
 #pragma once
+#include <cuda.h>  // CUtensorMap (TMA descriptors; encoded through the runtime's driver entry point)
+
 #include "imf_common.cuh"
 
 namespace imf {
@@ -20,8 +22,9 @@ __global__ void __launch_bounds__(1024) k1_sort(Geom g, uint16_t* __restrict__ o
                                                long long gscratch_stride, const int* __restrict__ only);
 template <int DT>
 __global__ void __launch_bounds__(1024) k1_count(Geom g, uint16_t* __restrict__ omega_out);
-template <int DT, int NK>
-__global__ void __launch_bounds__(1024) k1_count_reg(Geom g, uint16_t* __restrict__ omega_out);
+template <int DT, int NK, bool TMA>
+__global__ void __launch_bounds__(1024) k1_count_reg(Geom g, uint16_t* __restrict__ omega_out,
+                                                     const __grid_constant__ CUtensorMap tmap);
 __global__ void __launch_bounds__(1024) k1_count_g(Geom g, uint16_t* __restrict__ omega_out);
 template <int NK, bool GENT>
 __global__ void __launch_bounds__(1024) k1_f32_bucket(Geom g, uint16_t* __restrict__ omega_out,
@@ -79,6 +82,7 @@ struct PairParams {
     int hs;          // 1: I holds rank >> 1 (tiles with 32768 < N <= 65536), pivots even
     int* status;
     int debug_defect;  // test hook (IMF_FLAG_DEBUG_DEFECT): corrupt one slide count in tile 0
+    int refine_mode;   // phase-D refine: 0 both walks per iteration, 1 walks in sequence (IMF_REFINE)
 };
 
 template <int SHAPE, bool OMG>

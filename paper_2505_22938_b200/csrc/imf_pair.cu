@@ -389,6 +389,34 @@ __device__ __forceinline__ void refine8x2(const PairCtx& c, int cx, int cy, int 
 #endif
 }
 
+// The pair's two walks one after the other in ONE loop (a lane switches to
+// window B when A is done): a warp iterates max over lanes of (steps_A +
+// steps_B) single-walk iterations instead of max over lanes of max(steps_A,
+// steps_B) double iterations -- never more work, less when the pair's walk
+// lengths differ (IMF_REFINE=1).
+template <int SHAPE, bool OMG>
+__device__ __forceinline__ void refine8x2_seq(const PairCtx& c, int cx, int cy, int PA, int cntA, int tA, int PB,
+                                              int cntB, int tB, int& mA, int& mB) {
+    Walk w;
+    uint32_t mk = walk_init(w, PA, cntA, tA, cx, cy);
+    w.Kc = window_key<SHAPE>(cx, cy);
+    int cxc = cx;
+    bool second = false;
+    for (;;) {
+        walk_step2<SHAPE, OMG>(c, w, mk, cxc, cy);
+        mk = 0xffu;
+        if (w.done) {
+            if (second) break;
+            mA = walk_result(c, w);
+            mk = walk_init(w, PB, cntB, tB, cx + 1, cy);
+            w.Kc = window_key<SHAPE>(cx + 1, cy);
+            cxc = cx + 1;
+            second = true;
+        }
+    }
+    mB = walk_result(c, w);
+}
+
 // Gather C[m] (the input value at omega[m]'s position, core.py:366) and the
 // flat destination index; the store is issued later so the L2 latency of the
 // gather overlaps the next slide.
@@ -847,7 +875,10 @@ __global__ void __launch_bounds__(512, 2) k2_pair(Geom g, PairParams p, const __
             const int tA = target_at2(g, p, tc, row, j0);
             const int tB = target_at2(g, p, tc, row, j1);
             int mA, mB;
-            refine8x2<SHAPE, OMG>(c, j0 + r, row + r, PA, cA, tA, PB, cB, tB, mA, mB);
+            if (p.refine_mode == 1)
+                refine8x2_seq<SHAPE, OMG>(c, j0 + r, row + r, PA, cA, tA, PB, cB, tB, mA, mB);
+            else
+                refine8x2<SHAPE, OMG>(c, j0 + r, row + r, PA, cA, tA, PB, cB, tB, mA, mB);
             if ((mA | mB) < 0) {
                 atomicOr(p.status, 1);
                 mA = max(mA, 0);

@@ -19,8 +19,9 @@
 // When the tile does not fit shared memory, the large arrays live in a
 // per-CTA global scratch slot (L2-resident) -- same code, GMEM=true.
 #include <algorithm>
+#include <type_traits>
 
-#include "imf_kernels.cuh"
+#include "imf_k1.cuh"
 
 namespace imf {
 
@@ -134,25 +135,6 @@ __device__ __forceinline__ uint16_t pack_pos(int i, int Sw, float invS) {
     return (uint16_t)(x | (y << 8));
 }
 
-// Copy the finished omega (smem, N entries) to its global slot, 16 B at a time.
-// Global omega slot of a tile: OMEGA_SLOT_PAD sentinel entries on both sides
-// of Npad ranks, so scans may step a few ranks past either end.
-__device__ __forceinline__ uint16_t* omega_slot(const Geom& g, uint16_t* base, int bt = -1) {
-    if (bt < 0) bt = blockIdx.x;
-    return base + (long long)bt * (g.Npad + 2 * OMEGA_SLOT_PAD) + OMEGA_SLOT_PAD;
-}
-
-__device__ __forceinline__ void store_omega(const Geom& g, const uint16_t* om_s, uint16_t* om_g) {
-    const int n16 = g.Npad >> 3;  // uint4 count
-    const uint4* s = reinterpret_cast<const uint4*>(om_s);
-    uint4* d = reinterpret_cast<uint4*>(om_g);
-    for (int i = threadIdx.x; i < n16; i += blockDim.x) d[i] = s[i];
-    if (threadIdx.x < OMEGA_SLOT_PAD) {
-        om_g[-OMEGA_SLOT_PAD + (int)threadIdx.x] = 0xffffu;
-        om_g[g.Npad + threadIdx.x] = 0xffffu;
-    }
-}
-
 template <int DT, bool GMEM>
 __device__ void k1_sort_tile(const Geom& g, uint16_t* __restrict__ omega_out, unsigned char* __restrict__ gscratch,
                              long long gscratch_stride, const int bt) {
@@ -240,134 +222,6 @@ __global__ void __launch_bounds__(1024) k1_sort(Geom g, uint16_t* __restrict__ o
     }
 }
 
-// Exclusive scan, in place, of the 2*NW 16-bit counters packed two per word
-// in hw[0..NW).  Warp w owns words [w*NW/nw, (w+1)*NW/nw); lanes stride by one
-// word, so every shared access is bank-conflict free.  Ends with the counters
-// replaced by their exclusive prefix (no trailing barrier).
-__device__ __forceinline__ void hist16_exclusive_scan(uint32_t* hw, const int NW,
-                                                      uint32_t* starts = nullptr,
-                                                      unsigned long long* sumsq = nullptr) {
-    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
-    __shared__ uint32_t wt[32];
-    const int per = NW / nw;  // words per warp (NW and nw are powers of two)
-    if (per >= 128) {
-        // 16-byte chunks: lane l of the warp handles chunk i*32 + l of the warp's
-        // range (conflict-free), 8 counters per lane per step.  Every prefix of a
-        // tile's counters is < 65536, so the scan runs on PACKED words: adding
-        // words adds both 16-bit halves independently (no carry can cross), and
-        // counter 2i's exclusive prefix is lo + hi of the packed word prefix.
-        uint4* wb = reinterpret_cast<uint4*>(hw + wid * per);
-        const int nch = per >> 2;  // chunks per warp, multiple of 32
-        uint32_t sum = 0;
-        for (int i = lane; i < nch; i += 32) {
-            const uint4 q = wb[i];
-            sum += q.x + q.y + q.z + q.w;
-        }
-        sum = __reduce_add_sync(0xffffffffu, sum);
-        sum = (sum & 0xffffu) + (sum >> 16);
-        if (lane == 0) wt[wid] = sum;
-        __syncthreads();
-        if (wid == 0) {
-            uint32_t v = lane < nw ? wt[lane] : 0, x = v;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                uint32_t t = __shfl_up_sync(0xffffffffu, x, o);
-                if (lane >= o) x += t;
-            }
-            if (lane < nw) wt[lane] = x - v;
-        }
-        __syncthreads();
-        uint32_t carry = wt[wid];  // plain (unpacked) count before this chunk row
-        unsigned long long sqacc = 0;  // this lane's sum of squared counters (sumsq)
-        for (int i0 = 0; i0 < nch; i0 += 32) {
-            uint4 q = wb[i0 + lane];
-            const uint32_t p1 = q.x, p2 = p1 + q.y, p3 = p2 + q.z, tot = p3 + q.w;  // packed prefixes
-            uint32_t incl = tot;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += t;
-            }
-            const uint32_t ex = incl - tot;  // packed exclusive prefix of this lane's chunk
-            const uint32_t base = carry + (ex & 0xffffu) + (ex >> 16);
-            // counters before word k: base + flat(packed prefix of words < k)
-            const uint32_t b0 = base, b1 = base + (p1 & 0xffffu) + (p1 >> 16);
-            const uint32_t b2 = base + (p2 & 0xffffu) + (p2 >> 16), b3 = base + (p3 & 0xffffu) + (p3 >> 16);
-            if (starts || sumsq) {
-                const uint32_t cw[4] = {q.x, q.y, q.z, q.w}, bw[4] = {b0, b1, b2, b3};
-#pragma unroll
-                for (int k = 0; k < 4; k++) {
-                    const uint32_t lo = cw[k] & 0xffffu, hi = cw[k] >> 16, e0 = bw[k], e1 = bw[k] + lo;
-                    if (starts) {  // bit at every non-empty counter's first position (bucket starts)
-                        if (lo) atomicOr(&starts[e0 >> 5], 1u << (e0 & 31));
-                        if (hi) atomicOr(&starts[e1 >> 5], 1u << (e1 & 31));
-                    }
-                    sqacc += (unsigned long long)(lo * lo) + (unsigned long long)(hi * hi);
-                }
-            }
-            q.x = b0 | ((b0 + (q.x & 0xffffu)) << 16);
-            q.y = b1 | ((b1 + (q.y & 0xffffu)) << 16);
-            q.z = b2 | ((b2 + (q.z & 0xffffu)) << 16);
-            q.w = b3 | ((b3 + (q.w & 0xffffu)) << 16);
-            wb[i0 + lane] = q;
-            const uint32_t last = __shfl_sync(0xffffffffu, incl, 31);
-            carry += (last & 0xffffu) + (last >> 16);
-        }
-        if (sumsq) {
-            // clamp per lane at 2^26 (> kMaxSumSq: the tile falls back anyway) so
-            // the 32-bit warp sum cannot wrap
-            const unsigned wsq = __reduce_add_sync(0xffffffffu, (unsigned)min(sqacc, 1ull << 26));
-            if (lane == 0 && wsq) atomicAdd(sumsq, (unsigned long long)wsq);
-        }
-        return;
-    }
-    // small histograms (u8: 128 words): one word per lane per step
-    const uint32_t* wbase = hw + wid * per;
-    uint32_t sum = 0;
-    for (int i = lane; i < per; i += 32) {
-        const uint32_t w = wbase[i];
-        sum += (w & 0xffffu) + (w >> 16);
-    }
-    sum = __reduce_add_sync(0xffffffffu, sum);
-    if (lane == 0) wt[wid] = sum;
-    __syncthreads();
-    if (wid == 0) {
-        uint32_t v = lane < nw ? wt[lane] : 0, x = v;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            uint32_t t = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= o) x += t;
-        }
-        if (lane < nw) wt[lane] = x - v;
-    }
-    __syncthreads();
-    uint32_t carry = wt[wid];
-    uint32_t* wb = hw + wid * per;
-    for (int i0 = 0; i0 < per; i0 += 32) {
-        const bool ok = i0 + lane < per;
-        const uint32_t w = ok ? wb[i0 + lane] : 0u;
-        const uint32_t lo = w & 0xffffu, tot = lo + (w >> 16);
-        uint32_t incl = tot;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += t;
-        }
-        const uint32_t ex = carry + incl - tot;
-        if (ok) wb[i0 + lane] = ex | ((ex + lo) << 16);
-        if (starts && ok) {  // bucket starts, as in the chunked branch
-            const uint32_t hi = w >> 16;
-            if (lo) atomicOr(&starts[ex >> 5], 1u << (ex & 31));
-            if (hi) atomicOr(&starts[(ex + lo) >> 5], 1u << ((ex + lo) & 31));
-            if (sumsq) {
-                const unsigned long long sq = (unsigned long long)lo * lo + (unsigned long long)hi * hi;
-                atomicAdd(sumsq, sq);
-            }
-        }
-        carry += __shfl_sync(0xffffffffu, incl, 31);
-    }
-}
-
 // Direct counting sort for 8/16-bit tiles (ordinal.py:62-79 _rank_by_bucket,
 // the paper's 16-bit bucket sort): one 2^bits-bin histogram
 // of u16 counters packed two per 32-bit word in shared memory (65536 bins =
@@ -437,108 +291,6 @@ __global__ void __launch_bounds__(1024) k1_count(Geom g, uint16_t* __restrict__ 
     store_omega(g, om, omega_slot(g, omega_out));
 }
 
-// k1_count with the tile held in registers: warp w owns input rows w + 32j,
-// lane l owns columns l + 32k (j, k < NK = ceil(S/32)), so every value is read
-// from global memory ONCE, with all NK*NK loads of a thread in flight together
-// (the two-pass k1_count re-reads the tile and exposes the L2 latency per row).
-// 1024 threads; same histogram / scan / scatter as k1_count.
-template <int DT, int NK>
-__global__ void __launch_bounds__(1024) k1_count_reg(Geom g, uint16_t* __restrict__ omega_out) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    constexpr int NB = DT == DT_U8 ? 256 : 65536;
-    constexpr int NW = NB / 2;
-    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const TileCoord tc = tile_coord(g, g.tile_begin + blockIdx.x);
-    const int S = g.Sw, SH = g.Sh;
-    uint32_t* hw = reinterpret_cast<uint32_t*>(smem);
-    uint16_t* om = reinterpret_cast<uint16_t*>(hw + NW);
-    uint32_t v[NK][NK];
-    {
-        // element offsets within one (image, channel) plane fit 32 bits
-        int xo[NK];
-#pragma unroll
-        for (int k = 0; k < NK; k++) {
-            int x = tc.ox0 + lane + 32 * k - g.r + g.vshift;
-            x = x < 0 ? 0 : (x >= g.W ? g.W - 1 : x);
-            xo[k] = x * (int)g.s_x;
-        }
-#pragma unroll
-        for (int j = 0; j < NK; j++) {
-            const int y = wid + 32 * j;
-            int yy = tc.oy0 + y - g.r + g.vshift;
-            yy = yy < 0 ? 0 : (yy >= g.H ? g.H - 1 : yy);
-            const int ro = yy * (int)g.s_y;
-            // footprint columns of this row: [flo, fhi] (all columns without one)
-            int flo = 0, fhi = S - 1;
-            if (g.fp) {
-                const int ey = max(0, max(g.r - y, y - (g.r + g.Th - 1)));
-                const int D = g.fpR2 - ey * ey;
-                int w = D < 0 ? -1 : (int)sqrtf((float)D);
-                if (w >= 0) {
-                    while (w * w > D) w--;
-                    while ((w + 1) * (w + 1) <= D) w++;
-                }
-                flo = w < 0 ? S : g.r - w;
-                fhi = g.r + g.Tw - 1 + w;
-            }
-#pragma unroll
-            for (int k = 0; k < NK; k++) {
-                const int x = lane + 32 * k;
-                const bool ok = y < SH && x < S && x >= flo && x <= fhi;
-                uint32_t val = 0xffffffffu;
-                if (ok) {
-                    val = DT == DT_U8 ? (uint32_t)__ldg((const uint8_t*)tc.src + (ro + xo[k]))
-                                      : (uint32_t)__ldg((const uint16_t*)tc.src + (ro + xo[k]));
-                }
-                v[j][k] = val;
-            }
-        }
-    }
-    {
-        uint4* h4 = reinterpret_cast<uint4*>(hw);
-        for (int i = tid; i < NW / 4; i += blockDim.x) h4[i] = make_uint4(0, 0, 0, 0);
-    }
-    __syncthreads();
-    // counting pass: the count a pixel's atomic returns is its index among the
-    // tile's equal values, kept in the key's high half, so rank = prefix(value)
-    // + that index -- the scatter needs a load, not a second atomic
-#pragma unroll
-    for (int j = 0; j < NK; j++)
-#pragma unroll
-        for (int k = 0; k < NK; k++)
-            if (v[j][k] != 0xffffffffu) {
-                const uint32_t sh = (v[j][k] & 1) << 4;
-                const uint32_t old = atomicAdd(&hw[v[j][k] >> 1], 1u << sh);
-                v[j][k] |= ((old >> sh) & 0xffffu) << 16;
-            }
-    __syncthreads();
-    hist16_exclusive_scan(hw, NW);
-    __syncthreads();
-#pragma unroll
-    for (int j = 0; j < NK; j++)
-#pragma unroll
-        for (int k = 0; k < NK; k++) {
-            const uint32_t val = v[j][k];
-            if (val != 0xffffffffu) {
-                const uint32_t sh = (val & 1) << 4;
-                const uint32_t rank = ((hw[(val & 0xffffu) >> 1] >> sh) & 0xffffu) + (val >> 16);
-                om[rank] = (uint16_t)((lane + 32 * k) | ((wid + 32 * j) << 8));
-            }
-        }
-    for (int i = g.N + tid; i < g.Npad; i += blockDim.x) om[i] = 0xffffu;
-    __syncthreads();
-    store_omega(g, om, omega_slot(g, omega_out));
-}
-
-#define IMF_K1R(DT) \
-    template __global__ void k1_count_reg<DT, 1>(Geom, uint16_t*); \
-    template __global__ void k1_count_reg<DT, 2>(Geom, uint16_t*); \
-    template __global__ void k1_count_reg<DT, 3>(Geom, uint16_t*); \
-    template __global__ void k1_count_reg<DT, 4>(Geom, uint16_t*); \
-    template __global__ void k1_count_reg<DT, 5>(Geom, uint16_t*); \
-    template __global__ void k1_count_reg<DT, 6>(Geom, uint16_t*);
-IMF_K1R(DT_U8)
-IMF_K1R(DT_U16)
 #undef IMF_K1R
 
 
@@ -552,7 +304,6 @@ IMF_K1R(DT_U16)
 // regions) writes flag 1 and no omega; a k1_sort launch redoes those tiles.
 // Ranking cost is sum(n_b^2) entry compares per tile; above this (about 60K per
 // thread of a 1024-thread CTA) the tile goes to the LSD radix sort instead.
-constexpr unsigned long long kMaxSumSq = 64ull << 20;
 
 // Adaptive buckets for f32 keys.  Bucketing on the key's top 16 bits
 // (sign, exponent, 7 mantissa bits) leaves a tile's values in a few hundred
@@ -1271,7 +1022,7 @@ __global__ void __launch_bounds__(1024) k1_count_g(Geom g, uint16_t* __restrict_
 size_t k1_count_g_smem_bytes() { return 32768 * 4 + 16; }
 
 size_t k1_count_smem_bytes(int dtype, int Npad) {
-    return (dtype == DT_U8 ? 128 * 4 : 32768 * 4) + 2 * (size_t)Npad;
+    return (dtype == DT_U8 ? 128 * 4 : 32768 * 4) + 256 + 2 * (size_t)Npad;  // + k1_count_reg's sink words, mbarrier
 }
 
 template __global__ void k1_sort<DT_U8, false>(Geom, uint16_t*, unsigned char*, long long, const int*);

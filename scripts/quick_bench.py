@@ -10,6 +10,19 @@ import cases as C
 from paper_2505_22938_b200 import FilterParams, ShapeSpec, _lib, make_kernel
 from paper_2505_22938_b200.tiling import run_device
 
+_PEAK = None
+
+
+def int_peak():
+    """Measured int32 add throughput of this GPU (imf_int_peak), ops/s."""
+    global _PEAK
+    if _PEAK is None:
+        pk = ctypes.c_double()
+        _lib.lib().imf_int_peak(ctypes.byref(pk), None)
+        _PEAK = pk.value
+    return _PEAK
+
+
 def run(name, img, spec, reps=5, gold=None):
     t = torch.from_numpy(img).cuda().unsqueeze(0)
     params = FilterParams(shape=ShapeSpec(*spec))
@@ -33,7 +46,10 @@ def run(name, img, spec, reps=5, gold=None):
     print(json.dumps({"cfg": name, "ms": round(ms, 3), "k1_ms": round(float(np.median(k1)), 3),
                       "k2_ms": round(float(np.median(k2)), 3), "MP/s": round(h*w/1e3/ms, 1),
                       "chMP/s": round(h*w*c/1e3/ms, 1), "tile": tl.value, "qs": qs.value,
-                      "frac_nominal18.6": round(h*w*c/1e3/ms*1e6*W/18.6e12, 3), "parity": ok,
+                      "path_frac": round(h*w*c/1e3/ms*1e6*W/int_peak(), 4),
+                      "k2_frac": (round(h*w*c/1e3/float(np.median(k2))*1e6*W/int_peak(), 4)
+                                  if np.median(k2) > 0 else None),
+                      "peak_Tops": round(int_peak()/1e12, 2), "parity": ok,
                       "env": {k_: os.environ.get(k_) for k_ in ("IMF_TILE", "IMF_SEED_ROWS", "IMF_SEEDS") if os.environ.get(k_)}}), flush=True)
 
 which = sys.argv[1:] or ["c1", "c2", "c3", "c4"]

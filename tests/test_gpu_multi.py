@@ -138,3 +138,35 @@ def test_device_scan_defect_raises(monkeypatch, cfg):
         filter_image_bracket(img, params, [0.25, 0.5])
     monkeypatch.delenv("IMF_DEBUG_DEFECT")
     assert np.array_equal(filter_image(img, params), oracle.fast_filter(img, params.shape, 0.5))
+
+
+@pytest.mark.parametrize("dt,r,boundary", [(np.uint16, 20, "replicate"), (np.uint8, 9, "valid"),
+                                           (np.uint16, 64, "replicate")])
+def test_k1_tma_tile_loads(dt, r, boundary):
+    """Planar (pixel-contiguous) u8/u16 images: K1 loads its tile boxes with TMA
+    (cp.async.bulk.tensor, clamped box reads = replicate padding); a row-shifted
+    view that breaks the 16-byte alignment falls back to per-lane loads.  Both
+    bit-exact against the oracle."""
+    import torch
+    from paper_2505_22938_b200 import _lib
+    FilterParams, ShapeSpec, filter_image = _api()
+    rng = np.random.default_rng(38)
+    hi = 256 if dt == np.uint8 else 65536
+    img = rng.integers(0, hi, (3, 457, 389), dtype=dt)  # batch of planes
+    params = FilterParams(shape=ShapeSpec("circle", r), boundary=boundary)
+    from paper_2505_22938_b200 import filter_batch
+    src = torch.from_numpy(img).cuda()
+    pad = torch.zeros((3, 457, 400), dtype=src.dtype, device="cuda")
+    pad[:, :, :389] = src  # row stride 400 elements: a 16-byte multiple for u8 and u16
+    L = _lib.lib()
+    seen_tma = False
+    for t in (src, pad[:, :, :389], src[:, :, :384].contiguous()):
+        out = filter_batch(t, params).cpu().numpy()
+        tma = bool(L.imf_last_features() & _lib.IMF_FEATURE_K1_TMA)
+        row_bytes = t.stride(1) * t.element_size()
+        assert tma == (row_bytes % 16 == 0 and t.data_ptr() % 16 == 0), (tma, row_bytes)
+        seen_tma = seen_tma or tma
+        host = t.cpu().numpy()
+        for b in range(3):
+            assert np.array_equal(out[b], oracle.fast_filter(host[b], params.shape, 0.5, boundary)), b
+    assert seen_tma  # the aligned layouts did take the TMA path
