@@ -19,20 +19,22 @@ rows = [r for r in src[2:] if r[ia].isdigit()]
 base = int(rows[0][0], 16)
 tmp = tempfile.mkdtemp()
 subprocess.run(["cuobjdump", "-xelf", "all", os.path.join(ROOT, "paper_2505_22938_b200", "libisomedian_b200.so")], cwd=tmp, capture_output=True)
-cub = [f for f in os.listdir(tmp) if f.endswith(".cubin")][0]
-# find the mangled name whose demangled form matches
-syms = subprocess.run(["cuobjdump", "-symbols", os.path.join(tmp, cub)], capture_output=True, text=True).stdout
-cands = re.findall(r"(_ZN3imf\S+)", syms)
+cubs = [f for f in os.listdir(tmp) if f.endswith(".cubin")]
+# find the cubin and mangled name whose demangled form matches (one cubin per kernel TU)
+cands = []
+for cb in cubs:
+    syms = subprocess.run(["cuobjdump", "-symbols", os.path.join(tmp, cb)], capture_output=True, text=True).stdout
+    cands += [(cb, c) for c in re.findall(r"(_ZN3imf\S+)", syms)]
 def norm(x):
     x = re.sub(r"\((?:imf::)?\w+\)(?=-?\d)", "", x)
     x = x.replace("(bool)", "").replace("imf::", "").replace("void ", "").replace(" ", "")
     return x.replace("true", "1").replace("false", "0")
 want = norm(kname)
-best = None
-for c in cands:
+best = cub = None
+for cb, c in cands:
     dm = norm(subprocess.run(["cu++filt", c], capture_output=True, text=True).stdout.strip())
     if dm == want:
-        best = c
+        best, cub = c, cb
         break
 dis = subprocess.run(["nvdisasm", "-gi", "-c", os.path.join(tmp, cub)], capture_output=True, text=True).stdout
 lines_all = dis.splitlines()
