@@ -235,12 +235,18 @@ def work_per_chpx(kernel):
     return 4 * len(kernel.col_dx) + 384
 
 
-def load_ncu_traffic():
-    p = os.path.join(ROOT, "profiles", "ncu_k2_pair_c2_r1.json")
+def load_ncu_traffic(workload):
+    """DRAM bytes of one K2 launch from the newest committed `ncu --set full`
+    capture of this workload (profiles/ncu_k2_pair_<workload>_r<N>.json)."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", f"ncu_k2_pair_{workload}_r*.json")),
+                   key=lambda f: int(f.rsplit("_r", 1)[1].split(".")[0]))
+    if not files:
+        return None, f"no ncu capture of {workload} committed under profiles/"
     try:
-        with open(p) as f:
+        with open(files[-1]) as f:
             d = json.load(f)
-        return d.get("dram_bytes_per_launch"), d.get("source")
+        return d.get("dram_bytes_per_launch"), f"{os.path.basename(files[-1])} ({d.get('source')})"
     except (OSError, ValueError):
         return None, None
 
@@ -499,9 +505,9 @@ def run_ours(args):
     W = work_per_chpx(kernel)
     k2_ops = chp_rank * 1e6 * W * args.steps  # per rank
     achieved = k2_ops / (select_max * 1e-3)
-    traffic, tsrc = load_ncu_traffic()
-    if args.workload != "c2" or args.radius is not None:  # the committed capture is of c2
-        traffic, tsrc = None, "no ncu capture committed for this workload (profiles/ holds c2's)"
+    traffic, tsrc = load_ncu_traffic(args.workload)
+    if args.radius is not None:  # the committed captures are at the configs' own radii
+        traffic, tsrc = None, "no ncu capture at this radius"
     im0 = images[0]
     line = {
         "metric": "megapixels/sec circular median (r=8..100, 8/16-bit/f32)",
