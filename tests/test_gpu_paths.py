@@ -7,8 +7,9 @@ shared memory vs in L2 (IMF_PAIR_OMG), rounded-rect footprint on/off
 register-resident vs two-pass u16 counting sort (IMF_K1REG), the pair path on
 generic-span kernels (IMF_PAIR_ANY), polygons on the general path
 (IMF_PAIR_POLY=0), one chunk stream (IMF_LANES), per-group phases (IMF_GROUPED),
-direct selection for tiny windows (IMF_DIRECT), f32 image ranks (IMF_GRANK),
-rectangular pair tiles (IMF_PAIR_RECT),
+direct selection for tiny windows (IMF_DIRECT), TMA vs per-lane K1 tile loads
+(IMF_TMA), both phase-D refine loops (IMF_REFINE), rectangular pair tiles
+(IMF_PAIR_RECT),
 and tile / seed-row overrides.  Compared against the C oracle, which is itself
 pinned to the reference's golden outputs (tests/test_oracle.py)."""
 import os
@@ -33,7 +34,8 @@ VARIANTS = [
     {"IMF_LANES": "1"},
     {"IMF_GROUPED": "0"},
     {"IMF_DIRECT": "0"},
-    {"IMF_GRANK": "1"},
+    {"IMF_TMA": "0"},
+    {"IMF_REFINE": "0"},
     {"IMF_PAIR_RECT": "1", "IMF_TILE": "64"},
     {"IMF_TILE": "40", "IMF_SEED_ROWS": "4"},
     {"IMF_STRIPE_EDGE": "1", "IMF_STRIPE_MID": "5"},
