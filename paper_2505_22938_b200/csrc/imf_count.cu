@@ -152,7 +152,10 @@ __global__ void __launch_bounds__(1024) k1_count_reg(Geom g, uint16_t* __restric
             v[j][k] = ok ? val | (((old >> sh) & 0xffffu) << 16) : val;
         }
     __syncthreads();
-    hist16_exclusive_scan(hw, NW);
+    if (NW == 32768 && blockDim.x == 1024)
+        hist16_scan_lanes(hw);
+    else
+        hist16_exclusive_scan(hw, NW);
     __syncthreads();
 #pragma unroll
     for (int j = 0; j < NK; j++)

@@ -152,4 +152,66 @@ __device__ __forceinline__ void hist16_exclusive_scan(uint32_t* hw, const int NW
     }
 }
 
+// hist16_exclusive_scan without bucket-start / sum-of-squares outputs, for
+// 1024-thread CTAs and NW = 32768 words: lane l of warp w owns the 32
+// CONSECUTIVE words [w*1024 + 32l, +32) (8 uint4 chunks), so the lane scans
+// them sequentially in registers and the warp needs ONE shuffle scan (not one
+// per chunk row).  Chunk loads are rotated by lane ((i + l) & 7) so a warp's
+// 32 LDS.128 hit all 8 bank quads (4 wavefronts, conflict-free); the in-order
+// prefix of chunk k is rebuilt from P = (sum of the lane's chunks before its
+// first rotated chunk) and a running sum reset where the rotation wraps.
+__device__ __forceinline__ void hist16_scan_lanes(uint32_t* hw) {
+    constexpr int NW = 32768, PER = 1024, CH = 8;  // words per warp, chunks per lane
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    __shared__ uint32_t wt[32];
+    uint4* wb = reinterpret_cast<uint4*>(hw + wid * PER + lane * 32);
+    const int a = lane & (CH - 1);  // the lane's first chunk in rotated order
+    uint32_t tot = 0, pre = 0;      // packed: all chunks / chunks before chunk a
+#pragma unroll
+    for (int i = 0; i < CH; i++) {
+        const uint4 q = wb[(a + i) & (CH - 1)];
+        const uint32_t cs = q.x + q.y + q.z + q.w;
+        tot += cs;
+        if (i >= CH - a) pre += cs;  // rotated position i holds chunk (a + i) - CH < a
+    }
+    const uint32_t T = (tot & 0xffffu) + (tot >> 16);
+    uint32_t incl = T;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+    }
+    if (lane == 31) wt[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+        const uint32_t v = wt[lane];
+        uint32_t x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += t;
+        }
+        wt[lane] = x - v;
+    }
+    __syncthreads();
+    const uint32_t base = wt[wid] + incl - T;  // counters before the lane's first word
+    uint32_t run = pre;                          // packed counters before the current chunk
+#pragma unroll
+    for (int i = 0; i < CH; i++) {
+        const int k = (a + i) & (CH - 1);
+        if (k == 0) run = 0;  // wrapped to the lane's first chunk
+        uint4 q = wb[k];
+        const uint32_t p1 = run + q.x, p2 = p1 + q.y, p3 = p2 + q.z;
+        const uint32_t b0 = base + (run & 0xffffu) + (run >> 16), b1 = base + (p1 & 0xffffu) + (p1 >> 16);
+        const uint32_t b2 = base + (p2 & 0xffffu) + (p2 >> 16), b3 = base + (p3 & 0xffffu) + (p3 >> 16);
+        run = p3 + q.w;
+        q.x = b0 | ((b0 + (q.x & 0xffffu)) << 16);
+        q.y = b1 | ((b1 + (q.y & 0xffffu)) << 16);
+        q.z = b2 | ((b2 + (q.z & 0xffffu)) << 16);
+        q.w = b3 | ((b3 + (q.w & 0xffffu)) << 16);
+        wb[k] = q;
+    }
+    (void)NW;
+}
+
 }  // namespace imf

@@ -270,7 +270,10 @@ __global__ void __launch_bounds__(1024) k1_count(Geom g, uint16_t* __restrict__ 
         }
     }
     __syncthreads();
-    hist16_exclusive_scan(hw, NW);
+    if (NW == 32768 && blockDim.x == 1024)
+        hist16_scan_lanes(hw);
+    else
+        hist16_exclusive_scan(hw, NW);
     __syncthreads();
     for (int y = wid; y < Sh; y += nw) {
         const char* rp = row_ptr(y);
@@ -1005,7 +1008,10 @@ __global__ void __launch_bounds__(1024) k1_count_g(Geom g, uint16_t* __restrict_
     };
     each_pixel([&](int, int, uint32_t v) { atomicAdd(&hw[v >> 1], 1u << ((v & 1) << 4)); });
     __syncthreads();
-    hist16_exclusive_scan(hw, NW);
+    if (NW == 32768 && blockDim.x == 1024)
+        hist16_scan_lanes(hw);
+    else
+        hist16_exclusive_scan(hw, NW);
     __syncthreads();
     each_pixel([&](int x, int y, uint32_t v) {
         const uint32_t sh = (v & 1) << 4;
