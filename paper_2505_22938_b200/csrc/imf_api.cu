@@ -267,23 +267,43 @@ int make_plan(const imf_image* src, const imf_kernel* k, const imf_options* opt,
     const bool k1reg = p.k1_count && ((g.Sw + 31) >> 5) <= 6 && env_int("IMF_K1REG", 1) &&
                        (long long)(g.H - 1) * g.s_y + (long long)(g.W - 1) * g.s_x < (1ll << 31);
     if (p.pair && k->shape_code != IMF_SHAPE_SQUARE && k1reg && g.Sh <= 256 && env_int("IMF_FOOTPRINT", 1)) {
+        // the table depends on the kernel's row spans and the tile geometry only:
+        // memoized per thread (the host pipeline plans every stripe of a frame)
+        uint64_t h = 1469598103934665603ull;
+        auto mix = [&](uint64_t v) { h = (h ^ v) * 1099511628211ull; };
+        mix((uint64_t)r | (uint64_t)g.Tw << 16 | (uint64_t)g.Th << 32 | (uint64_t)g.Sw << 48);
+        mix((uint64_t)g.Sh | (uint64_t)k->nrows << 16);
+        for (int i = 0; i < k->nrows; i++)
+            mix((uint64_t)(uint32_t)k->row_dy[i] | (uint64_t)(uint16_t)k->row_xlo[i] << 32 |
+                (uint64_t)(uint16_t)k->row_xhi[i] << 48);
+        static thread_local uint64_t fp_key = 0;
+        static thread_local int fp_n = 0;
+        static thread_local uint32_t fp_rows[256];
         int nfp = 0;
-        for (int y = 0; y < g.Sh; y++) {
-            int lo = 1 << 30, hi = -1;
-            for (int i = 0; i < k->nrows; i++) {
-                const int cy = y - k->row_dy[i];  // window centre row (input-tile coordinates)
-                if (cy < r || cy > r + g.Th - 1 || k->row_xhi[i] <= k->row_xlo[i]) continue;
-                lo = std::min(lo, r + k->row_xlo[i]);
-                hi = std::max(hi, r + g.Tw - 1 + k->row_xhi[i] - 1);
+        if (fp_key == h && h != 0) {
+            memcpy(p.fprow, fp_rows, sizeof(fp_rows));
+            nfp = fp_n;
+        } else {
+            for (int y = 0; y < g.Sh; y++) {
+                int lo = 1 << 30, hi = -1;
+                for (int i = 0; i < k->nrows; i++) {
+                    const int cy = y - k->row_dy[i];  // window centre row (input-tile coordinates)
+                    if (cy < r || cy > r + g.Th - 1 || k->row_xhi[i] <= k->row_xlo[i]) continue;
+                    lo = std::min(lo, r + k->row_xlo[i]);
+                    hi = std::max(hi, r + g.Tw - 1 + k->row_xhi[i] - 1);
+                }
+                lo = std::max(lo, 0);
+                hi = std::min(hi, g.Sw - 1);
+                if (lo > hi) {
+                    p.fprow[y] = 0xffffffffu;  // lo = hi = 65535: no pixel of this row
+                    continue;
+                }
+                p.fprow[y] = (uint32_t)lo | ((uint32_t)hi << 16);
+                nfp += hi - lo + 1;
             }
-            lo = std::max(lo, 0);
-            hi = std::min(hi, g.Sw - 1);
-            if (lo > hi) {
-                p.fprow[y] = 0xffffffffu;  // lo = hi = 65535: no pixel of this row
-                continue;
-            }
-            p.fprow[y] = (uint32_t)lo | ((uint32_t)hi << 16);
-            nfp += hi - lo + 1;
+            memcpy(fp_rows, p.fprow, sizeof(fp_rows));
+            fp_n = nfp;
+            fp_key = h;
         }
         const int NI = g.Sw * g.Sh;
         g.fp = 1;
