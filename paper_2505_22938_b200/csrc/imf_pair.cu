@@ -93,7 +93,7 @@ __device__ __forceinline__ void vcount(uint32_t b, const int2* __restrict__ v, i
                                        uint32_t& ge_in, uint32_t& ge_out) {
     uint32_t ai = 0, ao = 0, ri = 0, ro = 0;
     int k = 0;
-#pragma unroll 2
+#pragma unroll 4
     for (; k + 1 < ne; k += 2) {
         const int2 o0 = v[k], o1 = v[k + 1];
         acc_ge4(ai, lds32(b + o0.x) + K, lds32(b + o1.x) + K);
@@ -104,7 +104,7 @@ __device__ __forceinline__ void vcount(uint32_t b, const int2* __restrict__ v, i
         acc_ge2(ri, lds32(b + o.x) + K);
         acc_ge2(ro, lds32(b + o.y) + K);
     }
-#pragma unroll 2
+#pragma unroll 4
     for (k = ne; k + 1 < n; k += 2) {
         const int2 o0 = v[k], o1 = v[k + 1];
         acc_ge4(ai, prmt(lds32(b + o0.x), lds32(b + o0.x + 4), 0x5432) + K,
