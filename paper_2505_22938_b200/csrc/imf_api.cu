@@ -256,6 +256,9 @@ int make_plan(const imf_image* src, const imf_kernel* k, const imf_options* opt,
     // descriptors); the LSD fallback reuses the same slot (k1_gscratch_bytes(f32)
     // = 6 B per pixel when it needs one)
     if (p.k1_f32b_g) p.k1_gs_per_tile = std::max(p.k1_gs_per_tile, (size_t)6 * g.Npad);  // + run descriptors
+    // k1_f32_bucket<NK <= 6, global entries>: interior tiles keep 16-bit entries
+    // in shared memory after the coarse table (imf_sort.cu OWN16)
+    if (p.k1_f32b_g && ((g.Sw + 31) >> 5) <= 6) p.k1b_smem += 2 * (size_t)g.Npad + 16;
 
     // Tile footprint (pair path, register-resident K1): rank only the input
     // pixels some window of the tile contains -- the Minkowski sum of the

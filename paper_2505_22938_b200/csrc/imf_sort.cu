@@ -653,10 +653,19 @@ __device__ __forceinline__ void f32_bucket_tile(const Geom& g, const TileCoord& 
     uint32_t* ctab = GENT ? starts + ((nsw + 3) & ~3) : ent;
     uint16_t* d16 = GENT ? reinterpret_cast<uint16_t*>(ent + N) : nullptr;  // run descriptors (2 B / slot)
     const bool adaptive = g.dtype == DT_F32 && N > kAdaptiveMinN;
+    // OWN16 (interior tiles too large for 4-byte shared entries, N > ~23.7K):
+    // each slot keeps only its entry's low 16 key bits, in SHARED memory after
+    // the coarse table (2 B per pixel, S <= 192: 221 KB in all); a thread
+    // holds (bucket << 16 | slot) per pixel and ranks its own pixels against
+    // the bucket's slots (ties by slot), so the bucket entries never go
+    // through the global scratch slot (whose scattered stores and dependent
+    // L2 reads bound this kernel: profiles/ncu_k1_f32_c3r64_r2*).
+    constexpr bool OWN16 = GENT && !EDGE;
+    uint16_t* l16 = reinterpret_cast<uint16_t*>(ctab + kCoarse);
     // interior tiles with adaptive (~2-key) buckets rank their own register
-    // pixels (lanes in different buckets: fine while buckets are that small;
-    // NK = 6 would spill); others rank slot-parallel over a start bitmap
-    const bool own_rank = !EDGE && NK <= 5 && adaptive;
+    // pixels (lanes in different buckets: fine while buckets are that small);
+    // others rank slot-parallel over a start bitmap
+    const bool own_rank = !EDGE && (NK <= 5 || OWN16) && adaptive;
     __shared__ unsigned long long s_sumsq;
     __shared__ int s_runs;
     __shared__ RunList s_rl;
@@ -762,8 +771,14 @@ __device__ __forceinline__ void f32_bucket_tile(const Geom& g, const TileCoord& 
                 const uint32_t key = v[j][k], h = key >> 16, sh = (h & 1) << 4;
                 const int wt = weight(j, k);
                 const uint32_t old = atomicAdd(&hw[h >> 1], (uint32_t)wt << sh);
-                put_entry(ent, d16, (old >> sh) & 0xffffu, key & 0xffffu, lane + 32 * k, wid + 32 * j, wt,
-                          cnt_x(k), cnt_y(j), &s_rl);
+                if (OWN16 && own_rank) {
+                    const uint32_t slot = (old >> sh) & 0xffffu;
+                    l16[slot] = (uint16_t)(key & 0xffffu);
+                    v[j][k] = (h << 16) | slot;
+                } else {
+                    put_entry(ent, d16, (old >> sh) & 0xffffu, key & 0xffffu, lane + 32 * k, wid + 32 * j, wt,
+                              cnt_x(k), cnt_y(j), &s_rl);
+                }
             }
     __syncthreads();
     uint16_t* om = reinterpret_cast<uint16_t*>(hw);  // the histogram is dead: omega goes here
@@ -776,11 +791,20 @@ __device__ __forceinline__ void f32_bucket_tile(const Geom& g, const TileCoord& 
             for (int k = 0; k < NK; k++)
                 if ((okm >> (j * NK + k)) & 1ull) {
                     const uint32_t id = v[j][k] >> 16;
-                    const uint32_t e = (v[j][k] << 16) | (uint32_t)((lane + 32 * k) | ((wid + 32 * j) << 8));
                     const int b1 = (int)((hw[id >> 1] >> ((id & 1u) << 4)) & 0xffffu);
                     const int b0 = id ? (int)((hw[(id - 1) >> 1] >> (((id - 1) & 1u) << 4)) & 0xffffu) : 0;
                     int rk = b0;
-                    for (int q = b0; q < b1; q++) rk += ent[q] < e ? 1 : 0;
+                    if (OWN16) {
+                        const int slot = (int)(v[j][k] & 0xffffu);
+                        const uint32_t my = l16[slot];
+                        for (int q = b0; q < b1; q++) {
+                            const uint32_t l = l16[q];
+                            rk += (l < my || (l == my && q < slot)) ? 1 : 0;
+                        }
+                    } else {
+                        const uint32_t e = (v[j][k] << 16) | (uint32_t)((lane + 32 * k) | ((wid + 32 * j) << 8));
+                        for (int q = b0; q < b1; q++) rk += ent[q] < e ? 1 : 0;
+                    }
                     v[j][k] = (uint32_t)rk;
                 }
         __syncthreads();
