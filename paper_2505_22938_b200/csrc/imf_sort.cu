@@ -512,7 +512,7 @@ __device__ __forceinline__ void mark_runs(uint32_t* ent, const RunList* rl) {
 // omega.  RUNS: the (entry | 1, slot) order above; the head of a run writes
 // its w ranks (long runs: queued for fill_big_runs).
 #ifdef IMF_STATS
-__device__ unsigned long long g_rstats[128];  // [0, 64): bucket span per ranked entry (dev aid)
+__device__ unsigned long long g_rstats[128];  // [64 + 2k], k < 12: phase cycles  // [0, 64): bucket span per ranked entry (dev aid)
 // [64 + 2k]: sum, [65 + 2k]: max over CTAs of phase k's clock cycles (thread 0)
 #define PHASE_T0 long long _t0 = clock64()
 #define PHASE(k)                                                              \
@@ -674,6 +674,7 @@ __device__ __forceinline__ void f32_bucket_tile(const Geom& g, const TileCoord& 
     // replicate copies (rep_axis), edge tiles only, recomputed where used
     // (keeps the 1024-thread register budget for the keys)
     const int X0 = tc.ox0 - g.r + g.vshift, Y0 = tc.oy0 - g.r + g.vshift;
+    PHASE_T0;
     auto weight = [&](int j, int k) {
         if (!EDGE) return 1;
         int cx, cy;
@@ -727,6 +728,7 @@ __device__ __forceinline__ void f32_bucket_tile(const Geom& g, const TileCoord& 
         }
     }
     __syncthreads();
+    PHASE(6);
     if (adaptive) {  // keys -> fine bucket << 16 | low 16 key bits
         if (!g.ctab_g) {  // no call-wide table: this tile's own coarse pass
 #pragma unroll
@@ -755,8 +757,10 @@ __device__ __forceinline__ void f32_bucket_tile(const Geom& g, const TileCoord& 
             }
     if (runs) s_runs = 1;
     __syncthreads();
+    PHASE(7);
     hist16_exclusive_scan(hw, NW, own_rank ? nullptr : starts, &s_sumsq);
     __syncthreads();
+    PHASE(8);
     // tiles with runs skip the estimate (run weights inflate it); their scans
     // are budgeted instead (rank_buckets)
     if (!s_runs && s_sumsq > max_sumsq) {  // block-uniform: hand the tile to the radix sort
@@ -781,6 +785,7 @@ __device__ __forceinline__ void f32_bucket_tile(const Geom& g, const TileCoord& 
                 }
             }
     __syncthreads();
+    PHASE(9);
     uint16_t* om = reinterpret_cast<uint16_t*>(hw);  // the histogram is dead: omega goes here
     if (own_rank) {
         // each thread ranks its own pixels: the counters now hold every bucket's
@@ -808,6 +813,7 @@ __device__ __forceinline__ void f32_bucket_tile(const Geom& g, const TileCoord& 
                     v[j][k] = (uint32_t)rk;
                 }
         __syncthreads();
+        PHASE(10);
 #pragma unroll
         for (int j = 0; j < NK; j++)
 #pragma unroll
@@ -816,6 +822,7 @@ __device__ __forceinline__ void f32_bucket_tile(const Geom& g, const TileCoord& 
         for (int i = N + tid; i < g.Npad; i += blockDim.x) om[i] = 0xffffu;
         __syncthreads();
         store_omega(g, om, omega_slot(g, omega_out));
+        PHASE(11);
         return;
     }
     mark_runs(ent, &s_rl);

@@ -45,7 +45,7 @@ for ln in lines_all[start + 1:]:
         break
     locs = re.findall(r'File "([^"]+)", line (\d+)', ln)
     if locs:
-        f, l = locs[-1]  # outermost (kernel-body) location of an inlined chain
+        f, l = locs[0] if os.environ.get("NCU_INNER") else locs[-1]  # outermost (kernel-body) location of an inlined chain (NCU_INNER=1: innermost)
         cur = (os.path.basename(f), int(l))
         continue
     m = re.match(r"\s*/\*([0-9a-f]{4,})\*/", ln)
