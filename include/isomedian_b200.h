@@ -154,6 +154,22 @@ uint64_t imf_launch_count(void);        /* kernels launched by this process (dia
 int imf_profile_last(float* sort_ms, float* select_ms, int32_t* launches, int64_t* tiles,
                      int32_t* tile_side, int32_t* qshift);
 
+/*
+ * Ordinal transform of ONE tile (device-side counterpart of the reference's
+ * per-tile ordinal_transform, ordinal.py:126-172; for invariant checks as in
+ * the reference's test_ordinal.py): runs the call's K1 on tile `tile` (index
+ * as the filter enumerates them: x fastest, then y, channel, image) and copies
+ * its omega -- the rank -> position map, x | y << 8 in input-tile coordinates
+ * -- to host memory omega[0..N).  Only the tile's footprint is ranked (when
+ * the planner uses one); ties are in arbitrary order (output-neutral for the
+ * filter).  info[8] receives N, the input tile's image origin x0, y0 (before
+ * clamping: replicate tiles read clamp(x0 + x), clamp(y0 + y)), its extent
+ * Sw, Sh, channel, image, and whether a footprint was applied.  Synchronous.
+ */
+int imf_tile_omega(const imf_image* src, const imf_kernel* kernel, const imf_options* opt, int64_t tile,
+                   uint16_t* omega, int32_t capacity, int32_t* info, void* workspace, size_t workspace_bytes,
+                   void* stream);
+
 /* Kernel paths the last imf_filter / imf_filter_bracket on this thread took
  * (diagnostic): IMF_FEATURE_K1_TMA = the ordinal transform loaded its tile
  * boxes with TMA (cp.async.bulk.tensor). */

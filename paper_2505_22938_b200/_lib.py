@@ -25,7 +25,7 @@ IMF_ERR_UNSUPPORTED = 5
 EXPORTED = ("imf_workspace_size", "imf_filter", "imf_filter_bracket", "imf_workspace_status",
             "imf_filter_host",
             "imf_strerror", "imf_version", "imf_last_error", "imf_launch_count",
-            "imf_profile_last", "imf_int_peak", "imf_last_features")
+            "imf_profile_last", "imf_int_peak", "imf_last_features", "imf_tile_omega")
 
 _i32p = ctypes.POINTER(ctypes.c_int32)
 
@@ -96,6 +96,10 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.imf_int_peak.restype = ctypes.c_int
     lib.imf_last_features.argtypes = []
     lib.imf_last_features.restype = ctypes.c_uint32
+    lib.imf_tile_omega.argtypes = [P(ImfImage), P(ImfKernel), P(ImfOptions), ctypes.c_int64, ctypes.c_void_p,
+                                   ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t,
+                                   ctypes.c_void_p]
+    lib.imf_tile_omega.restype = ctypes.c_int
     return lib
 
 

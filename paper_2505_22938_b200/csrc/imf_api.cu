@@ -610,6 +610,36 @@ size_t imf_workspace_size(const imf_image* src, const imf_kernel* kernel, const 
 
 }  // extern "C"
 
+// Device-side inputs of K1 for a call: the launch geometry, the footprint
+// table (uploaded into the workspace), the call-wide f32 coarse bucket table
+// (k_coarse_hist / k_coarse_alloc), and the TMA descriptor of planar tiles.
+static int prep_k1(const Plan& p, const imf_image* src, unsigned char* ws, cudaStream_t s, Geom& g,
+                   CUtensorMap& tmap, bool& use_tma) {
+    g = p.g;
+    g.src = src->data;
+    g.ctab_g = nullptr;
+    g.fprow = nullptr;
+    if (g.fp) {  // footprint rows into the workspace (the copy is staged at call time)
+        uint32_t* d = (uint32_t*)(ws + kFpOffset);
+        if (cudaError_t e = cudaMemcpyAsync(d, p.fprow, 4 * (size_t)g.Sh, cudaMemcpyHostToDevice, s))
+            return cuda_fail(e, "footprint table upload");
+        g.fprow = d;
+    }
+    if (p.ws_ctab && p.ct_y1 > p.ct_y0) {
+        uint32_t* ct = (uint32_t*)(ws + kStatusBytes + p.lanes * p.ws_lane);
+        if (cudaError_t e = cudaMemsetAsync(ct, 0, p.ws_ctab, s)) return cuda_fail(e, "coarse table memset");
+        const long long rows = (long long)(p.ct_y1 - p.ct_y0) * g.B * g.C;
+        const int cgrid = (int)std::min<long long>(296, (rows + 31) / 32);
+        k_coarse_hist<<<cgrid, 1024, 0, s>>>(g, p.ct_y0, p.ct_y1, ct);
+        k_coarse_alloc<<<1, 1024, 0, s>>>(ct);
+        g_launches += 2;
+        g.ctab_g = ct;
+    }
+    use_tma = p.k1_tma && make_k1_tmap(g, src->data, &tmap);
+    g_last_tma = use_tma;
+    return IMF_OK;
+}
+
 // One K1 (ordinal transform) per chunk of tiles, then one K2 (selection) per
 // requested output: n scalar targets (the "bracket", core.py:412-426) reuse
 // the same omega.  n == 1 with an optional per-pixel target map is imf_filter.
@@ -683,29 +713,10 @@ static int filter_impl(const imf_image* src, imf_image* dsts, int n, const int32
     if (!(opt->flags & IMF_FLAG_KEEP_STATUS))
         if (cudaError_t e = cudaMemsetAsync(status, 0, sizeof(int), s)) return cuda_fail(e, "status memset");
 
-    Geom g = p.g;
-    g.src = src->data;
-    g.ctab_g = nullptr;
-    g.fprow = nullptr;
-    if (g.fp) {  // footprint rows into the workspace (the copy is staged at call time)
-        uint32_t* d = (uint32_t*)(ws + kFpOffset);
-        if (cudaError_t e = cudaMemcpyAsync(d, p.fprow, 4 * (size_t)g.Sh, cudaMemcpyHostToDevice, s))
-            return cuda_fail(e, "footprint table upload");
-        g.fprow = d;
-    }
-    if (p.ws_ctab && p.ct_y1 > p.ct_y0) {
-        uint32_t* ct = (uint32_t*)(ws + kStatusBytes + p.lanes * p.ws_lane);
-        if (cudaError_t e = cudaMemsetAsync(ct, 0, p.ws_ctab, s)) return cuda_fail(e, "coarse table memset");
-        const long long rows = (long long)(p.ct_y1 - p.ct_y0) * g.B * g.C;
-        const int cgrid = (int)std::min<long long>(296, (rows + 31) / 32);
-        k_coarse_hist<<<cgrid, 1024, 0, s>>>(g, p.ct_y0, p.ct_y1, ct);
-        k_coarse_alloc<<<1, 1024, 0, s>>>(ct);
-        g_launches += 2;
-        g.ctab_g = ct;
-    }
+    Geom g;
     CUtensorMap k1_tmap;
-    const bool use_tma = p.k1_tma && make_k1_tmap(g, src->data, &k1_tmap);
-    g_last_tma = use_tma;
+    bool use_tma = false;
+    if (int e = prep_k1(p, src, ws, s, g, k1_tmap, use_tma)) return e;
 
     SelParams sp;
     memset(&sp, 0, sizeof(sp));
@@ -887,6 +898,54 @@ int imf_profile_last(float* sort_ms, float* select_ms, int32_t* launches, int64_
 }
 
 uint32_t imf_last_features(void) { return g_last_tma ? IMF_FEATURE_K1_TMA : 0u; }
+
+int imf_tile_omega(const imf_image* src, const imf_kernel* kernel, const imf_options* opt, int64_t tile,
+                   uint16_t* omega, int32_t capacity, int32_t* info, void* workspace, size_t workspace_bytes,
+                   void* stream) {
+    if (!src || !kernel || !opt || !src->data || !omega || !info) return IMF_ERR_INVALID;
+    Plan p;
+    if (int st = make_plan(src, kernel, opt, &p)) return st;
+    if (p.direct) return IMF_ERR_UNSUPPORTED;  // tiny windows: no ordinal transform
+    if (tile < 0 || tile >= p.total_tiles) return IMF_ERR_INVALID;
+    if (!workspace || workspace_bytes < p.ws_total) return IMF_ERR_WORKSPACE;
+    if (capacity < p.g.N) return IMF_ERR_INVALID;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (cudaError_t e = set_attrs()) return cuda_fail(e, "cudaFuncSetAttribute");
+    unsigned char* ws = (unsigned char*)workspace;
+    Geom g;
+    CUtensorMap tmap;
+    bool use_tma = false;
+    if (int e = prep_k1(p, src, ws, s, g, tmap, use_tma)) return e;
+    g.tile_begin = tile;
+    unsigned char* lane = ws + kStatusBytes;
+    launch_k1(p, g, 1, (uint16_t*)lane, lane + p.ws_omega, (int*)(lane + p.ws_omega + p.ws_k1g), s,
+              use_tma ? &tmap : nullptr);
+    if (cudaError_t e = cudaGetLastError()) return cuda_fail(e, "K1 launch");
+    if (cudaError_t e = cudaMemcpyAsync(omega, (uint16_t*)lane + OMEGA_SLOT_PAD, 2 * (size_t)p.g.N,
+                                        cudaMemcpyDeviceToHost, s))
+        return cuda_fail(e, "omega download");
+    if (cudaError_t e = cudaStreamSynchronize(s)) return cuda_fail(e, "stream synchronize");
+    // the tile's input origin (image coordinates of input-tile pixel (0, 0),
+    // before clamping; tile_coord on the host) and its input extent
+    const Geom& q = p.g;
+    long long t = tile;
+    const int tx = (int)(t % q.tiles_x);
+    t /= q.tiles_x;
+    const int ty = (int)(t % q.tiles_y);
+    t /= q.tiles_y;
+    const int c = (int)(t % q.C), b = (int)(t / q.C);
+    const int oy0 = q.oy_base + std::min(ty * q.Th, std::max(q.out_h - q.oy_base - q.Th, 0));
+    const int ox0 = std::min(tx * q.Tw, std::max(q.out_w - q.Tw, 0));
+    info[0] = q.N;
+    info[1] = ox0 - q.r + q.vshift;
+    info[2] = oy0 - q.r + q.vshift;
+    info[3] = q.Sw;
+    info[4] = q.Sh;
+    info[5] = c;
+    info[6] = b;
+    info[7] = q.fp;
+    return IMF_OK;
+}
 
 int imf_workspace_status(void* workspace, void* stream) {
     int h = 0;
