@@ -508,6 +508,18 @@ def run_ours(args):
     traffic, tsrc = load_ncu_traffic(args.workload)
     if args.radius is not None:  # the committed captures are at the configs' own radii
         traffic, tsrc = None, "no ncu capture at this radius"
+    # the same K2 launch without ncu's L2 flush (omega still in L2 from K1, as
+    # in the pipelined bench): profiles/ncu_k2_traffic_<workload>_r<N>.json
+    traffic_pipe = None
+    import glob
+    tf = sorted(glob.glob(os.path.join(ROOT, "profiles", f"ncu_k2_traffic_{args.workload}_r*.json")))
+    if tf and args.radius is None:
+        try:
+            with open(tf[-1]) as f:
+                td = json.load(f)
+            traffic_pipe = next(v["dram_bytes_per_launch"] for k, v in td.items() if k.startswith("no_flush"))
+        except (OSError, ValueError, StopIteration, KeyError, TypeError):
+            traffic_pipe = None
     im0 = images[0]
     line = {
         "metric": "megapixels/sec circular median (r=8..100, 8/16-bit/f32)",
@@ -535,7 +547,8 @@ def run_ours(args):
                      "work_per_chpx": W,
                      "peak_source": "measured on this GPU: imf_int_peak (IADD3 chains)",
                      "path_frac": round(ch_value * 1e6 * W / peak.value, 4),
-                     "traffic": traffic, "traffic_source": tsrc},
+                     "traffic": traffic, "traffic_source": tsrc,
+                     "traffic_no_l2_flush": traffic_pipe},
         "clocks": clk.summary(),
         "parity_digest_ok": parity,
     }
