@@ -427,26 +427,6 @@ struct Pend {
     bool ok;
 };
 
-__device__ __forceinline__ Pend gather_out(const Geom& g, const TileCoord& tc, const uint16_t* om, int m, int row,
-                                           int col) {
-    Pend o;
-    const int oy = tc.oy0 + row, ox = tc.ox0 + col;
-    o.ok = oy < g.out_h && ox < g.out_w;
-    o.d = tc.b * g.d_b + (long long)oy * g.d_y + (long long)ox * g.d_x + tc.c * g.d_c;
-    o.v = 0;
-    if (o.ok) {
-        const uint32_t e = om[m];
-        const long long so = src_offset(g, tc, (int)(e >> 8), (int)(e & 0xff));
-        if (g.dtype == DT_U8)
-            o.v = __ldg((const uint8_t*)tc.src + so);
-        else if (g.dtype == DT_U16)
-            o.v = __ldg((const uint16_t*)tc.src + so);
-        else
-            o.v = __ldg((const uint32_t*)tc.src + so);
-    }
-    return o;
-}
-
 __device__ __forceinline__ void store_out(const Geom& g, const Pend& o) {
     if (!o.ok) return;
     if (g.dtype == DT_U8)
@@ -455,6 +435,41 @@ __device__ __forceinline__ void store_out(const Geom& g, const Pend& o) {
         ((uint16_t*)g.dst)[o.d] = (uint16_t)o.v;
     else
         ((uint32_t*)g.dst)[o.d] = o.v;
+}
+
+// Phase-D output path of one thread: the pair's destination index advances by
+// one output row per step, and the source of C[m] -- input-tile pixel (x, y)
+// of omega[m] -- is base + y*s_y + x*s_x with 32-bit strides when the tile's
+// input box lies inside the image (no clamp; src_offset otherwise).
+struct PairOut {
+    long long d;        // destination element index of window A at the current row
+    long long dx;       // destination stride between A and B (one output column)
+    long long drow;     // destination stride of one output row
+    long long sbase;    // interior tiles: element offset of input-tile pixel (0, 0)
+    int sy, sx;         // interior tiles: 32-bit source strides
+    bool interior;
+    bool okA, okB;      // the pair's columns lie inside the output
+};
+
+__device__ __forceinline__ Pend gather_pair(const Geom& g, const TileCoord& tc, const PairOut& po,
+                                            const uint16_t* om, int m, bool okrow, bool okcol,
+                                            long long d) {
+    Pend o;
+    o.ok = okrow && okcol;
+    o.d = d;
+    o.v = 0;
+    if (o.ok) {
+        const uint32_t e = om[m];
+        const int ly = (int)(e >> 8), lx = (int)(e & 0xff);
+        const long long so = po.interior ? po.sbase + (ly * po.sy + lx * po.sx) : src_offset(g, tc, ly, lx);
+        if (g.dtype == DT_U8)
+            o.v = __ldg((const uint8_t*)tc.src + so);
+        else if (g.dtype == DT_U16)
+            o.v = __ldg((const uint16_t*)tc.src + so);
+        else
+            o.v = __ldg((const uint32_t*)tc.src + so);
+    }
+    return o;
 }
 
 __device__ __forceinline__ int target_at2(const Geom& g, const PairParams& p, const TileCoord& tc, int row,
@@ -847,10 +862,25 @@ __global__ void __launch_bounds__(512, 2) k2_pair(Geom g, PairParams p, const __
         int PA, cA, PB, cB;
         to_state<SHAPE>(c, hs, mA0, st_C[gi * T + j0], j0 + r, row0 + r, PA, cA);
         to_state<SHAPE>(c, hs, mB0, st_C[gi * T + j1], j1 + r, row0 + r, PB, cB);
+        PairOut po;
+        {
+            const int X0 = tc.ox0 - r + g.vshift, Y0 = tc.oy0 - r + g.vshift;
+            po.interior = X0 >= 0 && Y0 >= 0 && X0 + Sw <= g.W && Y0 + g.Sh <= g.H &&
+                          (long long)(g.H - 1) * g.s_y + (long long)(g.W - 1) * g.s_x < (1ll << 31);
+            po.sbase = (long long)Y0 * g.s_y + (long long)X0 * g.s_x;
+            po.sy = (int)g.s_y;
+            po.sx = (int)g.s_x;
+            po.dx = g.d_x;
+            po.drow = g.d_y;
+            po.d = tc.b * g.d_b + tc.c * g.d_c + (long long)(tc.oy0 + row0) * g.d_y + (long long)(tc.ox0 + j0) * g.d_x;
+            po.okA = tc.ox0 + j0 < g.out_w;
+            po.okB = tc.ox0 + j1 < g.out_w;
+        }
         Pend wa{0, 0, false}, wb{0, 0, false};
         if (down) {
-            wa = gather_out(g, tc, om, mA0, row0, j0);
-            wb = gather_out(g, tc, om, mB0, row0, j1);
+            const bool okr = tc.oy0 + row0 < g.out_h;
+            wa = gather_pair(g, tc, po, om, mA0, okr, po.okA, po.d);
+            wb = gather_pair(g, tc, po, om, mB0, okr, po.okB, po.d + po.dx);
         }
         const int nsteps = down ? (rend - 1 - row0) : (row0 - gi * R);
         int row = row0;
@@ -885,8 +915,10 @@ __global__ void __launch_bounds__(512, 2) k2_pair(Geom g, PairParams p, const __
                 mA = max(mA, 0);
                 mB = max(mB, 0);
             }
-            wa = gather_out(g, tc, om, mA, row, j0);
-            wb = gather_out(g, tc, om, mB, row, j1);
+            po.d += down ? po.drow : -po.drow;
+            const bool okr = tc.oy0 + row < g.out_h;
+            wa = gather_pair(g, tc, po, om, mA, okr, po.okA, po.d);
+            wb = gather_pair(g, tc, po, om, mB, okr, po.okB, po.d + po.dx);
             to_state<SHAPE>(c, hs, mA, tA, j0 + r, row + r, PA, cA);
             to_state<SHAPE>(c, hs, mB, tB, j1 + r, row + r, PB, cB);
         }
