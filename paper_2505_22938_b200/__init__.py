@@ -14,7 +14,7 @@ everything else in one CUDA extension behind a C ABI
 from .kernels import (MAX_POLYGON_SIDES, MAX_RADIUS, KernelShape, ShapeSpec, contains,
                       make_kernel, target_rank)
 from .netpbm import read_image, write_image
-from .shard import filter_multi
+from .shard import filter_batch_multi, filter_multi
 from .tiling import (FilterParams, ScanDefectError, Tile, TileGrid, decompose, filter_batch,
                      filter_image, filter_image_bracket, pad_image)
 
@@ -23,7 +23,7 @@ __all__ = [
     "MAX_RADIUS", "MAX_POLYGON_SIDES",
     "FilterParams", "ScanDefectError", "Tile", "TileGrid", "decompose", "filter_image",
     "filter_batch", "filter_image_bracket", "pad_image", "float_order_key",
-    "read_image", "write_image", "filter_multi",
+    "read_image", "write_image", "filter_multi", "filter_batch_multi",
 ]
 
 __version__ = "0.1.0"

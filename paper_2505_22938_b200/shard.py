@@ -168,3 +168,48 @@ def filter_multi(images, params, devices=None, *, batched: bool = False, out=Non
     if errors:
         raise errors[0]
     return o
+
+
+def filter_batch_multi(images, params, devices=None, *, out=None):
+    """Filter a CUDA batch (B, H, W[, C]) that lives on ONE GPU using several
+    GPUs (a device-resident batch is scattered to its peers over
+    NVLink / NVSwitch by peer copies -- no NCCL -- filtered in place there, and
+    gathered back).  Whole images per device, contiguous blocks; each device
+    works on its own stream, so the copies of one device overlap the kernels of
+    another.  `devices` defaults to every visible GPU; the batch's own device
+    keeps the first block without copies."""
+    import torch
+
+    from .tiling import filter_batch
+
+    if not (isinstance(images, torch.Tensor) and images.is_cuda and images.dim() >= 3):
+        raise ValueError("filter_batch_multi expects a CUDA batch (B, H, W[, C])")
+    home = images.device
+    if devices is None:
+        devices = list(range(torch.cuda.device_count()))
+    devices = [torch.device("cuda", d) if isinstance(d, int) else torch.device(d) for d in devices]
+    if not devices:
+        raise RuntimeError("filter_batch_multi needs at least one CUDA device")
+    nb = images.shape[0]
+    cuts = [nb * i // len(devices) for i in range(len(devices) + 1)]
+    parts = []
+    for d, b0, b1 in zip(devices, cuts[:-1], cuts[1:]):
+        if b1 <= b0:
+            continue
+        stream = torch.cuda.Stream(device=d)
+        stream.wait_stream(torch.cuda.current_stream(home))  # the batch is ready
+        with torch.cuda.device(d), torch.cuda.stream(stream):
+            src = images[b0:b1].to(d, non_blocking=True)   # peer copy (NVLink) when d != home
+            res = filter_batch(src, params, check=True, stream=stream)
+            parts.append((b0, b1, res, stream, src))
+    if out is None:
+        out = torch.empty_like(images) if params.boundary != "valid" else None
+    chunks = []
+    for b0, b1, res, stream, src in parts:
+        stream.synchronize()
+        chunks.append((b0, b1, res))
+    if out is None:
+        return torch.cat([res.to(home) for _, _, res in sorted(chunks, key=lambda c: c[0])])
+    for b0, b1, res in chunks:
+        out[b0:b1].copy_(res.to(home))
+    return out

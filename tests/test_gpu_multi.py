@@ -170,3 +170,18 @@ def test_k1_tma_tile_loads(dt, r, boundary):
         for b in range(3):
             assert np.array_equal(out[b], oracle.fast_filter(host[b], params.shape, 0.5, boundary)), b
     assert seen_tma  # the aligned layouts did take the TMA path
+
+
+@pytest.mark.parametrize("boundary", ["replicate", "valid"])
+def test_filter_batch_multi_device_resident(boundary):
+    """A device-resident batch scattered to peers (here: cuda:0 listed twice)
+    and gathered back equals the single-device batch result."""
+    import torch
+    from paper_2505_22938_b200 import filter_batch, filter_batch_multi
+    FilterParams, ShapeSpec, _ = _api()
+    imgs = torch.from_numpy(np.random.default_rng(39).integers(0, 65536, (5, 170, 190, 3),
+                                                               dtype=np.uint16)).cuda()
+    params = FilterParams(shape=ShapeSpec("circle", 11), boundary=boundary)
+    got = filter_batch_multi(imgs, params, devices=[0, 0])
+    want = filter_batch(imgs, params)
+    assert torch.equal(got, want)
