@@ -416,6 +416,21 @@ __device__ __forceinline__ void refine8x2_seq(const PairCtx& c, int cx, int cy, 
         }
     }
     mB = walk_result(c, w);
+#ifdef IMF_STATS
+    // [128..]: pairs, same direction, sum |PA-PB|, sum |mA-PA|, sum |mB-PB|, sum union length (same dir)
+    {
+        const bool upA = cntA <= tA, upB = cntB <= tB;
+        atomicAdd(&g_stats[128], 1ull);
+        if (upA == upB) {
+            atomicAdd(&g_stats[129], 1ull);
+            const int lo = min(min(PA, PB), min(mA, mB)), hi = max(max(PA, PB), max(mA, mB));
+            atomicAdd(&g_stats[133], (unsigned long long)(hi - lo));
+        }
+        atomicAdd(&g_stats[130], (unsigned long long)abs(PA - PB));
+        atomicAdd(&g_stats[131], (unsigned long long)abs(mA - PA));
+        atomicAdd(&g_stats[132], (unsigned long long)abs(mB - PB));
+    }
+#endif
 }
 
 // Gather C[m] (the input value at omega[m]'s position, core.py:366) and the

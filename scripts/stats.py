@@ -26,3 +26,8 @@ print("lane iterations per window pair: mean %.2f" % ((lane * i).sum() / lane.su
 print("warp trip count per pair-step:   mean %.2f  (lane efficiency %.2f)" % ((warp * i).sum() / warp.sum(), (lane * i).sum() / lane.sum() / ((warp * i).sum() / warp.sum())))
 print("lane hist:", {int(k): int(v) for k, v in zip(i, lane) if v})
 print("warp hist:", {int(k): int(v) for k, v in zip(i, warp) if v})
+
+x = np.array(buf[128:134], dtype=np.float64)
+if x[0]:
+    print("pairs %d  same direction %.3f  mean |PA-PB| %.1f  mean walk A %.1f  B %.1f ranks  mean union (same dir) %.1f"
+          % (x[0], x[1] / x[0], x[2] / x[0], x[3] / x[0], x[4] / x[0], x[5] / max(x[1], 1)))
