@@ -670,7 +670,10 @@ __device__ __forceinline__ void f32_bucket_tile(const Geom& g, const TileCoord& 
     __shared__ int s_runs;
     __shared__ RunList s_rl;
     uint32_t v[NK][NK];
-    unsigned long long okm = 0;  // which of this thread's pixels are ranked (weight > 0)
+    // which of this thread's pixels are ranked: a mask for edge tiles (weights
+    // are costly to recompute), recomputed from the tile extent elsewhere (no
+    // registers held: the 1024-thread budget is 64 per thread)
+    unsigned long long okm = 0;
     // replicate copies (rep_axis), edge tiles only, recomputed where used
     // (keeps the 1024-thread register budget for the keys)
     const int X0 = tc.ox0 - g.r + g.vshift, Y0 = tc.oy0 - g.r + g.vshift;
@@ -682,6 +685,10 @@ __device__ __forceinline__ void f32_bucket_tile(const Geom& g, const TileCoord& 
         rep_axis(X0, lane + 32 * k, S, g.W, cx, fx);
         rep_axis(Y0, wid + 32 * j, SH, g.H, cy, fy);
         return pixel_weight(cx, fx, cy, fy, g.run_min);
+    };
+    auto okf = [&](int j, int k) -> bool {
+        if (EDGE) return (okm >> (j * NK + k)) & 1ull;
+        return wid + 32 * j < SH && lane + 32 * k < S && in_footprint(g, lane + 32 * k, wid + 32 * j);
     };
     auto cnt_x = [&](int k) {
         int c;
@@ -711,7 +718,7 @@ __device__ __forceinline__ void f32_bucket_tile(const Geom& g, const TileCoord& 
             for (int k = 0; k < NK; k++) {
                 const bool ok = y < SH && lane + 32 * k < S && in_footprint(g, lane + 32 * k, y) && weight(j, k) > 0;
                 v[j][k] = ok ? f32_key(g, tc, yy, xc[k]) : 0u;
-                okm |= (ok ? 1ull : 0ull) << (j * NK + k);
+                if (EDGE) okm |= (ok ? 1ull : 0ull) << (j * NK + k);
             }
         }
     }
@@ -735,21 +742,21 @@ __device__ __forceinline__ void f32_bucket_tile(const Geom& g, const TileCoord& 
             for (int j = 0; j < NK; j++)
 #pragma unroll
                 for (int k = 0; k < NK; k++)
-                    if ((okm >> (j * NK + k)) & 1ull) atomicAdd(&ctab[v[j][k] >> 20], (uint32_t)weight(j, k));
+                    if (okf(j, k)) atomicAdd(&ctab[v[j][k] >> 20], (uint32_t)weight(j, k));
             coarse_alloc(ctab, N);
         }
 #pragma unroll
         for (int j = 0; j < NK; j++)
 #pragma unroll
             for (int k = 0; k < NK; k++)
-                if ((okm >> (j * NK + k)) & 1ull) v[j][k] = (fine_bucket(ctab, v[j][k]) << 16) | (v[j][k] & 0xffffu);
+                if (okf(j, k)) v[j][k] = (fine_bucket(ctab, v[j][k]) << 16) | (v[j][k] & 0xffffu);
     }
     bool runs = false;
 #pragma unroll
     for (int j = 0; j < NK; j++)
 #pragma unroll
         for (int k = 0; k < NK; k++)
-            if ((okm >> (j * NK + k)) & 1ull) {
+            if (okf(j, k)) {
                 const uint32_t h = v[j][k] >> 16, sh = (h & 1) << 4;
                 const int wt = weight(j, k);
                 runs |= wt > 1;
@@ -771,7 +778,7 @@ __device__ __forceinline__ void f32_bucket_tile(const Geom& g, const TileCoord& 
     for (int j = 0; j < NK; j++)
 #pragma unroll
         for (int k = 0; k < NK; k++)
-            if ((okm >> (j * NK + k)) & 1ull) {
+            if (okf(j, k)) {
                 const uint32_t key = v[j][k], h = key >> 16, sh = (h & 1) << 4;
                 const int wt = weight(j, k);
                 const uint32_t old = atomicAdd(&hw[h >> 1], (uint32_t)wt << sh);
@@ -794,7 +801,7 @@ __device__ __forceinline__ void f32_bucket_tile(const Geom& g, const TileCoord& 
         for (int j = 0; j < NK; j++)
 #pragma unroll
             for (int k = 0; k < NK; k++)
-                if ((okm >> (j * NK + k)) & 1ull) {
+                if (okf(j, k)) {
                     const uint32_t id = v[j][k] >> 16;
                     const int b1 = (int)((hw[id >> 1] >> ((id & 1u) << 4)) & 0xffffu);
                     const int b0 = id ? (int)((hw[(id - 1) >> 1] >> (((id - 1) & 1u) << 4)) & 0xffffu) : 0;
@@ -818,7 +825,7 @@ __device__ __forceinline__ void f32_bucket_tile(const Geom& g, const TileCoord& 
         for (int j = 0; j < NK; j++)
 #pragma unroll
             for (int k = 0; k < NK; k++)
-                if ((okm >> (j * NK + k)) & 1ull) om[v[j][k]] = (uint16_t)((lane + 32 * k) | ((wid + 32 * j) << 8));
+                if (okf(j, k)) om[v[j][k]] = (uint16_t)((lane + 32 * k) | ((wid + 32 * j) << 8));
         for (int i = N + tid; i < g.Npad; i += blockDim.x) om[i] = 0xffffu;
         __syncthreads();
         store_omega(g, om, omega_slot(g, omega_out));
