@@ -512,6 +512,32 @@ bool make_k1_tmap(const Geom& g, const void* data, CUtensorMap* tm) {
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// Host mirror of the f32 bucket K1's has_runs (imf_sort.cu) for tile t of a
+// call: tiles whose replicate-copy groups reach run_min (image corners) are
+// the slow ones; the chunk lists them so their CTAs start first.
+int host_max_copies(int X0, int S, int W) {
+    if (W == 1) return S;
+    const int l = X0 < 0 ? std::min(S, 1 - X0) : 1;
+    const int r = X0 + S > W ? S - std::max(0, W - 1 - X0) : 1;
+    return std::max(l, r);
+}
+
+void list_costly_tiles(const Plan& p, Geom& g, long long t0, int nb) {
+    g.nrt = 0;
+    if (!p.k1_f32b || g.fp) return;
+    const Geom& q = p.g;
+    for (int b = 0; b < nb && g.nrt < 16; b++) {
+        long long t = t0 + b;
+        const int tx = (int)(t % q.tiles_x);
+        t /= q.tiles_x;
+        const int ty = (int)(t % q.tiles_y);
+        const int oy0 = q.oy_base + std::min(ty * q.Th, std::max(q.out_h - q.oy_base - q.Th, 0));
+        const int ox0 = std::min(tx * q.Tw, std::max(q.out_w - q.Tw, 0));
+        const int X0 = ox0 - q.r + q.vshift, Y0 = oy0 - q.r + q.vshift;
+        if (host_max_copies(X0, q.Sw, q.W) * host_max_copies(Y0, q.Sh, q.H) >= q.run_min) g.rt[g.nrt++] = b;
+    }
+}
+
 void launch_k1(const Plan& p, const Geom& g, int nblocks, uint16_t* omega, unsigned char* k1g,
                int* flags, cudaStream_t s, const CUtensorMap* tm) {
     const dim3 grid(nblocks), block(p.k1_threads);
@@ -795,7 +821,9 @@ static int filter_impl(const imf_image* src, imf_image* dsts, int n, const int32
             cudaEventCreate(&e2);
             cudaEventRecord(e0, s);
         }
+        if (env_int("IMF_COSTLY_FIRST", 1)) list_costly_tiles(p, g, t0, nb);
         launch_k1(p, g, nb, omega, k1g, k1flags, s, use_tma ? &k1_tmap : nullptr);
+        g.nrt = 0;
         if (prof) cudaEventRecord(e1, s);
         for (int i = 0; i < n; i++) {
         g.dst = dsts[i].data;

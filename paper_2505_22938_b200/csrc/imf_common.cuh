@@ -38,6 +38,8 @@ struct Geom {
     const uint32_t* fprow;         // footprint rows: input-tile row y ranks columns [lo, hi], lo | hi << 16
                                    // (lo > hi: none); device memory (workspace), nullptr = whole tile
     int tma_bw;                    // K1 TMA box width (elements per box row) when the launch uses TMA
+    int nrt;                       // f32 bucket K1: chunk tiles with replicate runs (the costly ones),
+    int rt[16];                    //   run first: chunk-relative indices, ascending (chunk_tile)
     int run_min;                   // bucket K1: copy groups (replicate boundary) this large rank as one run
     const uint32_t* ctab_g;        // f32 bucket K1: call-wide fine-bucket table (k_coarse_*), or nullptr
     int tiles_x, tiles_y;
@@ -72,6 +74,17 @@ struct SelParams {
     int* status;         // device status word (1 = scan defect)
     int debug_defect;    // test hook (IMF_FLAG_DEBUG_DEFECT): corrupt one slide count in tile 0
 };
+
+// Chunk-relative tile of this CTA: the listed costly tiles (g.rt) first, then
+// the rest in order (the b-th unlisted index: step over each listed index <= it).
+__device__ __forceinline__ int chunk_tile(const Geom& g) {
+    int b = blockIdx.x;
+    if (b < g.nrt) return g.rt[b];
+    b -= g.nrt;
+    for (int i = 0; i < g.nrt; i++)
+        if (g.rt[i] <= b) b++;
+    return b;
+}
 
 __device__ __forceinline__ TileCoord tile_coord(const Geom& g, long long t64) {
     TileCoord tc;

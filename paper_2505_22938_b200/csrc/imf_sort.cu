@@ -637,7 +637,8 @@ __device__ void fill_big_runs(uint16_t* om, const RunList* rl) {
 // pixel are ranked as a run (pixel_weight).  Interior tiles take the EDGE =
 // false instance, which carries none of that.
 template <int NK, bool GENT, bool EDGE>
-__device__ __forceinline__ void f32_bucket_tile(const Geom& g, const TileCoord& tc, uint16_t* __restrict__ omega_out,
+__device__ __forceinline__ void f32_bucket_tile(const Geom& g, const TileCoord& tc, const int bt,
+                                                uint16_t* __restrict__ omega_out,
                                                 int* __restrict__ fallback, uint32_t* __restrict__ gent,
                                                 long long gent_stride, unsigned long long max_sumsq) {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -645,7 +646,7 @@ __device__ __forceinline__ void f32_bucket_tile(const Geom& g, const TileCoord& 
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int S = g.Sw, SH = g.Sh, N = g.N;
     uint32_t* hw = reinterpret_cast<uint32_t*>(smem);
-    uint32_t* ent = GENT ? gent + blockIdx.x * gent_stride : hw + NW;  // N entries
+    uint32_t* ent = GENT ? gent + bt * gent_stride : hw + NW;  // N entries
     // bucket starts, ceil(N/32) words; the coarse table (f32) aliases the
     // shared entries (dead until the scatter) or follows the starts
     uint32_t* starts = GENT ? hw + NW : ent + max((N + 3) & ~3, kCoarse);
@@ -771,7 +772,7 @@ __device__ __forceinline__ void f32_bucket_tile(const Geom& g, const TileCoord& 
     // tiles with runs skip the estimate (run weights inflate it); their scans
     // are budgeted instead (rank_buckets)
     if (!s_runs && s_sumsq > max_sumsq) {  // block-uniform: hand the tile to the radix sort
-        if (tid == 0) fallback[1 + atomicAdd(fallback, 1)] = blockIdx.x;
+        if (tid == 0) fallback[1 + atomicAdd(fallback, 1)] = bt;
         return;
     }
 #pragma unroll
@@ -828,13 +829,13 @@ __device__ __forceinline__ void f32_bucket_tile(const Geom& g, const TileCoord& 
                 if (okf(j, k)) om[v[j][k]] = (uint16_t)((lane + 32 * k) | ((wid + 32 * j) << 8));
         for (int i = N + tid; i < g.Npad; i += blockDim.x) om[i] = 0xffffu;
         __syncthreads();
-        store_omega(g, om, omega_slot(g, omega_out));
+        store_omega(g, om, omega_slot(g, omega_out, bt));
         PHASE(11);
         return;
     }
     mark_runs(ent, &s_rl);
     if (s_rl.abort) {  // run list overflow (block-uniform after the scatter barrier)
-        if (tid == 0) fallback[1 + atomicAdd(fallback, 1)] = blockIdx.x;
+        if (tid == 0) fallback[1 + atomicAdd(fallback, 1)] = bt;
         return;
     }
     if (s_runs)
@@ -843,24 +844,25 @@ __device__ __forceinline__ void f32_bucket_tile(const Geom& g, const TileCoord& 
         rank_buckets<false>(ent, d16, starts, N, om, &s_rl);
     __syncthreads();
     if (s_rl.abort) {  // a scan over budget (block-uniform after the barrier)
-        if (tid == 0) fallback[1 + atomicAdd(fallback, 1)] = blockIdx.x;
+        if (tid == 0) fallback[1 + atomicAdd(fallback, 1)] = bt;
         return;
     }
     fill_big_runs(om, &s_rl);
     for (int i = N + tid; i < g.Npad; i += blockDim.x) om[i] = 0xffffu;
     __syncthreads();
-    store_omega(g, om, omega_slot(g, omega_out));
+    store_omega(g, om, omega_slot(g, omega_out, bt));
 }
 
 template <int NK, bool GENT>
 __global__ void __launch_bounds__(1024) k1_f32_bucket(Geom g, uint16_t* __restrict__ omega_out,
                                                      int* __restrict__ fallback, uint32_t* __restrict__ gent,
                                                      long long gent_stride, unsigned long long max_sumsq) {
-    const TileCoord tc = tile_coord(g, g.tile_begin + blockIdx.x);
+    const int bt = chunk_tile(g);  // costly (replicate-run) tiles start first
+    const TileCoord tc = tile_coord(g, g.tile_begin + bt);
     if (has_runs(g, tc))
-        f32_bucket_tile<NK, GENT, true>(g, tc, omega_out, fallback, gent, gent_stride, max_sumsq);
+        f32_bucket_tile<NK, GENT, true>(g, tc, bt, omega_out, fallback, gent, gent_stride, max_sumsq);
     else
-        f32_bucket_tile<NK, GENT, false>(g, tc, omega_out, fallback, gent, gent_stride, max_sumsq);
+        f32_bucket_tile<NK, GENT, false>(g, tc, bt, omega_out, fallback, gent, gent_stride, max_sumsq);
 }
 
 // k1_f32_bucket for tiles too large for shared-memory entries (N > ~23.7K,
@@ -875,7 +877,8 @@ __global__ void __launch_bounds__(1024) k1_f32_bucket_g(Geom g, uint16_t* __rest
     extern __shared__ __align__(16) unsigned char smem[];
     constexpr int NW = 32768;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
-    const TileCoord tc = tile_coord(g, g.tile_begin + blockIdx.x);
+    const int bt = chunk_tile(g);  // costly (replicate-run) tiles start first
+    const TileCoord tc = tile_coord(g, g.tile_begin + bt);
     PHASE_T0;
     const int S = g.Sw, SH = g.Sh, N = g.N;
     uint32_t* hw = reinterpret_cast<uint32_t*>(smem);
@@ -883,7 +886,7 @@ __global__ void __launch_bounds__(1024) k1_f32_bucket_g(Geom g, uint16_t* __rest
     const int nsw = (N + 31) >> 5;
     uint32_t* ctab = starts + ((nsw + 3) & ~3);  // coarse bins / fine-bucket table (f32)
     const bool adaptive = g.dtype == DT_F32 && N > kAdaptiveMinN;
-    uint32_t* ent = gent + blockIdx.x * gent_stride;
+    uint32_t* ent = gent + bt * gent_stride;
     uint16_t* d16 = reinterpret_cast<uint16_t*>(ent + N);  // run descriptors (2 B / slot)
     __shared__ unsigned long long s_sumsq;
     __shared__ int s_runs;
@@ -959,7 +962,7 @@ __global__ void __launch_bounds__(1024) k1_f32_bucket_g(Geom g, uint16_t* __rest
     __syncthreads();
     PHASE(2);
     if (!s_runs && s_sumsq > max_sumsq) {
-        if (tid == 0) fallback[1 + atomicAdd(fallback, 1)] = blockIdx.x;
+        if (tid == 0) fallback[1 + atomicAdd(fallback, 1)] = bt;
         return;
     }
     each_pixel([&](int x, int y, uint32_t key, int wt, int cx, int cy) {
@@ -972,7 +975,7 @@ __global__ void __launch_bounds__(1024) k1_f32_bucket_g(Geom g, uint16_t* __rest
     PHASE(3);
     uint16_t* om = reinterpret_cast<uint16_t*>(hw);
     if (s_rl.abort) {  // run list overflow (block-uniform after the scatter barrier)
-        if (tid == 0) fallback[1 + atomicAdd(fallback, 1)] = blockIdx.x;
+        if (tid == 0) fallback[1 + atomicAdd(fallback, 1)] = bt;
         return;
     }
     if (s_runs)
@@ -982,13 +985,13 @@ __global__ void __launch_bounds__(1024) k1_f32_bucket_g(Geom g, uint16_t* __rest
     __syncthreads();
     PHASE(4);
     if (s_rl.abort) {  // a scan over budget (block-uniform after the barrier)
-        if (tid == 0) fallback[1 + atomicAdd(fallback, 1)] = blockIdx.x;
+        if (tid == 0) fallback[1 + atomicAdd(fallback, 1)] = bt;
         return;
     }
     fill_big_runs(om, &s_rl);
     for (int i = N + tid; i < g.Npad; i += blockDim.x) om[i] = 0xffffu;
     __syncthreads();
-    store_omega(g, om, omega_slot(g, omega_out));
+    store_omega(g, om, omega_slot(g, omega_out, bt));
     PHASE(5);
 
 }
