@@ -538,6 +538,34 @@ void list_costly_tiles(const Plan& p, Geom& g, long long t0, int nb) {
     }
 }
 
+// K2's costly tiles of a chunk: the top and bottom tile rows of each plane
+// whose input boxes reach past the image (clamped margins: windows there walk
+// long runs of ties) -- as ranges, run first so they do not form the tail.
+void list_costly_rows(const Plan& p, Geom& g, long long t0, int nb) {
+    g.nrr = 0;
+    const Geom& q = p.g;
+    const long long per_plane = (long long)q.tiles_x * q.tiles_y;
+    const int last_oy0 = q.oy_base + std::min((q.tiles_y - 1) * q.Th, std::max(q.out_h - q.oy_base - q.Th, 0));
+    const bool top = q.oy_base - q.r + q.vshift < 0, bottom = last_oy0 - q.r + q.vshift + q.Sh > q.H;
+    auto add = [&](long long a, long long b) {  // tiles [a, b) of the call, clipped to the chunk
+        a = std::max(a, t0);
+        b = std::min(b, t0 + nb);
+        if (b <= a || g.nrr >= 4) return;
+        if (g.nrr && g.rr_lo[g.nrr - 1] + g.rr_len[g.nrr - 1] == (int)(a - t0)) {  // merge adjacent
+            g.rr_len[g.nrr - 1] += (int)(b - a);
+            return;
+        }
+        g.rr_lo[g.nrr] = (int)(a - t0);
+        g.rr_len[g.nrr] = (int)(b - a);
+        g.nrr++;
+    };
+    for (long long pl = t0 / per_plane; pl * per_plane < t0 + nb; pl++) {
+        const long long base = pl * per_plane;
+        if (top && q.tiles_y > 1) add(base, base + q.tiles_x);
+        if (bottom) add(base + (long long)(q.tiles_y - 1) * q.tiles_x, base + per_plane);
+    }
+}
+
 void launch_k1(const Plan& p, const Geom& g, int nblocks, uint16_t* omega, unsigned char* k1g,
                int* flags, cudaStream_t s, const CUtensorMap* tm) {
     const dim3 grid(nblocks), block(p.k1_threads);
@@ -824,6 +852,7 @@ static int filter_impl(const imf_image* src, imf_image* dsts, int n, const int32
         if (env_int("IMF_COSTLY_FIRST", 1)) list_costly_tiles(p, g, t0, nb);
         launch_k1(p, g, nb, omega, k1g, k1flags, s, use_tma ? &k1_tmap : nullptr);
         g.nrt = 0;
+        if (env_int("IMF_COSTLY_FIRST", 1)) list_costly_rows(p, g, t0, nb);
         if (prof) cudaEventRecord(e1, s);
         for (int i = 0; i < n; i++) {
         g.dst = dsts[i].data;
@@ -863,6 +892,7 @@ static int filter_impl(const imf_image* src, imf_image* dsts, int n, const int32
             ev.push_back(e2);
         }
         g_launches += 1 + n;
+        g.nrr = 0;
     }
     if (lanes == 2) {
         cudaEventRecord(join_ev, ls[1]);

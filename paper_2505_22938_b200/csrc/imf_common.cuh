@@ -40,6 +40,8 @@ struct Geom {
     int tma_bw;                    // K1 TMA box width (elements per box row) when the launch uses TMA
     int nrt;                       // f32 bucket K1: chunk tiles with replicate runs (the costly ones),
     int rt[16];                    //   run first: chunk-relative indices, ascending (chunk_tile)
+    int nrr;                       // K2: chunk-relative tile ranges to run first (bottom image-border
+    int rr_lo[4], rr_len[4];       //   tile rows: clamped margins make their walks long), ascending
     int run_min;                   // bucket K1: copy groups (replicate boundary) this large rank as one run
     const uint32_t* ctab_g;        // f32 bucket K1: call-wide fine-bucket table (k_coarse_*), or nullptr
     int tiles_x, tiles_y;
@@ -83,6 +85,19 @@ __device__ __forceinline__ int chunk_tile(const Geom& g) {
     b -= g.nrt;
     for (int i = 0; i < g.nrt; i++)
         if (g.rt[i] <= b) b++;
+    return b;
+}
+
+// K2's chunk-relative tile of this CTA: the listed ranges first (in order),
+// then the remaining tiles in order.
+__device__ __forceinline__ int chunk_tile_ranges(const Geom& g) {
+    int b = blockIdx.x;
+    for (int i = 0; i < g.nrr; i++) {
+        if (b < g.rr_len[i]) return g.rr_lo[i] + b;
+        b -= g.rr_len[i];
+    }
+    for (int i = 0; i < g.nrr; i++)
+        if (g.rr_lo[i] <= b) b += g.rr_len[i];
     return b;
 }
 

@@ -570,9 +570,13 @@ __global__ void __launch_bounds__(512, 2) k2_pair(Geom g, PairParams p, const __
     const int N = g.N, Npad = g.Npad, Sw = g.Sw, r = g.r;
     const int T = g.Tw, TY = g.Th, G = p.G, TH = T >> 1;  // T: tile columns, TY: tile rows
     const int hs = p.hs;
-    const TileCoord tc = tile_coord(g, g.tile_begin + blockIdx.x);
+    // chunk-relative tile: the chunk's bottom image-border tile rows first (slow:
+    // their windows reach into the clamped margin, long all-tie walks), so
+    // they do not form the launch's tail
+    const int bt = chunk_tile_ranges(g);
+    const TileCoord tc = tile_coord(g, g.tile_begin + bt);
 
-    const uint16_t* om_g = omega_in + (long long)blockIdx.x * (Npad + 2 * OMEGA_SLOT_PAD) + OMEGA_SLOT_PAD;
+    const uint16_t* om_g = omega_in + (long long)bt * (Npad + 2 * OMEGA_SLOT_PAD) + OMEGA_SLOT_PAD;
     // omega: shared copy (8 sentinels before rank 0), or the global slot (OMG)
     uint16_t* om_sh = reinterpret_cast<uint16_t*>(smem) + 8;
     const uint16_t* om = OMG ? om_g : om_sh;
@@ -917,7 +921,7 @@ __global__ void __launch_bounds__(512, 2) k2_pair(Geom g, PairParams p, const __
             cA += dA;
             cB += dB;
             // test hook: an inconsistent count (core.py:31-36 defect path)
-            if (p.debug_defect && blockIdx.x == 0 && g.tile_begin == 0 && u == 0 && s == 0) cA += 1 << 20;
+            if (p.debug_defect && bt == 0 && g.tile_begin == 0 && u == 0 && s == 0) cA += 1 << 20;
             const int tA = target_at2(g, p, tc, row, j0);
             const int tB = target_at2(g, p, tc, row, j1);
             int mA, mB;

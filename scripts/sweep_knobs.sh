@@ -1,3 +1,4 @@
-for s in "IMF_RUNMIN=1024" "IMF_RUNMIN=256" "IMF_RUNMIN=64" "IMF_MAXSUMSQ_K=1048576" "IMF_RUNMIN=100000"; do
-  env $s python scripts/quick_bench.py c3 | grep "r48\|r64\|r100" | cut -c1-100 | sed "s/^/$s /"
+timeout 900 python -m pytest tests -x -q -m gpu 2>&1 | tail -1
+for s in "IMF_COSTLY_FIRST=0" "IMF_COSTLY_FIRST=1" "IMF_COSTLY_FIRST=0" "IMF_COSTLY_FIRST=1"; do
+  env $s python scripts/quick_bench.py c2 c4 c5 | cut -c1-110 | sed "s/^/$s /"
 done
