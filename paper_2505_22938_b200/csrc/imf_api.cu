@@ -336,6 +336,7 @@ int make_plan(const imf_image* src, const imf_kernel* k, const imf_options* opt,
             p.k1_smem = std::max(p.k1_smem, k1_count_smem_bytes(g.dtype, 0) + (size_t)g.tma_bw * g.Sh * esz);
         }
     }
+    g.k1_bulk = env_int("IMF_K1_BULK", 1);
     const size_t slot = 2 * (size_t)(g.Npad + 2 * OMEGA_SLOT_PAD);
     const size_t per_tile = slot + p.k1_gs_per_tile;
     // Two lanes (streams) alternate chunks when there are enough tiles: each

@@ -38,6 +38,7 @@ struct Geom {
     const uint32_t* fprow;         // footprint rows: input-tile row y ranks columns [lo, hi], lo | hi << 16
                                    // (lo > hi: none); device memory (workspace), nullptr = whole tile
     int tma_bw;                    // K1 TMA box width (elements per box row) when the launch uses TMA
+    int k1_bulk;                   // k1_count_reg copies omega out with one bulk async copy (IMF_K1_BULK)
     int nrt;                       // f32 bucket K1: chunk tiles with replicate runs (the costly ones),
     int rt[16];                    //   run first: chunk-relative indices, ascending (chunk_tile)
     int nrr;                       // K2: chunk-relative tile ranges to run first (bottom image-border

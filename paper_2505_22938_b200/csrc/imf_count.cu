@@ -170,7 +170,10 @@ __global__ void __launch_bounds__(1024) k1_count_reg(Geom g, uint16_t* __restric
         }
     for (int i = g.N + tid; i < g.Npad; i += blockDim.x) om[i] = 0xffffu;
     __syncthreads();
-    store_omega(g, om, omega_slot(g, omega_out));
+    if (g.k1_bulk)
+        store_omega_bulk(g, om, omega_slot(g, omega_out));
+    else
+        store_omega(g, om, omega_slot(g, omega_out));
 }
 
 #define IMF_K1R(DT, TMA)                                                                     \

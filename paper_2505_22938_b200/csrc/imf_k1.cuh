@@ -24,6 +24,25 @@ __device__ __forceinline__ void store_omega(const Geom& g, const uint16_t* om_s,
     }
 }
 
+// store_omega through the TMA engine: one thread issues a bulk shared->global
+// copy of the Npad entries (cp.async.bulk), the pads are stored by 16 threads,
+// and the issuing thread waits for the copy to finish reading shared memory
+// before the CTA exits (the other threads are free at once).
+__device__ __forceinline__ void store_omega_bulk(const Geom& g, const uint16_t* om_s, uint16_t* om_g) {
+    if (threadIdx.x == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the scatter's stores -> async proxy
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(om_g),
+                     "r"((uint32_t)__cvta_generic_to_shared(om_s)), "r"(2 * g.Npad)
+                     : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    }
+    if (threadIdx.x < OMEGA_SLOT_PAD) {
+        om_g[-OMEGA_SLOT_PAD + (int)threadIdx.x] = 0xffffu;
+        om_g[g.Npad + threadIdx.x] = 0xffffu;
+    }
+}
+
 // Exclusive scan, in place, of the 2*NW 16-bit counters packed two per word
 // in hw[0..NW).  Warp w owns words [w*NW/nw, (w+1)*NW/nw); lanes stride by one
 // word, so every shared access is bank-conflict free.  Ends with the counters
