@@ -35,6 +35,8 @@ VARIANTS = [
     {"IMF_GROUPED": "0"},
     {"IMF_DIRECT": "0"},
     {"IMF_TMA": "0"},
+    {"IMF_K1_BULK": "0"},
+    {"IMF_COSTLY_FIRST": "0"},
     {"IMF_REFINE": "0"},
     {"IMF_PAIR_RECT": "1", "IMF_TILE": "64"},
     {"IMF_TILE": "40", "IMF_SEED_ROWS": "4"},
