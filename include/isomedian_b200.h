@@ -158,7 +158,8 @@ int imf_profile_last(float* sort_ms, float* select_ms, int32_t* launches, int64_
  * Ordinal transform of ONE tile (device-side counterpart of the reference's
  * per-tile ordinal_transform, ordinal.py:126-172; for invariant checks as in
  * the reference's test_ordinal.py): runs the call's K1 on tile `tile` (index
- * as the filter enumerates them: x fastest, then y, channel, image) and copies
+ * as the filter enumerates them: channel fastest, then tile column, tile row,
+ * image) and copies
  * its omega -- the rank -> position map, x | y << 8 in input-tile coordinates
  * -- to host memory omega[0..N).  Only the tile's footprint is ranked (when
  * the planner uses one); ties are in arbitrary order (output-neutral for the

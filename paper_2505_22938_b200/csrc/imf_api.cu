@@ -513,6 +513,19 @@ bool make_k1_tmap(const Geom& g, const void* data, CUtensorMap* tm) {
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// Host mirror of tile_coord (imf_common.cuh): channel fastest, then tile
+// column, tile row, image; output origin of the tile (edge tiles shifted in).
+void host_tile(const Geom& q, long long t, int& tx, int& ty, int& c, int& b, int& ox0, int& oy0) {
+    c = (int)(t % q.C);
+    t /= q.C;
+    tx = (int)(t % q.tiles_x);
+    t /= q.tiles_x;
+    ty = (int)(t % q.tiles_y);
+    b = (int)(t / q.tiles_y);
+    oy0 = q.oy_base + std::min(ty * q.Th, std::max(q.out_h - q.oy_base - q.Th, 0));
+    ox0 = std::min(tx * q.Tw, std::max(q.out_w - q.Tw, 0));
+}
+
 // Host mirror of the f32 bucket K1's has_runs (imf_sort.cu) for tile t of a
 // call: tiles whose replicate-copy groups reach run_min (image corners) are
 // the slow ones; the chunk lists them so their CTAs start first.
@@ -528,12 +541,8 @@ void list_costly_tiles(const Plan& p, Geom& g, long long t0, int nb) {
     if (!p.k1_f32b || g.fp) return;
     const Geom& q = p.g;
     for (int b = 0; b < nb && g.nrt < 16; b++) {
-        long long t = t0 + b;
-        const int tx = (int)(t % q.tiles_x);
-        t /= q.tiles_x;
-        const int ty = (int)(t % q.tiles_y);
-        const int oy0 = q.oy_base + std::min(ty * q.Th, std::max(q.out_h - q.oy_base - q.Th, 0));
-        const int ox0 = std::min(tx * q.Tw, std::max(q.out_w - q.Tw, 0));
+        int tx, ty, c, im, ox0, oy0;
+        host_tile(q, t0 + b, tx, ty, c, im, ox0, oy0);
         const int X0 = ox0 - q.r + q.vshift, Y0 = oy0 - q.r + q.vshift;
         if (host_max_copies(X0, q.Sw, q.W) * host_max_copies(Y0, q.Sh, q.H) >= q.run_min) g.rt[g.nrt++] = b;
     }
@@ -545,7 +554,6 @@ void list_costly_tiles(const Plan& p, Geom& g, long long t0, int nb) {
 void list_costly_rows(const Plan& p, Geom& g, long long t0, int nb) {
     g.nrr = 0;
     const Geom& q = p.g;
-    const long long per_plane = (long long)q.tiles_x * q.tiles_y;
     const int last_oy0 = q.oy_base + std::min((q.tiles_y - 1) * q.Th, std::max(q.out_h - q.oy_base - q.Th, 0));
     const bool top = q.oy_base - q.r + q.vshift < 0, bottom = last_oy0 - q.r + q.vshift + q.Sh > q.H;
     auto add = [&](long long a, long long b) {  // tiles [a, b) of the call, clipped to the chunk
@@ -560,10 +568,12 @@ void list_costly_rows(const Plan& p, Geom& g, long long t0, int nb) {
         g.rr_len[g.nrr] = (int)(b - a);
         g.nrr++;
     };
-    for (long long pl = t0 / per_plane; pl * per_plane < t0 + nb; pl++) {
-        const long long base = pl * per_plane;
-        if (top && q.tiles_y > 1) add(base, base + q.tiles_x);
-        if (bottom) add(base + (long long)(q.tiles_y - 1) * q.tiles_x, base + per_plane);
+    // tiles of tile row ty of image b: [((b * tiles_y + ty) * tiles_x) * C, + tiles_x * C)
+    const long long row_tiles = (long long)q.tiles_x * q.C, per_image = row_tiles * q.tiles_y;
+    for (long long im = t0 / per_image; im * per_image < t0 + nb; im++) {
+        const long long base = im * per_image;
+        if (top && q.tiles_y > 1) add(base, base + row_tiles);
+        if (bottom) add(base + (long long)(q.tiles_y - 1) * row_tiles, base + per_image);
     }
 }
 
@@ -987,14 +997,8 @@ int imf_tile_omega(const imf_image* src, const imf_kernel* kernel, const imf_opt
     // the tile's input origin (image coordinates of input-tile pixel (0, 0),
     // before clamping; tile_coord on the host) and its input extent
     const Geom& q = p.g;
-    long long t = tile;
-    const int tx = (int)(t % q.tiles_x);
-    t /= q.tiles_x;
-    const int ty = (int)(t % q.tiles_y);
-    t /= q.tiles_y;
-    const int c = (int)(t % q.C), b = (int)(t / q.C);
-    const int oy0 = q.oy_base + std::min(ty * q.Th, std::max(q.out_h - q.oy_base - q.Th, 0));
-    const int ox0 = std::min(tx * q.Tw, std::max(q.out_w - q.Tw, 0));
+    int tx, ty, c, b, ox0, oy0;
+    host_tile(q, tile, tx, ty, c, b, ox0, oy0);
     info[0] = q.N;
     info[1] = ox0 - q.r + q.vshift;
     info[2] = oy0 - q.r + q.vshift;

@@ -106,16 +106,20 @@ __device__ __forceinline__ TileCoord tile_coord(const Geom& g, long long t64) {
     TileCoord tc;
     // tile indices fit 32 bits (<= 2^31 tiles per call); 32-bit unsigned
     // division is a few instructions, the 64-bit one a ~100-instruction call
+    // Enumeration: channel fastest, then tile column, tile row, image -- the
+    // channels of one (interleaved) tile are neighbours (they read the same
+    // bytes), and consecutive tile indices walk DOWN the image, which lets the
+    // host pipeline gate chunks on the input rows uploaded so far.
     unsigned t = (unsigned)t64;
     const unsigned tx = (unsigned)g.tiles_x, ty = (unsigned)g.tiles_y, C = (unsigned)g.C;
-    unsigned q = (unsigned)(((unsigned long long)t * g.mx) >> g.sx);  // t / tx (exact for t < 2^31)
+    unsigned q = (unsigned)(((unsigned long long)t * g.mc) >> g.sc);  // t / C (exact for t < 2^31)
+    tc.c = (int)(t - q * C);
+    t = q;
+    q = (unsigned)(((unsigned long long)t * g.mx) >> g.sx);
     tc.tx = (int)(t - q * tx);
     t = q;
     q = (unsigned)(((unsigned long long)t * g.my) >> g.sy);
     tc.ty = (int)(t - q * ty);
-    t = q;
-    q = (unsigned)(((unsigned long long)t * g.mc) >> g.sc);
-    tc.c = (int)(t - q * C);
     tc.b = (int)q;
     // The last tile of a row / column is shifted back to end at the image edge
     // (overlapping its neighbour; both write identical values) instead of

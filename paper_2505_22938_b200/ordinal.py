@@ -58,8 +58,8 @@ class DeviceOrdinalTile:
 
 
 def tile_ordinal(image, params, tile: int, *, batched: bool = False) -> DeviceOrdinalTile:
-    """Run the filter call's K1 on tile `tile` (x fastest, then y, channel,
-    image) of a CUDA tensor and return its ordinal transform."""
+    """Run the filter call's K1 on tile `tile` (channel fastest, then tile
+    column, tile row, image) of a CUDA tensor and return its ordinal transform."""
     import torch
 
     from .tiling import _DTYPES, _WS, _image_struct, _kernel_struct, _np_dtype_of
