@@ -7,6 +7,8 @@
 #include <mutex>
 #include <cstdlib>
 #include <cstring>
+#include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/isomedian_b200.h"
@@ -1080,12 +1082,22 @@ int imf_filter_host(const imf_image* src, imf_image* dst, const imf_kernel* kern
     }
     void *dsrc = nullptr, *ddst = nullptr, *dws = nullptr, *dws2 = nullptr, *dtm = nullptr;
     std::vector<cudaEvent_t> evs;
+    // IMF_HOST_TRACE=1: timed events, and a per-stripe timeline on stderr (dev aid)
+    const bool trace = env_int("IMF_HOST_TRACE", 0) != 0;
+    std::vector<std::pair<std::string, cudaEvent_t>> tl;
     auto event = [&]() {
         cudaEvent_t e = nullptr;
-        cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&e, trace ? cudaEventDefault : cudaEventDisableTiming);
         evs.push_back(e);
         return e;
     };
+    auto mark = [&](const char* what, int i, cudaStream_t st) {
+        if (!trace) return;
+        cudaEvent_t e = event();
+        cudaEventRecord(e, st);
+        tl.emplace_back(std::string(what) + " " + std::to_string(i), e);
+    };
+    mark("start", 0, s);
     int rc = IMF_OK;
     // two compute lanes (stripes alternate between them, each with its own
     // workspace) so one stripe's K1 fills the tail of the previous stripe's K2
@@ -1174,6 +1186,7 @@ int imf_filter_host(const imf_image* src, imf_image* dst, const imf_kernel* kern
                 const int lane_i = (two && pipe) ? (nstripe & 1) : 0;
                 cudaStream_t cs = lane_i ? g_hs.comp2 : s;
                 void* wsl = lane_i ? dws2 : dws;
+                mark("uploaded", nstripe, g_hs.up);
                 cudaEvent_t e_up = event();
                 cudaEventRecord(e_up, g_hs.up);
                 cudaStreamWaitEvent(cs, e_up, 0);
@@ -1194,6 +1207,7 @@ int imf_filter_host(const imf_image* src, imf_image* dst, const imf_kernel* kern
                 if (!rc)
                     rc = imf_filter(&dsi, &ddi, kernel, target, (const int32_t*)dtm, tmin, tmax, &o, wsl,
                                     p.ws_total, cs);
+                mark("filtered", nstripe - 1, cs);
                 cudaEvent_t e_done = event();
                 cudaEventRecord(e_done, cs);
                 cudaStreamWaitEvent(g_hs.down, e_done, 0);
@@ -1210,6 +1224,7 @@ int imf_filter_host(const imf_image* src, imf_image* dst, const imf_kernel* kern
                         rc = cuda_fail(cudaGetLastError(), "download");
                     }
                 }
+                mark("downloaded", nstripe - 1, g_hs.down);
                 if (!pipe) break;
             }
             if (ring) {
@@ -1235,6 +1250,13 @@ int imf_filter_host(const imf_image* src, imf_image* dst, const imf_kernel* kern
     if (dws2) cudaFreeAsync(dws2, s);
     if (dtm) cudaFreeAsync(dtm, s);
     cudaStreamSynchronize(s);
+    if (trace && !tl.empty()) {
+        for (auto& kv : tl) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, tl[0].second, kv.second);
+            fprintf(stderr, "imf_host_trace %-14s %8.3f ms\n", kv.first.c_str(), ms);
+        }
+    }
     for (cudaEvent_t e : evs) cudaEventDestroy(e);
     return rc;
 }
