@@ -171,6 +171,18 @@ int imf_tile_omega(const imf_image* src, const imf_kernel* kernel, const imf_opt
                    uint16_t* omega, int32_t capacity, int32_t* info, void* workspace, size_t workspace_bytes,
                    void* stream);
 
+/*
+ * The launch plan the library would use for this call (host only, no CUDA
+ * work; diagnostics and tests): info[16] = output tile Tw, Th; input tile Sw,
+ * Sh; ranked pixels per tile N (the footprint when one is used) and Npad;
+ * tiles in the call; tiles per chunk; chunk streams; selection kernel (0
+ * direct, 1 general, 2 pair); footprint used; K1 tile loads by TMA (when the
+ * data pointer is 16-byte aligned); halved ranks; seed rows; workspace bytes;
+ * ordinal-transform family (0 radix, 1 f32 buckets, 2 f32 buckets with global
+ * entries, 3 counting sort).
+ */
+int imf_plan_info(const imf_image* src, const imf_kernel* kernel, const imf_options* opt, int64_t* info);
+
 /* Kernel paths the last imf_filter / imf_filter_bracket on this thread took
  * (diagnostic): IMF_FEATURE_K1_TMA = the ordinal transform loaded its tile
  * boxes with TMA (cp.async.bulk.tensor). */

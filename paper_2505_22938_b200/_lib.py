@@ -25,7 +25,7 @@ IMF_ERR_UNSUPPORTED = 5
 EXPORTED = ("imf_workspace_size", "imf_filter", "imf_filter_bracket", "imf_workspace_status",
             "imf_filter_host",
             "imf_strerror", "imf_version", "imf_last_error", "imf_launch_count",
-            "imf_profile_last", "imf_int_peak", "imf_last_features", "imf_tile_omega")
+            "imf_profile_last", "imf_int_peak", "imf_last_features", "imf_tile_omega", "imf_plan_info")
 
 _i32p = ctypes.POINTER(ctypes.c_int32)
 
@@ -100,6 +100,8 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
                                    ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t,
                                    ctypes.c_void_p]
     lib.imf_tile_omega.restype = ctypes.c_int
+    lib.imf_plan_info.argtypes = [P(ImfImage), P(ImfKernel), P(ImfOptions), ctypes.c_void_p]
+    lib.imf_plan_info.restype = ctypes.c_int
     return lib
 
 

@@ -970,6 +970,18 @@ int imf_profile_last(float* sort_ms, float* select_ms, int32_t* launches, int64_
 
 uint32_t imf_last_features(void) { return g_last_tma ? IMF_FEATURE_K1_TMA : 0u; }
 
+int imf_plan_info(const imf_image* src, const imf_kernel* kernel, const imf_options* opt, int64_t* info) {
+    if (!info) return IMF_ERR_INVALID;
+    Plan p;
+    if (int st = make_plan(src, kernel, opt, &p)) return st;
+    const Geom& g = p.g;
+    const int64_t v[16] = {g.Tw, g.Th, g.Sw, g.Sh, g.N, g.Npad, p.total_tiles, p.chunk_tiles, p.lanes,
+                           p.direct ? 0 : (p.pair ? 2 : 1), g.fp, p.k1_tma ? 1 : 0, p.hs, p.G,
+                           (int64_t)p.ws_total, p.k1_f32b ? (p.k1_f32b_g ? 2 : 1) : (p.k1_count ? 3 : 0)};
+    memcpy(info, v, sizeof(v));
+    return IMF_OK;
+}
+
 int imf_tile_omega(const imf_image* src, const imf_kernel* kernel, const imf_options* opt, int64_t tile,
                    uint16_t* omega, int32_t capacity, int32_t* info, void* workspace, size_t workspace_bytes,
                    void* stream) {

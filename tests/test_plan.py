@@ -1,0 +1,78 @@
+"""The launch planner, on the host (no GPU): imf_plan_info reports the plan the
+library would use.  The tile footprint -- the input pixels some window of the
+tile contains, i.e. the Minkowski sum of the output rectangle and the kernel
+(the reference's _footprint_mask, tiling.py:148-162) -- must equal a brute-force
+construction from the kernel's own span table, for every convex shape."""
+import ctypes
+
+import numpy as np
+import pytest
+
+from paper_2505_22938_b200 import ShapeSpec, _lib, make_kernel
+from paper_2505_22938_b200.tiling import _kernel_struct
+
+KEYS = ["Tw", "Th", "Sw", "Sh", "N", "Npad", "tiles", "chunk", "lanes", "k2", "fp", "tma", "hs", "G",
+        "ws", "k1"]
+
+
+def plan(shape_hw_c, spec, dtype=1, boundary=0, aligned=True):
+    L = _lib.load()
+    h, w, c = shape_hw_c
+    k = make_kernel(spec)
+    ks, keep = _kernel_struct(k)
+    img = _lib.ImfImage(0x1000 if aligned else 0x1002, dtype, 1, h, w, c, 0, w * c, c, 1)
+    opt = _lib.ImfOptions(boundary, 0, 0, 0)
+    info = (ctypes.c_int64 * 16)()
+    assert L.imf_plan_info(ctypes.byref(img), ctypes.byref(ks), ctypes.byref(opt), info) == 0
+    return dict(zip(KEYS, list(info))), k
+
+
+def brute_footprint(k, Tw, Th, Sw, Sh, r):
+    mask = np.zeros((Sh, Sw), bool)
+    for dy, xlo, xhi in zip(k.row_dy, k.row_xlo, k.row_xhi):
+        if xhi <= xlo:
+            continue
+        for cy in range(r, r + Th):
+            y = cy + dy
+            if 0 <= y < Sh:
+                mask[y, max(0, r + xlo):min(Sw, r + Tw - 1 + xhi)] = True
+    return int(mask.sum())
+
+
+@pytest.mark.parametrize("spec", [ShapeSpec("circle", 48), ShapeSpec("circle", 8), ShapeSpec("circle", 64),
+                                  ShapeSpec("regular_polygon", 32, sides=6),
+                                  ShapeSpec("regular_polygon", 32, sides=12),
+                                  ShapeSpec("regular_polygon", 20, sides=5, rotation_deg=17.0),
+                                  ShapeSpec("regular_polygon", 40, sides=3, rotation_deg=90.0)])
+def test_footprint_is_the_minkowski_sum(spec):
+    p, k = plan((2160, 3840, 3), spec)
+    assert p["k2"] == 2 and p["fp"] == 1
+    assert p["N"] == brute_footprint(k, p["Tw"], p["Th"], p["Sw"], p["Sh"], spec.radius)
+    assert p["N"] < p["Sw"] * p["Sh"]
+
+
+def test_c2_plan():
+    p, k = plan((2160, 3840, 3), ShapeSpec("circle", 48))
+    assert (p["Tw"], p["Th"], p["Sw"], p["Sh"]) == (64, 64, 160, 160)
+    assert p["N"] == 23584 and p["tiles"] == 60 * 34 * 3 and p["lanes"] == 2
+    assert p["tma"] == 0  # interleaved HWC: per-lane loads
+    assert p["k1"] == 3   # counting sort
+
+
+def test_planar_u16_uses_tma_when_aligned():
+    p, _ = plan((4320, 7680, 1), ShapeSpec("circle", 64))
+    assert p["tma"] == 1 and p["hs"] == 1  # c5: TMA tile boxes, halved ranks (N > 32768)
+    p, _ = plan((4321, 7681, 1), ShapeSpec("circle", 64))
+    assert p["tma"] == 0                   # rows of 15,362 bytes are not 16-byte multiples
+
+
+def test_square_and_f32_plans_have_no_footprint():
+    p, _ = plan((2160, 3840, 3), ShapeSpec("square", 32), dtype=0)
+    assert p["fp"] == 0 and p["N"] == p["Sw"] * p["Sh"]
+    p, _ = plan((2048, 2048, 1), ShapeSpec("circle", 64), dtype=2)
+    assert p["fp"] == 0 and p["k1"] in (1, 2) and p["N"] == 192 * 192
+
+
+def test_direct_selection_for_tiny_windows():
+    p, _ = plan((512, 512, 1), ShapeSpec("circle", 2), dtype=2)
+    assert p["k2"] == 0
