@@ -235,34 +235,43 @@ int make_plan(const imf_image* src, const imf_kernel* k, const imf_options* opt,
     set_magic((unsigned)g.C, g.mc, g.sc);
     if (p.total_tiles >= (1ll << 31)) return IMF_ERR_UNSUPPORTED;  // tile_coord uses 32-bit indices
 
-    p.k1_count = g.dtype != DT_F32 && k1_count_smem_bytes(g.dtype, g.Npad) <= kSmemMax;
     g.run_min = std::max(kRunMinFloor, env_int("IMF_RUNMIN", kRunMin));
-    p.k1b_smem = k1_f32_bucket_smem_bytes(g.N);
-    p.k1_f32b = g.dtype == DT_F32 && env_int("IMF_F32_BUCKET", 1) && g.Sw <= 160 && p.k1b_smem <= kSmemMax;
-    // f32 tiles beyond shared-memory entries, and u16 tiles beyond the 64K-bin
-    // counting sort (S > ~180): the bucket transform with global entries
-    // (u16 keys v << 16: every bucket is one value, ties only)
-    // u16 tiles beyond it: the counting sort with omega in global memory
-    p.k1_count_g = g.dtype == DT_U16 && !p.k1_count && env_int("IMF_K1_COUNT_G", 1);
-    if ((g.dtype == DT_F32 || (g.dtype == DT_U16 && !p.k1_count && !p.k1_count_g)) && !p.k1_f32b &&
-        env_int("IMF_F32_BUCKET", 1)) {
-        p.k1_f32b = p.k1_f32b_g = true;
-        p.k1b_smem = k1_f32_bucket_g_smem_bytes(g.N);
-    }
-    p.k1_threads = p.k1_count ? kK1Threads : kK1SortThreads;
-    p.k1_gmem = !p.k1_count && k1_smem_bytes(g.dtype, g.Npad, p.k1_threads / 32, false) > kSmemMax;
-    p.k1_smem = p.k1_count ? k1_count_smem_bytes(g.dtype, g.Npad)
-                           : k1_smem_bytes(g.dtype, g.Npad, p.k1_threads / 32, p.k1_gmem);
-    p.k1_gs_per_tile = (p.k1_gmem && !p.k1_count_g) ? k1_gscratch_bytes(g.dtype, g.Npad) : 0;
-    // the global-entries bucket kernels need 6 B per pixel (entries + run
-    // descriptors); the LSD fallback reuses the same slot (k1_gscratch_bytes(f32)
-    // = 6 B per pixel when it needs one)
-    if (p.k1_f32b_g) p.k1_gs_per_tile = std::max(p.k1_gs_per_tile, (size_t)6 * g.Npad);  // + run descriptors
-    // k1_f32_bucket<NK <= 6, global entries>: interior tiles keep 16-bit entries
-    // in shared memory after the coarse table (imf_sort.cu OWN16)
-    if (p.k1_f32b_g && ((g.Sw + 31) >> 5) <= 6) p.k1b_smem += 2 * (size_t)g.Npad + 16;
+    // K1 variant and its memory for the ranked pixels per tile g.N (chosen
+    // again once a footprint shrinks N)
+    auto choose_k1 = [&]() {
+        // k1_sort holds 1 KB of static shared memory for footprint tiles
+        p.k1_f32b_g = false;
+        const size_t k1s_max = kSmemMax - (g.fp ? 1024 : 0);
+        p.k1_count = g.dtype != DT_F32 && k1_count_smem_bytes(g.dtype, g.Npad) <= kSmemMax;
+        p.k1b_smem = k1_f32_bucket_smem_bytes(g.N);
+        p.k1_f32b = g.dtype == DT_F32 && env_int("IMF_F32_BUCKET", 1) && g.Sw <= 160 && p.k1b_smem <= kSmemMax;
+        // f32 tiles beyond shared-memory entries, and u16 tiles beyond the 64K-bin
+        // counting sort (S > ~180): the bucket transform with global entries
+        // (u16 keys v << 16: every bucket is one value, ties only)
+        // u16 tiles beyond it: the counting sort with omega in global memory
+        p.k1_count_g = g.dtype == DT_U16 && !p.k1_count && env_int("IMF_K1_COUNT_G", 1);
+        if ((g.dtype == DT_F32 || (g.dtype == DT_U16 && !p.k1_count && !p.k1_count_g)) && !p.k1_f32b &&
+            env_int("IMF_F32_BUCKET", 1)) {
+            p.k1_f32b = p.k1_f32b_g = true;
+            p.k1b_smem = k1_f32_bucket_g_smem_bytes(g.N);
+        }
+        p.k1_threads = p.k1_count ? kK1Threads : kK1SortThreads;
+        p.k1_gmem = !p.k1_count && k1_smem_bytes(g.dtype, g.Npad, p.k1_threads / 32, false) > k1s_max;
+        p.k1_smem = p.k1_count ? k1_count_smem_bytes(g.dtype, g.Npad)
+                               : k1_smem_bytes(g.dtype, g.Npad, p.k1_threads / 32, p.k1_gmem);
+        p.k1_gs_per_tile = (p.k1_gmem && !p.k1_count_g) ? k1_gscratch_bytes(g.dtype, g.Npad) : 0;
+        // the global-entries bucket kernels need 6 B per pixel (entries + run
+        // descriptors); the LSD fallback reuses the same slot (k1_gscratch_bytes(f32)
+        // = 6 B per pixel when it needs one)
+        if (p.k1_f32b_g) p.k1_gs_per_tile = std::max(p.k1_gs_per_tile, (size_t)6 * g.Npad);  // + run descriptors
+        // k1_f32_bucket<NK <= 6, global entries>: interior tiles keep 16-bit entries
+        // in shared memory after the coarse table (imf_sort.cu OWN16)
+        if (p.k1_f32b_g && ((g.Sw + 31) >> 5) <= 6) p.k1b_smem += 2 * (size_t)g.Npad + 16;
+    };
+    choose_k1();
 
-    // Tile footprint (pair path, register-resident K1): rank only the input
+    // Tile footprint (pair path; register-resident u8/u16 K1 or the f32 bucket
+    // transform and its LSD fallback): rank only the input
     // pixels some window of the tile contains -- the Minkowski sum of the
     // output rectangle and the kernel (tiling.py:148-162 _footprint_mask,
     // PAPER.md:283,294): per input-tile row y, kernel rows dy whose window
@@ -271,7 +280,14 @@ int make_plan(const imf_image* src, const imf_kernel* k, const imf_options* opt,
     // rounded rectangle (c2: 25,600 -> 23,616 pixels); squares the whole tile.
     const bool k1reg = p.k1_count && ((g.Sw + 31) >> 5) <= 6 && env_int("IMF_K1REG", 1) &&
                        (long long)(g.H - 1) * g.s_y + (long long)(g.W - 1) * g.s_x < (1ll << 31);
-    if (p.pair && k->shape_code != IMF_SHAPE_SQUARE && k1reg && g.Sh <= 256 && env_int("IMF_FOOTPRINT", 1)) {
+    // f32: the footprint pays on the global-entries kernel (S > 192: every
+    // ranked pixel costs scattered L2 traffic); on the shared-entries kernels
+    // its per-pixel tests cost what the ~10 % fewer pixels save (c3 r=64:
+    // K1 +0.5 %, path +3 %).  IMF_F32_FOOTPRINT: 0 never, 1 auto, 2 always.
+    const int f32fp = env_int("IMF_F32_FOOTPRINT", 1);
+    const bool fp_k1 = k1reg || (g.dtype == DT_F32 && p.k1_f32b &&
+                                 (f32fp == 2 || (f32fp == 1 && p.k1_f32b_g && ((g.Sw + 31) >> 5) > 6)));
+    if (p.pair && k->shape_code != IMF_SHAPE_SQUARE && fp_k1 && g.Sh <= 256 && env_int("IMF_FOOTPRINT", 1)) {
         // the table depends on the kernel's row spans and the tile geometry only:
         // memoized per thread (the host pipeline plans every stripe of a frame)
         uint64_t h = 1469598103934665603ull;
@@ -312,7 +328,6 @@ int make_plan(const imf_image* src, const imf_kernel* k, const imf_options* opt,
         }
         const int NI = g.Sw * g.Sh;
         g.fp = 1;
-        g.fpR2 = 0;
         g.N = nfp;
         g.Npad = (nfp + 63) & ~63;
         p.hs = nfp > 32768 ? 1 : 0;
@@ -321,7 +336,7 @@ int make_plan(const imf_image* src, const imf_kernel* k, const imf_options* opt,
                                       : k2_pair_smem_bytes(g.N, g.Npad, NI, r, p.G, g.Tw, g.Th, false) > 113 * 1024;
         p.omg = pomg;
         p.k2_smem = k2_pair_smem_bytes(g.N, g.Npad, NI, r, p.G, g.Tw, g.Th, pomg);
-        p.k1_smem = k1_count_smem_bytes(g.dtype, g.Npad);
+        choose_k1();
     }
 
     // K1 tile loads through TMA when the plane is pixel-contiguous (s_x == 1):
@@ -444,8 +459,10 @@ cudaError_t set_attrs() {
     IMF_K1R_ATTR(DT_U16, true)
 #undef IMF_K1R_ATTR
 #define IMF_K1F_ATTR(NK)                                               \
-    if (!e) e = allow_smem(k1_f32_bucket<NK, false>, optin);           \
-    if (!e) e = allow_smem(k1_f32_bucket<NK, true>, optin);
+    if (!e) e = allow_smem(k1_f32_bucket<NK, false, false>, optin);    \
+    if (!e) e = allow_smem(k1_f32_bucket<NK, true, false>, optin);     \
+    if (!e) e = allow_smem(k1_f32_bucket<NK, false, true>, optin);     \
+    if (!e) e = allow_smem(k1_f32_bucket<NK, true, true>, optin);
     IMF_K1F_ATTR(1)
     IMF_K1F_ATTR(2)
     IMF_K1F_ATTR(3)
@@ -540,7 +557,7 @@ int host_max_copies(int X0, int S, int W) {
 
 void list_costly_tiles(const Plan& p, Geom& g, long long t0, int nb) {
     g.nrt = 0;
-    if (!p.k1_f32b || g.fp) return;
+    if (!p.k1_f32b) return;
     const Geom& q = p.g;
     for (int b = 0; b < nb && g.nrt < 16; b++) {
         int tx, ty, c, im, ox0, oy0;
@@ -591,11 +608,17 @@ void launch_k1(const Plan& p, const Geom& g, int nblocks, uint16_t* omega, unsig
         if (p.k1_f32b_g && nk > 6) {
             k1_f32_bucket_g<<<grid, b1024, p.k1b_smem, s>>>(g, omega, flags, (uint32_t*)k1g, gs / 4, mss);
         } else {
-#define IMF_K1F_LAUNCH(NK)                                                                                  \
-    if (p.k1_f32b_g)                                                                                         \
-        k1_f32_bucket<NK, true><<<grid, b1024, p.k1b_smem, s>>>(g, omega, flags, (uint32_t*)k1g, gs / 4, mss); \
-    else                                                                                                     \
-        k1_f32_bucket<NK, false><<<grid, b1024, p.k1b_smem, s>>>(g, omega, flags, nullptr, 0, mss);
+#define IMF_K1F_LAUNCH2(NK, FP)                                                                              \
+    if (p.k1_f32b_g)                                                                                            \
+        k1_f32_bucket<NK, true, FP><<<grid, b1024, p.k1b_smem, s>>>(g, omega, flags, (uint32_t*)k1g, gs / 4, mss); \
+    else                                                                                                        \
+        k1_f32_bucket<NK, false, FP><<<grid, b1024, p.k1b_smem, s>>>(g, omega, flags, nullptr, 0, mss);
+#define IMF_K1F_LAUNCH(NK)        \
+    if (g.fp) {                   \
+        IMF_K1F_LAUNCH2(NK, true) \
+    } else {                      \
+        IMF_K1F_LAUNCH2(NK, false) \
+    }
             switch (nk) {
                 case 1: IMF_K1F_LAUNCH(1) break;
                 case 2: IMF_K1F_LAUNCH(2) break;
@@ -605,6 +628,7 @@ void launch_k1(const Plan& p, const Geom& g, int nblocks, uint16_t* omega, unsig
                 default: IMF_K1F_LAUNCH(6) break;
             }
 #undef IMF_K1F_LAUNCH
+#undef IMF_K1F_LAUNCH2
         }
         // tiles whose buckets are too large (sum of squared sizes above the
         // limit): LSD radix sort over the list

@@ -34,7 +34,7 @@ struct Geom {
     int vshift;                    // r in valid mode, 0 in replicate mode
     int r;
     int Tw, Th, Sw, Sh, N, Npad;   // N: ranked pixels per tile; Npad: N rounded up to a multiple of 64
-    int fp, fpR2;                  // fp: only footprint pixels are ranked (fprow; fpR2: circle radius^2 test)
+    int fp;                        // only footprint pixels are ranked (fprow)
     const uint32_t* fprow;         // footprint rows: input-tile row y ranks columns [lo, hi], lo | hi << 16
                                    // (lo > hi: none); device memory (workspace), nullptr = whole tile
     int tma_bw;                    // K1 TMA box width (elements per box row) when the launch uses TMA
@@ -141,16 +141,28 @@ __device__ __forceinline__ long long src_offset(const Geom& g, const TileCoord& 
     return (long long)y * g.s_y + (long long)x * g.s_x;
 }
 
-// Rounded-rect tile footprint (tiling.py:148-162 is the CPU
-// analog): input-tile pixel (x, y) is in some circle window of the tile iff its
-// squared distance to the output rectangle [r, r+Tw) x [r, r+Th) is <= r(r+1)
-// (kernels.py:70-71).  Pixels outside are never ranked: omega is shorter and
-// denser (output-neutral: they belong to no window).
-__device__ __forceinline__ bool in_footprint(const Geom& g, int x, int y) {
-    if (!g.fp) return true;
-    const int ex = max(0, max(g.r - x, x - (g.r + g.Tw - 1)));
-    const int ey = max(0, max(g.r - y, y - (g.r + g.Th - 1)));
-    return ex * ex + ey * ey <= g.fpR2;
+// Tile footprint (tiling.py:148-162 _footprint_mask is the
+// CPU analog): the input-tile pixels some window of the tile contains, i.e. the
+// Minkowski sum of the output rectangle and the kernel.  Convex kernels give
+// one column interval per input-tile row, the host's g.fprow table.  Pixels
+// outside are never ranked: omega is shorter and denser (output-neutral: they
+// belong to no window).
+__device__ __forceinline__ bool in_footprint(const uint32_t* fprow, int x, int y) {
+    if (!fprow) return true;
+    const uint32_t v = __ldg(fprow + y);  // empty row: lo = hi = 0xffff (no x < 256 matches)
+    const int lo = (int)(v & 0xffffu);
+    return (unsigned)(x - lo) <= (unsigned)((int)(v >> 16) - lo);
+}
+
+// Footprint pixels of the rectangle [x0, x0 + cx) x [y0, y0 + cy).
+__device__ __forceinline__ int fp_rect_count(const uint32_t* fprow, int x0, int cx, int y0, int cy) {
+    if (!fprow) return cx * cy;
+    int n = 0;
+    for (int y = y0; y < y0 + cy; y++) {
+        const uint32_t v = __ldg(fprow + y);
+        n += max(0, min((int)(v >> 16), x0 + cx - 1) - max((int)(v & 0xffffu), x0) + 1);
+    }
+    return n;
 }
 
 __device__ __forceinline__ uint32_t float_key(uint32_t u) {

@@ -26,7 +26,7 @@ template <int DT, int NK, bool TMA>
 __global__ void __launch_bounds__(1024) k1_count_reg(Geom g, uint16_t* __restrict__ omega_out,
                                                      const __grid_constant__ CUtensorMap tmap);
 __global__ void __launch_bounds__(1024) k1_count_g(Geom g, uint16_t* __restrict__ omega_out);
-template <int NK, bool GENT>
+template <int NK, bool GENT, bool FP>
 __global__ void __launch_bounds__(1024) k1_f32_bucket(Geom g, uint16_t* __restrict__ omega_out,
                                                      int* __restrict__ fallback, uint32_t* __restrict__ gent,
                                                      long long gent_stride, unsigned long long max_sumsq);

@@ -129,12 +129,6 @@ __device__ void stable_pass(int N, uint32_t* cnt, DigitFn digit, EmitFn emit) {
     __syncthreads();
 }
 
-__device__ __forceinline__ uint16_t pack_pos(int i, int Sw, float invS) {
-    int x, y;
-    lin_to_xy(i, Sw, invS, x, y);
-    return (uint16_t)(x | (y << 8));
-}
-
 template <int DT, bool GMEM>
 __device__ void k1_sort_tile(const Geom& g, uint16_t* __restrict__ omega_out, unsigned char* __restrict__ gscratch,
                              long long gscratch_stride, const int bt) {
@@ -144,6 +138,35 @@ __device__ void k1_sort_tile(const Geom& g, uint16_t* __restrict__ omega_out, un
     const int N = g.N, Sw = g.Sw;
     const float invS = 1.0f / (float)Sw;
     const int nw = blockDim.x >> 5;
+    // footprint tiles (g.fprow): index i < N is the i-th footprint pixel in
+    // row-major order; s_fpre[y] = footprint pixels in rows < y
+    __shared__ uint32_t s_fpre[256];
+    if (g.fprow) {
+        for (int y = threadIdx.x; y < 256; y += blockDim.x) {
+            const uint32_t v = y < g.Sh ? __ldg(g.fprow + y) : 0xffffffffu;
+            s_fpre[y] = (uint32_t)max(0, (int)(v >> 16) - (int)(v & 0xffffu) + 1);
+        }
+        __syncthreads();
+        block_exclusive_scan(s_fpre, 256);
+    }
+    auto xy_of = [&](int i, int& x, int& y) {
+        if (!g.fprow) {
+            lin_to_xy(i, Sw, invS, x, y);
+            return;
+        }
+        int lo = 0, hi = g.Sh - 1;  // the last row whose prefix is <= i
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if ((int)s_fpre[mid] <= i) lo = mid; else hi = mid - 1;
+        }
+        y = lo;
+        x = (int)(__ldg(g.fprow + lo) & 0xffffu) + i - (int)s_fpre[lo];
+    };
+    auto pos_of = [&](int i) {
+        int x, y;
+        xy_of(i, x, y);
+        return (uint16_t)(x | (y << 8));
+    };
     uint32_t* hist = reinterpret_cast<uint32_t*>(smem);
     uint32_t* cnt = hist + 256;
     uint16_t* om = reinterpret_cast<uint16_t*>(cnt + (DT == DT_U8 ? 0 : 256 * (nw + 1)));
@@ -154,22 +177,22 @@ __device__ void k1_sort_tile(const Geom& g, uint16_t* __restrict__ omega_out, un
     if (DT == DT_U8) {
         auto digit = [&](int i) {
             int x, y;
-            lin_to_xy(i, Sw, invS, x, y);
+            xy_of(i, x, y);
             return load_key(g, tc, y, x);
         };
-        auto emit = [&](int i, int dst) { om[dst] = pack_pos(i, Sw, invS); };
+        auto emit = [&](int i, int dst) { om[dst] = pos_of(i); };
         unstable_pass(N, hist, digit, emit);
     } else if (DT == DT_U16) {
         uint16_t* tpos = reinterpret_cast<uint16_t*>(big);
         uint8_t* thi = reinterpret_cast<uint8_t*>(tpos + g.Npad);
         auto d0 = [&](int i) {
             int x, y;
-            lin_to_xy(i, Sw, invS, x, y);
+            xy_of(i, x, y);
             return load_key(g, tc, y, x) & 0xffu;
         };
         auto e0 = [&](int i, int dst) {
             int x, y;
-            lin_to_xy(i, Sw, invS, x, y);
+            xy_of(i, x, y);
             tpos[dst] = (uint16_t)(x | (y << 8));
             thi[dst] = (uint8_t)(load_key(g, tc, y, x) >> 8);
         };
@@ -182,7 +205,7 @@ __device__ void k1_sort_tile(const Geom& g, uint16_t* __restrict__ omega_out, un
         uint16_t* posA = reinterpret_cast<uint16_t*>(keys + g.Npad);
         for (int i = threadIdx.x; i < N; i += blockDim.x) {
             int x, y;
-            lin_to_xy(i, Sw, invS, x, y);
+            xy_of(i, x, y);
             keys[i] = load_key(g, tc, y, x);
         }
         __syncthreads();
@@ -196,7 +219,7 @@ __device__ void k1_sort_tile(const Geom& g, uint16_t* __restrict__ omega_out, un
         auto e2 = [&](int k, int dst) { posA[dst] = om[k]; };
         stable_pass(N, cnt, d2, e2);
         auto d3 = [&](int k) { return keys[posA[k]] >> 24; };
-        auto e3 = [&](int k, int dst) { om[dst] = pack_pos(posA[k], Sw, invS); };
+        auto e3 = [&](int k, int dst) { om[dst] = pos_of(posA[k]); };
         stable_pass(N, cnt, d3, e3);
     }
     for (int i = N + threadIdx.x; i < g.Npad; i += blockDim.x) om[i] = 0xffffu;
@@ -455,21 +478,60 @@ __device__ __forceinline__ int max_copies(int X0, int S, int W) {
 
 __device__ __forceinline__ bool has_runs(const Geom& g, const TileCoord& tc) {
     const int X0 = tc.ox0 - g.r + g.vshift, Y0 = tc.oy0 - g.r + g.vshift;
-    return !g.fp && max_copies(X0, g.Sw, g.W) * max_copies(Y0, g.Sh, g.H) >= g.run_min;
+    return max_copies(X0, g.Sw, g.W) * max_copies(Y0, g.Sh, g.H) >= g.run_min;
 }
 
-__device__ __forceinline__ int pixel_weight(int cx, bool fx, int cy, bool fy, int run_min) {
-    const int m = cx * cy;
-    if (m < run_min) return 1;
-    return (fx && fy) ? m : 0;
+// Weight code of tile pixel (x, y) with copy counts cx, cy (fx, fy: it is the
+// first copy on that axis): the slots it takes in bits [0, 20) -- 1 for a
+// plain ranked pixel, the copies inside the tile footprint for the head of a
+// run, 0 otherwise -- plus kRunBit for a run head.  A run the footprint clips
+// to one slot stays a run: that slot is not the head's own position.
+constexpr int kRunBit = 1 << 20;
+__device__ __forceinline__ int wt_of(int code) { return code & (kRunBit - 1); }
+
+__device__ __forceinline__ int pixel_weight(const Geom& g, const uint32_t* fprow, int x, int cx, bool fx, int y,
+                                            int cy, bool fy) {
+    if (cx * cy < g.run_min) return in_footprint(fprow, x, y) ? 1 : 0;
+    if (!(fx && fy)) return 0;
+    const int w = fp_rect_count(fprow, x, cx, y, cy);
+    return w ? (w | kRunBit) : 0;
+}
+
+// The omega entries of a run ranked from rk: its copy rectangle (first copy
+// pos, cx x cy) row by row, each row clipped to the footprint; thread t0 of a
+// group of `step` writes every step-th position of a row.
+__device__ __forceinline__ void fill_run(const uint32_t* fprow, uint16_t* om, int rk, uint32_t pos, int cx, int cy,
+                                         int t0, int step) {
+    const int x0 = (int)(pos & 0xffu), y0 = (int)(pos >> 8);
+    for (int yy = y0; yy < y0 + cy; yy++) {
+        int lo = x0, hi = x0 + cx - 1;
+        if (fprow) {
+            const uint32_t v = __ldg(fprow + yy);
+            lo = max(lo, (int)(v & 0xffffu));
+            hi = min(hi, (int)(v >> 16));
+        }
+        for (int x = lo + t0; x <= hi; x += step) om[rk + x - lo] = (uint16_t)(x | (yy << 8));
+        rk += max(0, hi - lo + 1);
+    }
 }
 
 __device__ __forceinline__ void put_entry(uint32_t* ent, uint16_t* d16, int slot, uint32_t key16, int x, int y,
-                                          int w, int cx, int cy, RunList* rl) {
+                                          int code, int cx, int cy, RunList* rl, const uint32_t* fprow) {
     const uint32_t pos = (uint32_t)(x | (y << 8));
-    if (w == 1) {
+    const int w = wt_of(code);
+    if (!(code & kRunBit)) {
         ent[slot] = (key16 << 16) | pos;
         return;
+    }
+    if (w == 1 && fprow) {  // a run the footprint clips to one copy: a plain entry at that copy
+        for (int yy = y; yy < y + cy; yy++) {
+            const uint32_t v = __ldg(fprow + yy);
+            const int lo = max(x, (int)(v & 0xffffu));
+            if (lo <= min(x + cx - 1, (int)(v >> 16))) {
+                ent[slot] = (key16 << 16) | (uint32_t)(lo | (yy << 8));
+                return;
+            }
+        }
     }
     ent[slot] = (key16 << 16) | 0xffffu;
     if (d16) {
@@ -534,7 +596,7 @@ constexpr int kScanBudget = 32768;
 
 template <bool RUNS>
 __device__ void rank_buckets(const uint32_t* ent, const uint16_t* d16, const uint32_t* starts, int N, uint16_t* om,
-                             RunList* rl) {
+                             RunList* rl, const uint32_t* fprow) {
     const int nsw = (N + 31) >> 5;
     const int nlong = RUNS ? min(rl->nmark, kBigRuns) : 0;
     int work = 0;
@@ -611,23 +673,15 @@ __device__ void rank_buckets(const uint32_t* ent, const uint16_t* d16, const uin
                 continue;
             }
         }
-        for (int i = 0; i < len; i++) {
-            const int yy = i / cx, xx = i - yy * cx;
-            om[rk + i] = (uint16_t)(pos + (uint32_t)(xx | (yy << 8)));
-        }
+        fill_run(fprow, om, rk, pos, cx, (int)(d >> 24), 0, 1);
     }
 }
 
 // After the barrier closing rank_buckets: fill the long runs with the CTA.
-__device__ void fill_big_runs(uint16_t* om, const RunList* rl) {
+__device__ void fill_big_runs(uint16_t* om, const RunList* rl, const uint32_t* fprow) {
     for (int k = 0; k < min(rl->nbig, kBigRuns); k++) {
         const uint4 b = rl->big[k];
-        const int rk = (int)b.x, cx = (int)b.z, len = cx * (int)b.w;
-        const uint32_t pos = b.y;
-        for (int i = threadIdx.x; i < len; i += blockDim.x) {
-            const int yy = i / cx, xx = i - yy * cx;
-            om[rk + i] = (uint16_t)(pos + (uint32_t)(xx | (yy << 8)));
-        }
+        fill_run(fprow, om, (int)b.x, b.y, (int)b.z, (int)b.w, (int)threadIdx.x, (int)blockDim.x);
     }
 }
 
@@ -636,7 +690,7 @@ __device__ void fill_big_runs(uint16_t* om, const RunList* rl) {
 // EDGE: the tile reads clamped (replicated) image pixels; the copies of one
 // pixel are ranked as a run (pixel_weight).  Interior tiles take the EDGE =
 // false instance, which carries none of that.
-template <int NK, bool GENT, bool EDGE>
+template <int NK, bool GENT, bool EDGE, bool FP>
 __device__ __forceinline__ void f32_bucket_tile(const Geom& g, const TileCoord& tc, const int bt,
                                                 uint16_t* __restrict__ omega_out,
                                                 int* __restrict__ fallback, uint32_t* __restrict__ gent,
@@ -645,6 +699,7 @@ __device__ __forceinline__ void f32_bucket_tile(const Geom& g, const TileCoord& 
     constexpr int NW = 32768;  // histogram words (65536 16-bit counters)
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int S = g.Sw, SH = g.Sh, N = g.N;
+    const uint32_t* fpr = FP ? g.fprow : nullptr;  // footprint rows (FP: the plan ranks a footprint)
     uint32_t* hw = reinterpret_cast<uint32_t*>(smem);
     uint32_t* ent = GENT ? gent + bt * gent_stride : hw + NW;  // N entries
     // bucket starts, ceil(N/32) words; the coarse table (f32) aliases the
@@ -671,9 +726,10 @@ __device__ __forceinline__ void f32_bucket_tile(const Geom& g, const TileCoord& 
     __shared__ int s_runs;
     __shared__ RunList s_rl;
     uint32_t v[NK][NK];
-    // which of this thread's pixels are ranked: a mask for edge tiles (weights
-    // are costly to recompute), recomputed from the tile extent elsewhere (no
-    // registers held: the 1024-thread budget is 64 per thread)
+    // which of this thread's pixels are ranked (inside the tile and its
+    // footprint, weight > 0): a mask on edge and footprint tiles (weights and
+    // footprint rows are costly to recompute), recomputed from the tile extent
+    // otherwise (no registers held: the 1024-thread budget is 64 per thread)
     unsigned long long okm = 0;
     // replicate copies (rep_axis), edge tiles only, recomputed where used
     // (keeps the 1024-thread register budget for the keys)
@@ -685,11 +741,11 @@ __device__ __forceinline__ void f32_bucket_tile(const Geom& g, const TileCoord& 
         bool fx, fy;
         rep_axis(X0, lane + 32 * k, S, g.W, cx, fx);
         rep_axis(Y0, wid + 32 * j, SH, g.H, cy, fy);
-        return pixel_weight(cx, fx, cy, fy, g.run_min);
+        return pixel_weight(g, fpr, lane + 32 * k, cx, fx, wid + 32 * j, cy, fy);
     };
     auto okf = [&](int j, int k) -> bool {
-        if (EDGE) return (okm >> (j * NK + k)) & 1ull;
-        return wid + 32 * j < SH && lane + 32 * k < S && in_footprint(g, lane + 32 * k, wid + 32 * j);
+        if (EDGE || FP) return (okm >> (j * NK + k)) & 1ull;
+        return wid + 32 * j < SH && lane + 32 * k < S;
     };
     auto cnt_x = [&](int k) {
         int c;
@@ -717,9 +773,10 @@ __device__ __forceinline__ void f32_bucket_tile(const Geom& g, const TileCoord& 
             yy = yy < 0 ? 0 : (yy >= g.H ? g.H - 1 : yy);
 #pragma unroll
             for (int k = 0; k < NK; k++) {
-                const bool ok = y < SH && lane + 32 * k < S && in_footprint(g, lane + 32 * k, y) && weight(j, k) > 0;
+                const bool ok = y < SH && lane + 32 * k < S &&
+                                (EDGE ? weight(j, k) != 0 : in_footprint(fpr, lane + 32 * k, y));
                 v[j][k] = ok ? f32_key(g, tc, yy, xc[k]) : 0u;
-                if (EDGE) okm |= (ok ? 1ull : 0ull) << (j * NK + k);
+                if (EDGE || FP) okm |= (ok ? 1ull : 0ull) << (j * NK + k);
             }
         }
     }
@@ -743,7 +800,7 @@ __device__ __forceinline__ void f32_bucket_tile(const Geom& g, const TileCoord& 
             for (int j = 0; j < NK; j++)
 #pragma unroll
                 for (int k = 0; k < NK; k++)
-                    if (okf(j, k)) atomicAdd(&ctab[v[j][k] >> 20], (uint32_t)weight(j, k));
+                    if (okf(j, k)) atomicAdd(&ctab[v[j][k] >> 20], (uint32_t)wt_of(weight(j, k)));
             coarse_alloc(ctab, N);
         }
 #pragma unroll
@@ -759,9 +816,9 @@ __device__ __forceinline__ void f32_bucket_tile(const Geom& g, const TileCoord& 
         for (int k = 0; k < NK; k++)
             if (okf(j, k)) {
                 const uint32_t h = v[j][k] >> 16, sh = (h & 1) << 4;
-                const int wt = weight(j, k);
-                runs |= wt > 1;
-                atomicAdd(&hw[h >> 1], (uint32_t)wt << sh);
+                const int wc = weight(j, k);
+                runs |= (wc & kRunBit) != 0;
+                atomicAdd(&hw[h >> 1], (uint32_t)wt_of(wc) << sh);
             }
     if (runs) s_runs = 1;
     __syncthreads();
@@ -781,15 +838,15 @@ __device__ __forceinline__ void f32_bucket_tile(const Geom& g, const TileCoord& 
         for (int k = 0; k < NK; k++)
             if (okf(j, k)) {
                 const uint32_t key = v[j][k], h = key >> 16, sh = (h & 1) << 4;
-                const int wt = weight(j, k);
-                const uint32_t old = atomicAdd(&hw[h >> 1], (uint32_t)wt << sh);
+                const int wc = weight(j, k);
+                const uint32_t old = atomicAdd(&hw[h >> 1], (uint32_t)wt_of(wc) << sh);
                 if (OWN16 && own_rank) {
                     const uint32_t slot = (old >> sh) & 0xffffu;
                     l16[slot] = (uint16_t)(key & 0xffffu);
                     v[j][k] = (h << 16) | slot;
                 } else {
-                    put_entry(ent, d16, (old >> sh) & 0xffffu, key & 0xffffu, lane + 32 * k, wid + 32 * j, wt,
-                              cnt_x(k), cnt_y(j), &s_rl);
+                    put_entry(ent, d16, (old >> sh) & 0xffffu, key & 0xffffu, lane + 32 * k, wid + 32 * j, wc,
+                              cnt_x(k), cnt_y(j), &s_rl, fpr);
                 }
             }
     __syncthreads();
@@ -839,30 +896,32 @@ __device__ __forceinline__ void f32_bucket_tile(const Geom& g, const TileCoord& 
         return;
     }
     if (s_runs)
-        rank_buckets<true>(ent, d16, starts, N, om, &s_rl);
+        rank_buckets<true>(ent, d16, starts, N, om, &s_rl, fpr);
     else
-        rank_buckets<false>(ent, d16, starts, N, om, &s_rl);
+        rank_buckets<false>(ent, d16, starts, N, om, &s_rl, fpr);
     __syncthreads();
     if (s_rl.abort) {  // a scan over budget (block-uniform after the barrier)
         if (tid == 0) fallback[1 + atomicAdd(fallback, 1)] = bt;
         return;
     }
-    fill_big_runs(om, &s_rl);
+    fill_big_runs(om, &s_rl, fpr);
     for (int i = N + tid; i < g.Npad; i += blockDim.x) om[i] = 0xffffu;
     __syncthreads();
     store_omega(g, om, omega_slot(g, omega_out, bt));
 }
 
-template <int NK, bool GENT>
+// FP: the plan ranks a tile footprint (g.fprow); a separate instance, so the
+// footprint tests cost the usual (whole-tile) instance no registers.
+template <int NK, bool GENT, bool FP>
 __global__ void __launch_bounds__(1024) k1_f32_bucket(Geom g, uint16_t* __restrict__ omega_out,
                                                      int* __restrict__ fallback, uint32_t* __restrict__ gent,
                                                      long long gent_stride, unsigned long long max_sumsq) {
     const int bt = chunk_tile(g);  // costly (replicate-run) tiles start first
     const TileCoord tc = tile_coord(g, g.tile_begin + bt);
     if (has_runs(g, tc))
-        f32_bucket_tile<NK, GENT, true>(g, tc, bt, omega_out, fallback, gent, gent_stride, max_sumsq);
+        f32_bucket_tile<NK, GENT, true, FP>(g, tc, bt, omega_out, fallback, gent, gent_stride, max_sumsq);
     else
-        f32_bucket_tile<NK, GENT, false>(g, tc, bt, omega_out, fallback, gent, gent_stride, max_sumsq);
+        f32_bucket_tile<NK, GENT, false, FP>(g, tc, bt, omega_out, fallback, gent, gent_stride, max_sumsq);
 }
 
 // k1_f32_bucket for tiles too large for shared-memory entries (N > ~23.7K,
@@ -915,6 +974,9 @@ __global__ void __launch_bounds__(1024) k1_f32_bucket_g(Geom g, uint16_t* __rest
             int cy = 1;
             bool fy = true;
             if (edge) rep_axis(Y0, y, SH, g.H, cy, fy);
+            // footprint columns of this row (empty: lo = hi = 0xffff)
+            const uint32_t fr = g.fprow ? __ldg(g.fprow + y) : (uint32_t)(S - 1) << 16;
+            const int flo = (int)(fr & 0xffffu), fspan = (int)(fr >> 16) - flo;
             uint32_t kv[8];
 #pragma unroll
             for (int k = 0; k < 8; k++) {
@@ -930,9 +992,12 @@ __global__ void __launch_bounds__(1024) k1_f32_bucket_g(Geom g, uint16_t* __rest
                 if (k < nk && x < S) {
                     int cx = 1;
                     bool fx = true;
-                    if (edge) rep_axis(X0, x, S, g.W, cx, fx);
-                    const int wt = pixel_weight(cx, fx, cy, fy, g.run_min);
-                    if (wt) fn(x, y, kv[k], wt, cx, cy);
+                    int wc = (unsigned)(x - flo) <= (unsigned)fspan ? 1 : 0;
+                    if (edge) {
+                        rep_axis(X0, x, S, g.W, cx, fx);
+                        wc = pixel_weight(g, g.fprow, x, cx, fx, y, cy, fy);
+                    }
+                    if (wc) fn(x, y, kv[k], wc, cx, cy);
                 }
             }
         }
@@ -945,16 +1010,16 @@ __global__ void __launch_bounds__(1024) k1_f32_bucket_g(Geom g, uint16_t* __rest
         for (int i = tid; i < kCoarse; i += blockDim.x) ctab[i] = g.ctab_g ? g.ctab_g[i] : 0u;
         __syncthreads();
         if (!g.ctab_g) {  // no call-wide table: this tile's own coarse pass
-            each_pixel([&](int, int, uint32_t key, int wt, int, int) { atomicAdd(&ctab[key >> 20], (uint32_t)wt); });
+            each_pixel([&](int, int, uint32_t key, int wc, int, int) { atomicAdd(&ctab[key >> 20], (uint32_t)wt_of(wc)); });
             coarse_alloc(ctab, N);
         }
         PHASE(1);
     }
     bool runs = false;
-    each_pixel([&](int, int, uint32_t key, int wt, int, int) {
-        runs |= wt > 1;
+    each_pixel([&](int, int, uint32_t key, int wc, int, int) {
+        runs |= (wc & kRunBit) != 0;
         const uint32_t h = bucket_key(key) >> 16, sh = (h & 1) << 4;
-        atomicAdd(&hw[h >> 1], (uint32_t)wt << sh);
+        atomicAdd(&hw[h >> 1], (uint32_t)wt_of(wc) << sh);
     });
     if (runs) s_runs = 1;
     __syncthreads();
@@ -965,10 +1030,10 @@ __global__ void __launch_bounds__(1024) k1_f32_bucket_g(Geom g, uint16_t* __rest
         if (tid == 0) fallback[1 + atomicAdd(fallback, 1)] = bt;
         return;
     }
-    each_pixel([&](int x, int y, uint32_t key, int wt, int cx, int cy) {
+    each_pixel([&](int x, int y, uint32_t key, int wc, int cx, int cy) {
         const uint32_t bk = bucket_key(key), h = bk >> 16, sh = (h & 1) << 4;
-        const uint32_t old = atomicAdd(&hw[h >> 1], (uint32_t)wt << sh);
-        put_entry(ent, d16, (old >> sh) & 0xffffu, bk & 0xffffu, x, y, wt, cx, cy, &s_rl);
+        const uint32_t old = atomicAdd(&hw[h >> 1], (uint32_t)wt_of(wc) << sh);
+        put_entry(ent, d16, (old >> sh) & 0xffffu, bk & 0xffffu, x, y, wc, cx, cy, &s_rl, g.fprow);
     });
     __syncthreads();  // block-scope ordering of the entry stores (global, same CTA)
     mark_runs(ent, &s_rl);
@@ -979,16 +1044,16 @@ __global__ void __launch_bounds__(1024) k1_f32_bucket_g(Geom g, uint16_t* __rest
         return;
     }
     if (s_runs)
-        rank_buckets<true>(ent, d16, starts, N, om, &s_rl);
+        rank_buckets<true>(ent, d16, starts, N, om, &s_rl, g.fprow);
     else
-        rank_buckets<false>(ent, d16, starts, N, om, &s_rl);
+        rank_buckets<false>(ent, d16, starts, N, om, &s_rl, g.fprow);
     __syncthreads();
     PHASE(4);
     if (s_rl.abort) {  // a scan over budget (block-uniform after the barrier)
         if (tid == 0) fallback[1 + atomicAdd(fallback, 1)] = bt;
         return;
     }
-    fill_big_runs(om, &s_rl);
+    fill_big_runs(om, &s_rl, g.fprow);
     for (int i = N + tid; i < g.Npad; i += blockDim.x) om[i] = 0xffffu;
     __syncthreads();
     store_omega(g, om, omega_slot(g, omega_out, bt));
@@ -1000,11 +1065,12 @@ size_t k1_f32_bucket_g_smem_bytes(int N) {
     return 32768 * 4 + 4 * (size_t)(((N + 31) >> 5) + 3 & ~3) + 4 * (size_t)kCoarse + 16;
 }
 
-#define IMF_K1F(NK)                                                                                  \
-    template __global__ void k1_f32_bucket<NK, false>(Geom, uint16_t*, int*, uint32_t*, long long,  \
-                                                      unsigned long long);                          \
-    template __global__ void k1_f32_bucket<NK, true>(Geom, uint16_t*, int*, uint32_t*, long long,   \
-                                                     unsigned long long);
+#define IMF_K1F1(NK, FP)                                                                             \
+    template __global__ void k1_f32_bucket<NK, false, FP>(Geom, uint16_t*, int*, uint32_t*, long long, \
+                                                          unsigned long long);                      \
+    template __global__ void k1_f32_bucket<NK, true, FP>(Geom, uint16_t*, int*, uint32_t*, long long,  \
+                                                         unsigned long long);
+#define IMF_K1F(NK) IMF_K1F1(NK, false) IMF_K1F1(NK, true)
 IMF_K1F(1)
 IMF_K1F(2)
 IMF_K1F(3)

@@ -47,6 +47,10 @@ VARIANTS = [
     {"IMF_GCOARSE": "2"},    # call-wide coarse bucket table for every adaptive f32 tile
     {"IMF_GCOARSE": "0"},    # per-tile coarse passes only
     {"IMF_K1_COUNT_G": "0"},  # u16 tiles beyond the shared counting sort via the bucket transform
+    {"IMF_MAXSUMSQ_K": "0"},  # every run-free f32 tile to the LSD fallback (footprint index map at r=100)
+    {"IMF_F32_FOOTPRINT": "2"},  # f32 footprint on the shared-entry bucket kernels too
+    {"IMF_F32_FOOTPRINT": "2", "IMF_MAXSUMSQ_K": "0"},
+    {"IMF_F32_FOOTPRINT": "2", "IMF_RUNMIN": "2"},  # runs clipped by the footprint
 ]
 
 CASES = [  # (dtype, shape, kernel spec)
@@ -59,6 +63,7 @@ CASES = [  # (dtype, shape, kernel spec)
     ("float32", (300, 280), ("circle", 100, 0, 0.0)),     # f32 r=100: corner runs (bucket_g), wide pair K2
     ("uint8", (230, 210, 2), ("circle", 75, 0, 0.0)),     # wide pair K2 (T + r > 128), u8
     ("uint8", (190, 170, 2), ("regular_polygon", 11, 6, 15.0)),
+    ("float32", (200, 190), ("regular_polygon", 30, 7, 12.0)),  # f32 polygon footprint
     ("uint8", (120, 130), ("square", 7, 0, 0.0)),
     ("float32", (70, 90), ("circle", 2, 0, 0.0)),         # direct selection (area <= 32)
     ("uint16", (65, 77, 3), ("square", 2, 0, 0.0)),

@@ -66,11 +66,20 @@ def test_planar_u16_uses_tma_when_aligned():
     assert p["tma"] == 0                   # rows of 15,362 bytes are not 16-byte multiples
 
 
-def test_square_and_f32_plans_have_no_footprint():
+def test_square_has_no_footprint():
     p, _ = plan((2160, 3840, 3), ShapeSpec("square", 32), dtype=0)
     assert p["fp"] == 0 and p["N"] == p["Sw"] * p["Sh"]
-    p, _ = plan((2048, 2048, 1), ShapeSpec("circle", 64), dtype=2)
-    assert p["fp"] == 0 and p["k1"] in (1, 2) and p["N"] == 192 * 192
+
+
+@pytest.mark.parametrize("r", [8, 32, 64, 100])
+def test_f32_bucket_plans_rank_the_footprint(r, monkeypatch):
+    spec = ShapeSpec("circle", r)
+    p, _ = plan((2048, 2048, 1), spec, dtype=2)
+    assert p["fp"] == (1 if r == 100 else 0)  # auto: the global-entries kernel (S > 192) only
+    monkeypatch.setenv("IMF_F32_FOOTPRINT", "2")
+    p, k = plan((2048, 2048, 1), spec, dtype=2)
+    assert p["fp"] == 1 and p["k1"] in (1, 2)
+    assert p["N"] == brute_footprint(k, p["Tw"], p["Th"], p["Sw"], p["Sh"], r) < p["Sw"] * p["Sh"]
 
 
 def test_direct_selection_for_tiny_windows():
