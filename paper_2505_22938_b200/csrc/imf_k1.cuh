@@ -214,20 +214,26 @@ __device__ __forceinline__ void hist16_scan_lanes(uint32_t* hw) {
     }
     __syncthreads();
     const uint32_t base = wt[wid] + incl - T;  // counters before the lane's first word
-    uint32_t run = pre;                          // packed counters before the current chunk
+    // running exclusive prefix, unpacked: per word (counters lo, hi) the
+    // output is s | (s + lo) << 16 and s advances by lo + hi -- LOP3, IADD,
+    // LEA.HI and one PRMT per word
+    uint32_t s = base + (pre & 0xffffu) + (pre >> 16);
+    auto step = [&](uint32_t w) {
+        const uint32_t e0 = s, e1 = s + (w & 0xffffu);
+        s = e1 + (w >> 16);
+        uint32_t r;
+        asm("prmt.b32 %0, %1, %2, 0x5410;" : "=r"(r) : "r"(e0), "r"(e1));
+        return r;
+    };
 #pragma unroll
     for (int i = 0; i < CH; i++) {
         const int k = (a + i) & (CH - 1);
-        if (k == 0) run = 0;  // wrapped to the lane's first chunk
+        if (k == 0) s = base;  // wrapped to the lane's first chunk
         uint4 q = wb[k];
-        const uint32_t p1 = run + q.x, p2 = p1 + q.y, p3 = p2 + q.z;
-        const uint32_t b0 = base + (run & 0xffffu) + (run >> 16), b1 = base + (p1 & 0xffffu) + (p1 >> 16);
-        const uint32_t b2 = base + (p2 & 0xffffu) + (p2 >> 16), b3 = base + (p3 & 0xffffu) + (p3 >> 16);
-        run = p3 + q.w;
-        q.x = b0 | ((b0 + (q.x & 0xffffu)) << 16);
-        q.y = b1 | ((b1 + (q.y & 0xffffu)) << 16);
-        q.z = b2 | ((b2 + (q.z & 0xffffu)) << 16);
-        q.w = b3 | ((b3 + (q.w & 0xffffu)) << 16);
+        q.x = step(q.x);
+        q.y = step(q.y);
+        q.z = step(q.z);
+        q.w = step(q.w);
         wb[k] = q;
     }
     (void)NW;
