@@ -1074,8 +1074,10 @@ static bool rows_outermost(const imf_image* im) {
 }
 
 namespace {
+constexpr int kMaxStripeLanes = 4;
 struct HostStreams {
-    cudaStream_t up = nullptr, down = nullptr, comp2 = nullptr;
+    cudaStream_t up = nullptr, down = nullptr;
+    cudaStream_t comp[kMaxStripeLanes] = {};  // comp[0] unused: lane 0 is the caller's stream
 };
 thread_local HostStreams g_hs_dev[kMaxDev];  // per (thread, device), created once
 }  // namespace
@@ -1106,7 +1108,9 @@ int imf_filter_host(const imf_image* src, imf_image* dst, const imf_kernel* kern
     if (!g_hs.up) {
         if (cudaStreamCreateWithFlags(&g_hs.up, cudaStreamNonBlocking) ||
             cudaStreamCreateWithFlags(&g_hs.down, cudaStreamNonBlocking) ||
-            cudaStreamCreateWithFlags(&g_hs.comp2, cudaStreamNonBlocking))
+            cudaStreamCreateWithFlags(&g_hs.comp[1], cudaStreamNonBlocking) ||
+            cudaStreamCreateWithFlags(&g_hs.comp[2], cudaStreamNonBlocking) ||
+            cudaStreamCreateWithFlags(&g_hs.comp[3], cudaStreamNonBlocking))
             return cuda_fail(cudaGetLastError(), "stream create");
         // keep freed pool memory cached across calls (default threshold 0 returns
         // it to the driver at every synchronization)
@@ -1116,7 +1120,8 @@ int imf_filter_host(const imf_image* src, imf_image* dst, const imf_kernel* kern
             cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
         }
     }
-    void *dsrc = nullptr, *ddst = nullptr, *dws = nullptr, *dws2 = nullptr, *dtm = nullptr;
+    void *dsrc = nullptr, *ddst = nullptr, *dtm = nullptr;
+    void* dws[kMaxStripeLanes] = {};
     std::vector<cudaEvent_t> evs;
     // IMF_HOST_TRACE=1: timed events, and a per-stripe timeline on stderr (dev aid)
     const bool trace = env_int("IMF_HOST_TRACE", 0) != 0;
@@ -1135,9 +1140,9 @@ int imf_filter_host(const imf_image* src, imf_image* dst, const imf_kernel* kern
     };
     mark("start", 0, s);
     int rc = IMF_OK;
-    // two compute lanes (stripes alternate between them, each with its own
+    // compute lanes (stripes rotate over them, each with its own
     // workspace) so one stripe's K1 fills the tail of the previous stripe's K2
-    const bool two = env_int("IMF_STRIPE_LANES", 2) > 1;
+    const int nl0 = std::max(1, std::min(kMaxStripeLanes, env_int("IMF_STRIPE_LANES", 2)));
     const int OH0 = p.full_out_h;
     // output rows [R0, R1) (opt->row_begin/row_end: one device's stripe of a
     // multi-device job; the other rows of dst are left untouched)
@@ -1145,6 +1150,7 @@ int imf_filter_host(const imf_image* src, imf_image* dst, const imf_kernel* kern
     const int R0 = ranged ? opt->row_begin : 0, R1 = ranged ? opt->row_end : OH0;
     const bool pipe0 = rows_outermost(src) && rows_outermost(dst) && (ranged || OH0 > 2 * p.g.Th);
     if (ranged && !pipe0) return IMF_ERR_INVALID;  // row ranges need row-outermost layouts
+    const int nl = pipe0 ? nl0 : 1;
     // batches stream through a ring of two device image slots (image b in slot
     // b % 2, reused once image b - 2 is downloaded): device memory and the
     // per-call allocation stay two images deep however long the batch
@@ -1152,9 +1158,10 @@ int imf_filter_host(const imf_image* src, imf_image* dst, const imf_kernel* kern
     const int nslot = ring ? 2 : src->batch;
     const size_t sbA = ring ? (size_t)nslot * src->stride_b * dsz : sb;
     const size_t dbA = ring ? (size_t)nslot * dst->stride_b * dsz : db;
-    if (cudaMallocAsync(&dsrc, sbA, s) || cudaMallocAsync(&ddst, dbA, s) || cudaMallocAsync(&dws, p.ws_total, s) ||
-        (two && cudaMallocAsync(&dws2, p.ws_total, s)) || (tb && cudaMallocAsync(&dtm, tb, s)))
+    if (cudaMallocAsync(&dsrc, sbA, s) || cudaMallocAsync(&ddst, dbA, s) || (tb && cudaMallocAsync(&dtm, tb, s)))
         rc = cuda_fail(cudaGetLastError(), "cudaMallocAsync");
+    for (int i = 0; i < nl && !rc; i++)
+        if (cudaMallocAsync(&dws[i], p.ws_total, s)) rc = cuda_fail(cudaGetLastError(), "cudaMallocAsync");
     if (!rc && tb && cudaMemcpyAsync(dtm, target_map, tb, cudaMemcpyHostToDevice, s))
         rc = cuda_fail(cudaGetLastError(), "target map upload");
     cudaEvent_t e_alloc = event();
@@ -1175,12 +1182,24 @@ int imf_filter_host(const imf_image* src, imf_image* dst, const imf_kernel* kern
         const int tiles_y = (R1 - R0 + p.g.Th - 1) / p.g.Th;
         const int edge = std::max(1, env_int("IMF_STRIPE_EDGE", 1));
         const int mid = std::max(1, env_int("IMF_STRIPE_MID", 8));
-        if (tiles_y <= 2 * edge + 1) {
+        // ramp (IMF_STRIPE_RAMP=1): after the one-tile-row first stripe, stripes
+        // of 1 and 2 tile rows, so the GPU fills while the larger middle
+        // stripes upload; mirrored (2, 1) before the last one-row stripe
+        const int ramp = env_int("IMF_STRIPE_RAMP", 1) ? 3 : 0;  // tile rows in the ramp stripes, each end
+        if (tiles_y <= 2 * (edge + ramp) + 1) {
             for (int t = 1; t <= tiles_y; t++) cuts.push_back(t);
         } else {
             cuts.push_back(edge);
-            const int body = tiles_y - 2 * edge;
-            for (int i = 1; i <= mid; i++) cuts.push_back(edge + (int)((long long)body * i / mid));
+            if (ramp) {
+                cuts.push_back(edge + 1);
+                cuts.push_back(edge + 3);
+            }
+            const int lo = edge + ramp, body = tiles_y - 2 * (edge + ramp);
+            for (int i = 1; i <= mid; i++) cuts.push_back(lo + (int)((long long)body * i / mid));
+            if (ramp) {
+                cuts.push_back(tiles_y - edge - 1);
+                cuts.push_back(tiles_y - edge);
+            }
             cuts.push_back(tiles_y);
         }
         for (int& c : cuts) c = std::min(R1, R0 + c * p.g.Th);
@@ -1191,7 +1210,7 @@ int imf_filter_host(const imf_image* src, imf_image* dst, const imf_kernel* kern
     int nstripe = 0;
     if (!rc) {
         cudaStreamWaitEvent(g_hs.up, e_alloc, 0);
-        if (two) cudaStreamWaitEvent(g_hs.comp2, e_alloc, 0);
+        for (int i = 1; i < nl; i++) cudaStreamWaitEvent(g_hs.comp[i], e_alloc, 0);
         std::vector<cudaEvent_t> slot_free(nslot, nullptr);  // ring: last download of the slot's image
         for (int bi = 0; bi < src->batch && !rc; bi++) {
             // host offsets of image bi; device offsets of its slot
@@ -1219,16 +1238,16 @@ int imf_filter_host(const imf_image* src, imf_image* dst, const imf_kernel* kern
                     if (cudaMemcpyAsync(dsrc, src->data, sb, cudaMemcpyHostToDevice, g_hs.up))
                         rc = cuda_fail(cudaGetLastError(), "upload");
                 }
-                const int lane_i = (two && pipe) ? (nstripe & 1) : 0;
-                cudaStream_t cs = lane_i ? g_hs.comp2 : s;
-                void* wsl = lane_i ? dws2 : dws;
+                const int lane_i = nstripe % nl;
+                cudaStream_t cs = lane_i ? g_hs.comp[lane_i] : s;
+                void* wsl = dws[lane_i];
                 mark("uploaded", nstripe, g_hs.up);
                 cudaEvent_t e_up = event();
                 cudaEventRecord(e_up, g_hs.up);
                 cudaStreamWaitEvent(cs, e_up, 0);
                 imf_options o = *opt;
                 o.flags &= ~IMF_FLAG_PROFILE;
-                if (nstripe >= (two && pipe ? 2 : 1)) o.flags |= IMF_FLAG_KEEP_STATUS;  // earlier defects persist
+                if (nstripe >= nl) o.flags |= IMF_FLAG_KEEP_STATUS;  // earlier defects persist
                 nstripe++;
                 o.row_begin = y0;
                 o.row_end = y1;
@@ -1273,17 +1292,16 @@ int imf_filter_host(const imf_image* src, imf_image* dst, const imf_kernel* kern
     cudaEvent_t e_end = event();
     cudaEventRecord(e_end, g_hs.down);
     cudaStreamWaitEvent(s, e_end, 0);
-    if (two) {
-        cudaEvent_t e_c2 = event();
-        cudaEventRecord(e_c2, g_hs.comp2);
-        cudaStreamWaitEvent(s, e_c2, 0);
+    for (int i = 1; i < nl; i++) {
+        cudaEvent_t e_c = event();
+        cudaEventRecord(e_c, g_hs.comp[i]);
+        cudaStreamWaitEvent(s, e_c, 0);
     }
-    if (!rc) rc = imf_workspace_status(dws, stream);  // synchronizes s
-    if (!rc && two && nstripe > 1) rc = imf_workspace_status(dws2, stream);
+    for (int i = 0; i < std::min(nl, std::max(nstripe, 1)) && !rc; i++) rc = imf_workspace_status(dws[i], stream);  // synchronizes s
     if (dsrc) cudaFreeAsync(dsrc, s);
     if (ddst) cudaFreeAsync(ddst, s);
-    if (dws) cudaFreeAsync(dws, s);
-    if (dws2) cudaFreeAsync(dws2, s);
+    for (int i = 0; i < nl; i++)
+        if (dws[i]) cudaFreeAsync(dws[i], s);
     if (dtm) cudaFreeAsync(dtm, s);
     cudaStreamSynchronize(s);
     if (trace && !tl.empty()) {
