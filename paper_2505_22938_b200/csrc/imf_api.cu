@@ -280,13 +280,14 @@ int make_plan(const imf_image* src, const imf_kernel* k, const imf_options* opt,
     // rounded rectangle (c2: 25,600 -> 23,616 pixels); squares the whole tile.
     const bool k1reg = p.k1_count && ((g.Sw + 31) >> 5) <= 6 && env_int("IMF_K1REG", 1) &&
                        (long long)(g.H - 1) * g.s_y + (long long)(g.W - 1) * g.s_x < (1ll << 31);
-    // f32: the footprint pays on the global-entries kernel (S > 192: every
-    // ranked pixel costs scattered L2 traffic); on the shared-entries kernels
-    // its per-pixel tests cost what the ~10 % fewer pixels save (c3 r=64:
-    // K1 +0.5 %, path +3 %).  IMF_F32_FOOTPRINT: 0 never, 1 auto, 2 always.
+    // f32: the footprint pays on the shared-entry bucket kernel (S <= 160:
+    // c3 r=32 / 48 -2 / -3 %) and the global-entries kernel (S > 192: r=100
+    // -7 %), not on the 16-bit-entry kernel in between (161..192, r=64: its
+    // register spills cost K1 more than the 10 % fewer pixels save; path
+    // +13 %).  IMF_F32_FOOTPRINT: 0 never, 1 auto, 2 always.
     const int f32fp = env_int("IMF_F32_FOOTPRINT", 1);
-    const bool fp_k1 = k1reg || (g.dtype == DT_F32 && p.k1_f32b &&
-                                 (f32fp == 2 || (f32fp == 1 && p.k1_f32b_g && ((g.Sw + 31) >> 5) > 6)));
+    const bool own16 = p.k1_f32b_g && ((g.Sw + 31) >> 5) <= 6;
+    const bool fp_k1 = k1reg || (g.dtype == DT_F32 && p.k1_f32b && (f32fp == 2 || (f32fp == 1 && !own16)));
     if (p.pair && k->shape_code != IMF_SHAPE_SQUARE && fp_k1 && g.Sh <= 256 && env_int("IMF_FOOTPRINT", 1)) {
         // the table depends on the kernel's row spans and the tile geometry only:
         // memoized per thread (the host pipeline plans every stripe of a frame)

@@ -727,9 +727,14 @@ __device__ __forceinline__ void f32_bucket_tile(const Geom& g, const TileCoord& 
     __shared__ RunList s_rl;
     uint32_t v[NK][NK];
     // which of this thread's pixels are ranked (inside the tile and its
-    // footprint, weight > 0): a mask on edge and footprint tiles (weights and
-    // footprint rows are costly to recompute), recomputed from the tile extent
-    // otherwise (no registers held: the 1024-thread budget is 64 per thread)
+    // footprint, weight > 0): a mask on edge tiles (weights are costly to
+    // recompute); on interior tiles an unranked slot holds the key kSent
+    // instead (no register held, one compare per test: the 1024-thread budget
+    // is 64 registers).  A ranked key equal to kSent -- the NaN 0x7fffffff, or
+    // a fine-bucket entry 0xffff'ffff -- sends the tile to the LSD fallback.
+    constexpr uint32_t kSent = 0xffffffffu;
+    __shared__ int s_collide;
+    bool coll = false;
     unsigned long long okm = 0;
     // replicate copies (rep_axis), edge tiles only, recomputed where used
     // (keeps the 1024-thread register budget for the keys)
@@ -744,8 +749,8 @@ __device__ __forceinline__ void f32_bucket_tile(const Geom& g, const TileCoord& 
         return pixel_weight(g, fpr, lane + 32 * k, cx, fx, wid + 32 * j, cy, fy);
     };
     auto okf = [&](int j, int k) -> bool {
-        if (EDGE || FP) return (okm >> (j * NK + k)) & 1ull;
-        return wid + 32 * j < SH && lane + 32 * k < S;
+        if (EDGE) return (okm >> (j * NK + k)) & 1ull;
+        return v[j][k] != kSent;
     };
     auto cnt_x = [&](int k) {
         int c;
@@ -775,8 +780,13 @@ __device__ __forceinline__ void f32_bucket_tile(const Geom& g, const TileCoord& 
             for (int k = 0; k < NK; k++) {
                 const bool ok = y < SH && lane + 32 * k < S &&
                                 (EDGE ? weight(j, k) != 0 : in_footprint(fpr, lane + 32 * k, y));
-                v[j][k] = ok ? f32_key(g, tc, yy, xc[k]) : 0u;
-                if (EDGE || FP) okm |= (ok ? 1ull : 0ull) << (j * NK + k);
+                if (EDGE) {
+                    v[j][k] = ok ? f32_key(g, tc, yy, xc[k]) : 0u;
+                    okm |= (ok ? 1ull : 0ull) << (j * NK + k);
+                } else {
+                    v[j][k] = ok ? f32_key(g, tc, yy, xc[k]) : kSent;
+                    coll |= ok && v[j][k] == kSent;
+                }
             }
         }
     }
@@ -789,7 +799,7 @@ __device__ __forceinline__ void f32_bucket_tile(const Geom& g, const TileCoord& 
             for (int i = tid; i < kCoarse; i += blockDim.x) ctab[i] = g.ctab_g ? g.ctab_g[i] : 0u;
         if (tid == 0) {
             s_sumsq = 0;
-            s_runs = s_rl.n = s_rl.nbig = s_rl.nmark = s_rl.abort = 0;
+            s_runs = s_rl.n = s_rl.nbig = s_rl.nmark = s_rl.abort = s_collide = 0;
         }
     }
     __syncthreads();
@@ -807,7 +817,10 @@ __device__ __forceinline__ void f32_bucket_tile(const Geom& g, const TileCoord& 
         for (int j = 0; j < NK; j++)
 #pragma unroll
             for (int k = 0; k < NK; k++)
-                if (okf(j, k)) v[j][k] = (fine_bucket(ctab, v[j][k]) << 16) | (v[j][k] & 0xffffu);
+                if (okf(j, k)) {
+                    v[j][k] = (fine_bucket(ctab, v[j][k]) << 16) | (v[j][k] & 0xffffu);
+                    if (!EDGE) coll |= v[j][k] == kSent;
+                }
     }
     bool runs = false;
 #pragma unroll
@@ -821,6 +834,7 @@ __device__ __forceinline__ void f32_bucket_tile(const Geom& g, const TileCoord& 
                 atomicAdd(&hw[h >> 1], (uint32_t)wt_of(wc) << sh);
             }
     if (runs) s_runs = 1;
+    if (coll) s_collide = 1;
     __syncthreads();
     PHASE(7);
     hist16_exclusive_scan(hw, NW, own_rank ? nullptr : starts, &s_sumsq);
@@ -828,7 +842,7 @@ __device__ __forceinline__ void f32_bucket_tile(const Geom& g, const TileCoord& 
     PHASE(8);
     // tiles with runs skip the estimate (run weights inflate it); their scans
     // are budgeted instead (rank_buckets)
-    if (!s_runs && s_sumsq > max_sumsq) {  // block-uniform: hand the tile to the radix sort
+    if ((!s_runs && s_sumsq > max_sumsq) || s_collide) {  // block-uniform: hand the tile to the radix sort
         if (tid == 0) fallback[1 + atomicAdd(fallback, 1)] = bt;
         return;
     }

@@ -120,3 +120,25 @@ def test_direct_selection_maps_bracket_tiny_images(dt):
         outs = filter_image_bracket(img, FilterParams(shape=ShapeSpec("circle", 2)), [0.0, 0.5, 1.0])
         for out, p in zip(outs, (0.0, 0.5, 1.0)):
             assert out.tobytes() == oracle.fast_filter(img, ShapeSpec("circle", 2), p).tobytes()
+
+
+@pytest.mark.parametrize("fp", ["1", "2"])
+def test_f32_sentinel_key_collision(fp, monkeypatch):
+    """Interior tiles of the bucket K1 mark unranked slots with the entry
+    0xffffffff.  A ranked pixel can map to that entry too: values in ONE
+    coarse bin (key >> 20) get all 65,536 fine buckets, and +FLT_MAX lands in
+    the last one with low key bits 0xffff.  Such tiles must take the LSD
+    fallback and stay bit-exact."""
+    from paper_2505_22938_b200 import FilterParams, ShapeSpec, filter_image
+    monkeypatch.setenv("IMF_F32_FOOTPRINT", fp)
+    rng = np.random.default_rng(7)
+    fmax = np.finfo(np.float32).max
+    # [1.875 * 2^127, FLT_MAX]: one coarse bin (key 0xff7xxxxx)
+    img = rng.uniform(1.875 * 2.0 ** 127, float(fmax), (300, 290)).astype(np.float32)
+    img[rng.integers(40, 260, 60), rng.integers(40, 250, 60)] = fmax
+    assert len(np.unique(img.view(np.uint32) >> 20)) == 1
+    for r in (40, 60):
+        params = FilterParams(shape=ShapeSpec("circle", r), percentile=0.5)
+        got = filter_image(img, params)
+        want = oracle.fast_filter(img, params.shape, 0.5, "replicate")
+        assert got.tobytes() == want.tobytes(), r

@@ -75,7 +75,7 @@ def test_square_has_no_footprint():
 def test_f32_bucket_plans_rank_the_footprint(r, monkeypatch):
     spec = ShapeSpec("circle", r)
     p, _ = plan((2048, 2048, 1), spec, dtype=2)
-    assert p["fp"] == (1 if r == 100 else 0)  # auto: the global-entries kernel (S > 192) only
+    assert p["fp"] == (0 if r == 64 else 1)  # auto: not on the 16-bit-entry kernel (S 161..192)
     monkeypatch.setenv("IMF_F32_FOOTPRINT", "2")
     p, k = plan((2048, 2048, 1), spec, dtype=2)
     assert p["fp"] == 1 and p["k1"] in (1, 2)
