@@ -761,22 +761,32 @@ __global__ void __launch_bounds__(512, 2) k2_pair(Geom g, PairParams p, const __
                 if (lane == 0 && cnt) atomicAdd(&rowd[TY], cnt);
             }
             // down-slide deltas (entering < Pq) - (exiting < Pq) of the column-cs
-            // window from row y to y+1: lanes = rows, warps split the column list
-            const int nr = ybot - ytop;
-            if (nr > 0) {
-                const int nrc = (nr + 31) >> 5, kc_n = max(1, nwarps / nrc);
-                for (int u = wid; u < nrc * kc_n; u += nwarps) {
-                    const int rc = u / kc_n, kc = u - rc * kc_n;
-                    const int y = ytop + rc * 32 + lane;
-                    const int k0 = kc * p.nv / kc_n, k1 = (kc + 1) * p.nv / kc_n;
-                    const uint32_t b = I_a + 2 * (min(y, ybot - 1) * Sw + cs);
-                    int d = 0;
-                    for (int k = k0; k < k1; k++) {
+            // window from row y to y+1: warps = rows, lanes = kernel columns
+            // (their offsets loaded once into registers), one warp reduction
+            // per row.  (Lanes = rows would put the lanes 2*Sw bytes apart:
+            // 16-way shared bank conflicts.)
+            if (ybot > ytop) {
+                int2 ov[8];  // entering / exiting byte offsets of columns lane + 32i (nv <= 249)
+#pragma unroll
+                for (int i = 0; i < 8; i++) {
+                    const int k = lane + 32 * i;
+                    ov[i] = make_int2(0, 0);
+                    if (k < p.nv) {
                         const int2 o = kt.v[k];
                         const int adj = k >= p.nv_even ? 2 : 0;  // odd entries: the high half of the word
-                        d += ((int)lds16(b + o.x + adj) < Pq) - ((int)lds16(b + o.y + adj) < Pq);
+                        ov[i] = make_int2(o.x + adj, o.y + adj);
                     }
-                    if (y < ybot && d) atomicAdd(&rowd[y], d);
+                }
+                const int nvk = (p.nv + 31) >> 5;
+                for (int y = ytop + wid; y < ybot; y += nwarps) {
+                    const uint32_t b = I_a + 2 * (y * Sw + cs);
+                    int d = 0;
+#pragma unroll
+                    for (int i = 0; i < 8; i++)
+                        if (i < nvk && lane + 32 * i < p.nv)
+                            d += ((int)lds16(b + ov[i].x) < Pq) - ((int)lds16(b + ov[i].y) < Pq);
+                    d = (int)__reduce_add_sync(0xffffffffu, (unsigned)d);
+                    if (lane == 0) rowd[y] = d;
                 }
             }
         }

@@ -15,6 +15,7 @@ raw = page("raw"); d = dict(zip(raw[0], raw[2]))
 kname = d["Kernel Name"]
 src = page("source"); h = src[1]
 ia, iss, ith = h.index("Instructions Executed"), h.index("Warp Stall Sampling (All Samples)"), h.index("Thread Instructions Executed")
+iwf, iwx = h.index("L1 Wavefronts Shared"), h.index("L1 Wavefronts Shared Excessive")
 rows = [r for r in src[2:] if r[ia].isdigit()]
 base = int(rows[0][0], 16)
 tmp = tempfile.mkdtemp()
@@ -51,19 +52,21 @@ for ln in lines_all[start + 1:]:
     m = re.match(r"\s*/\*([0-9a-f]{4,})\*/", ln)
     if m and cur:
         line_of[int(m.group(1), 16)] = cur
-agg = collections.defaultdict(lambda: [0, 0, 0])
-tot = [0, 0, 0]
+agg = collections.defaultdict(lambda: [0, 0, 0, 0, 0])
+tot = [0, 0, 0, 0, 0]
+num = lambda x: int(x) if x.isdigit() else 0
 for r in rows:
     off = int(r[0], 16) - base
     key = line_of.get(off, ("?", 0))
-    v = (int(r[ia]), int(r[ith]), int(r[iss]))
-    for i in range(3):
+    v = (int(r[ia]), int(r[ith]), int(r[iss]), num(r[iwf]), num(r[iwx]))
+    for i in range(5):
         agg[key][i] += v[i]; tot[i] += v[i]
-print(f"kernel {kname[:70]}  warp-instr {tot[0]:,}  thread-instr {tot[1]:,}")
+print(f"kernel {kname[:70]}  warp-instr {tot[0]:,}  thread-instr {tot[1]:,}  smem wavefronts {tot[3]:,} (excessive {tot[4]:,})")
 srcs = {}
 for (f, l), v in sorted(agg.items(), key=lambda x: -x[1][0])[:top]:
     if f not in srcs:
         p = os.path.join(ROOT, "paper_2505_22938_b200", "csrc", f)
         srcs[f] = open(p).read().splitlines() if os.path.exists(p) else []
     text = srcs[f][l - 1].strip()[:60] if 0 < l <= len(srcs[f]) else ""
-    print(f"{f:>16}:{l:<4} warp%={100*v[0]/tot[0]:5.1f} eff={v[1]/max(v[0],1):5.1f} samp%={100*v[2]/max(tot[2],1):5.1f}  {text}")
+    print(f"{f:>16}:{l:<4} warp%={100*v[0]/tot[0]:5.1f} eff={v[1]/max(v[0],1):5.1f} samp%={100*v[2]/max(tot[2],1):5.1f} "
+          f"smem-excess%={100*v[4]/max(tot[4],1):5.1f}  {text}")
