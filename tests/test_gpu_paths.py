@@ -142,3 +142,23 @@ def test_f32_sentinel_key_collision(fp, monkeypatch):
         got = filter_image(img, params)
         want = oracle.fast_filter(img, params.shape, 0.5, "replicate")
         assert got.tobytes() == want.tobytes(), r
+
+
+@pytest.mark.parametrize("fp", ["1", "2"])
+def test_f32_batch_footprint_runs(fp, monkeypatch):
+    """A batch of f32 images (tile index crosses images) through the bucket K1
+    with the footprint and clipped corner runs: every image equals the oracle."""
+    import torch
+
+    from paper_2505_22938_b200 import FilterParams, ShapeSpec, filter_batch
+    monkeypatch.setenv("IMF_F32_FOOTPRINT", fp)
+    monkeypatch.setenv("IMF_RUNMIN", "64")  # edge copy groups as runs too
+    rng = np.random.default_rng(11)
+    imgs = rng.standard_normal((3, 170, 190)).astype(np.float32)
+    imgs[1, :40, :50] = 1.5  # a flat corner: a long tie run and a large bucket
+    for r in (20, 36, 70):
+        params = FilterParams(shape=ShapeSpec("circle", r), percentile=0.4)
+        out = filter_batch(torch.from_numpy(imgs).cuda(), params).cpu().numpy()
+        for b in range(3):
+            want = oracle.fast_filter(imgs[b], params.shape, 0.4, "replicate")
+            assert out[b].tobytes() == want.tobytes(), (r, b)
