@@ -263,7 +263,13 @@ def workspace_for(device, stream=None):
     return _WS.get(device, 1, stream)
 
 
+_KSTRUCT = {}  # id(kernel) -> (kernel, imf_kernel, arrays it points into); kernels are immutable
+
+
 def _kernel_struct(kernel):
+    hit = _KSTRUCT.get(id(kernel))
+    if hit is not None and hit[0] is kernel:
+        return hit[1], hit[2]
     keep = [np.ascontiguousarray(a, dtype=np.int32) for a in
             (kernel.row_dy, kernel.row_xlo, kernel.row_xhi, kernel.col_dx,
              kernel.col_ytop, kernel.col_ybot)]
@@ -271,6 +277,9 @@ def _kernel_struct(kernel):
                         keep[0].ctypes.data, keep[1].ctypes.data, keep[2].ctypes.data,
                         len(kernel.col_dx), keep[3].ctypes.data, keep[4].ctypes.data,
                         keep[5].ctypes.data)
+    if len(_KSTRUCT) > 256:
+        _KSTRUCT.clear()
+    _KSTRUCT[id(kernel)] = (kernel, ks, keep)
     return ks, keep
 
 
