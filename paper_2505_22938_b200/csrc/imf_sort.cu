@@ -748,10 +748,6 @@ __device__ __forceinline__ void f32_bucket_tile(const Geom& g, const TileCoord& 
         rep_axis(Y0, wid + 32 * j, SH, g.H, cy, fy);
         return pixel_weight(g, fpr, lane + 32 * k, cx, fx, wid + 32 * j, cy, fy);
     };
-    auto okf = [&](int j, int k) -> bool {
-        if (EDGE) return (okm >> (j * NK + k)) & 1ull;
-        return v[j][k] != kSent;
-    };
     auto cnt_x = [&](int k) {
         int c;
         bool f;
@@ -790,6 +786,10 @@ __device__ __forceinline__ void f32_bucket_tile(const Geom& g, const TileCoord& 
             }
         }
     }
+    auto okf = [&](int j, int k) -> bool {
+        if (EDGE) return (okm >> (j * NK + k)) & 1ull;
+        return v[j][k] != kSent;
+    };
     {
         uint4* h4 = reinterpret_cast<uint4*>(hw);
         for (int i = tid; i < NW / 4; i += blockDim.x) h4[i] = make_uint4(0, 0, 0, 0);
