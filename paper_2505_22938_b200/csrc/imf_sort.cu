@@ -144,7 +144,8 @@ __device__ void k1_sort_tile(const Geom& g, uint16_t* __restrict__ omega_out, un
     if (g.fprow) {
         for (int y = threadIdx.x; y < 256; y += blockDim.x) {
             const uint32_t v = y < g.Sh ? __ldg(g.fprow + y) : 0xffffffffu;
-            s_fpre[y] = (uint32_t)max(0, (int)(v >> 16) - (int)(v & 0xffffu) + 1);
+            const int lo = (int)(v & 0xffffu), hi = (int)(v >> 16);
+            s_fpre[y] = lo > 255 ? 0u : (uint32_t)(hi - lo + 1);  // empty row: lo = hi = 0xffff
         }
         __syncthreads();
         block_exclusive_scan(s_fpre, 256);

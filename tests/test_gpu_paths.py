@@ -64,6 +64,7 @@ CASES = [  # (dtype, shape, kernel spec)
     ("uint8", (230, 210, 2), ("circle", 75, 0, 0.0)),     # wide pair K2 (T + r > 128), u8
     ("uint8", (190, 170, 2), ("regular_polygon", 11, 6, 15.0)),
     ("float32", (200, 190), ("regular_polygon", 30, 7, 12.0)),  # f32 polygon footprint
+    ("float32", (60, 242), ("regular_polygon", 34, 3, 29.3)),   # empty footprint rows (triangle)
     ("uint8", (120, 130), ("square", 7, 0, 0.0)),
     ("float32", (70, 90), ("circle", 2, 0, 0.0)),         # direct selection (area <= 32)
     ("uint16", (65, 77, 3), ("square", 2, 0, 0.0)),
