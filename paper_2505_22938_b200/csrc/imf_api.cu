@@ -1161,12 +1161,8 @@ int imf_filter_host(const imf_image* src, imf_image* dst, const imf_kernel* kern
     const size_t dbA = ring ? (size_t)nslot * dst->stride_b * dsz : db;
     if (cudaMallocAsync(&dsrc, sbA, s) || cudaMallocAsync(&ddst, dbA, s) || (tb && cudaMallocAsync(&dtm, tb, s)))
         rc = cuda_fail(cudaGetLastError(), "cudaMallocAsync");
-    for (int i = 0; i < nl && !rc; i++)
-        if (cudaMallocAsync(&dws[i], p.ws_total, s)) rc = cuda_fail(cudaGetLastError(), "cudaMallocAsync");
     if (!rc && tb && cudaMemcpyAsync(dtm, target_map, tb, cudaMemcpyHostToDevice, s))
         rc = cuda_fail(cudaGetLastError(), "target map upload");
-    cudaEvent_t e_alloc = event();
-    if (!rc) cudaEventRecord(e_alloc, s);
     imf_image ds = *src, dd = *dst;
     ds.data = dsrc;
     dd.data = ddst;
@@ -1208,6 +1204,30 @@ int imf_filter_host(const imf_image* src, imf_image* dst, const imf_kernel* kern
     } else {
         cuts.push_back(OH);
     }
+    // Workspace per compute lane: the largest any stripe's launch plan needs (a
+    // one-image stripe plans fewer tiles than the whole call -- one chunk lane,
+    // whose single chunk can exceed the call's two-lane chunks); plans depend
+    // on the stripe height only, so each distinct height is planned once.
+    size_t ws_need = p.ws_total;
+    if (pipe) {
+        imf_image one = *src;
+        one.batch = 1;
+        std::vector<int> seen;
+        for (size_t si = 0; si + 1 < cuts.size(); si++) {
+            const int hgt = cuts[si + 1] - cuts[si];
+            if (std::find(seen.begin(), seen.end(), hgt) != seen.end()) continue;
+            seen.push_back(hgt);
+            imf_options o = *opt;
+            o.row_begin = cuts[si];
+            o.row_end = cuts[si + 1];
+            Plan q;
+            if (make_plan(&one, kernel, &o, &q) == IMF_OK) ws_need = std::max(ws_need, q.ws_total);
+        }
+    }
+    for (int i = 0; i < nl && !rc; i++)
+        if (cudaMallocAsync(&dws[i], ws_need, s)) rc = cuda_fail(cudaGetLastError(), "cudaMallocAsync");
+    cudaEvent_t e_alloc = event();
+    if (!rc) cudaEventRecord(e_alloc, s);
     int nstripe = 0;
     if (!rc) {
         cudaStreamWaitEvent(g_hs.up, e_alloc, 0);
@@ -1262,7 +1282,7 @@ int imf_filter_host(const imf_image* src, imf_image* dst, const imf_kernel* kern
                 }
                 if (!rc)
                     rc = imf_filter(&dsi, &ddi, kernel, target, (const int32_t*)dtm, tmin, tmax, &o, wsl,
-                                    p.ws_total, cs);
+                                    ws_need, cs);
                 mark("filtered", nstripe - 1, cs);
                 cudaEvent_t e_done = event();
                 cudaEventRecord(e_done, cs);
