@@ -179,7 +179,7 @@ int imf_tile_omega(const imf_image* src, const imf_kernel* kernel, const imf_opt
  * direct, 1 general, 2 pair); footprint used; K1 tile loads by TMA (when the
  * data pointer is 16-byte aligned); halved ranks; seed rows; workspace bytes;
  * ordinal-transform family (0 radix, 1 f32 buckets, 2 f32 buckets with global
- * entries, 3 counting sort).
+ * entries, 3 counting sort, 4 counting sort with omega in global memory).
  */
 int imf_plan_info(const imf_image* src, const imf_kernel* kernel, const imf_options* opt, int64_t* info);
 

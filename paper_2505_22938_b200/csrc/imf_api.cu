@@ -1002,7 +1002,8 @@ int imf_plan_info(const imf_image* src, const imf_kernel* kernel, const imf_opti
     const Geom& g = p.g;
     const int64_t v[16] = {g.Tw, g.Th, g.Sw, g.Sh, g.N, g.Npad, p.total_tiles, p.chunk_tiles, p.lanes,
                            p.direct ? 0 : (p.pair ? 2 : 1), g.fp, p.k1_tma ? 1 : 0, p.hs, p.G,
-                           (int64_t)p.ws_total, p.k1_f32b ? (p.k1_f32b_g ? 2 : 1) : (p.k1_count ? 3 : 0)};
+                           (int64_t)p.ws_total,
+                           p.k1_f32b ? (p.k1_f32b_g ? 2 : 1) : p.k1_count ? 3 : p.k1_count_g ? 4 : 0};
     memcpy(info, v, sizeof(v));
     return IMF_OK;
 }

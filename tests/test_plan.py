@@ -82,6 +82,11 @@ def test_f32_bucket_plans_rank_the_footprint(r, monkeypatch):
     assert p["N"] == brute_footprint(k, p["Tw"], p["Th"], p["Sw"], p["Sh"], r) < p["Sw"] * p["Sh"]
 
 
+def test_large_u16_tiles_use_the_global_counting_sort():
+    p, _ = plan((1024, 1024, 1), ShapeSpec("circle", 100))
+    assert p["k1"] == 4 and p["Sw"] > 192
+
+
 def test_direct_selection_for_tiny_windows():
     p, _ = plan((512, 512, 1), ShapeSpec("circle", 2), dtype=2)
     assert p["k2"] == 0
