@@ -1080,6 +1080,7 @@ constexpr int kMaxStripeLanes = 4;
 struct HostStreams {
     cudaStream_t up = nullptr, down = nullptr;
     cudaStream_t comp[kMaxStripeLanes] = {};  // comp[0] unused: lane 0 is the caller's stream
+    int* status_h = nullptr;                  // pinned: the lanes' status words, read once per call
 };
 thread_local HostStreams g_hs_dev[kMaxDev];  // per (thread, device), created once
 }  // namespace
@@ -1112,7 +1113,8 @@ int imf_filter_host(const imf_image* src, imf_image* dst, const imf_kernel* kern
             cudaStreamCreateWithFlags(&g_hs.down, cudaStreamNonBlocking) ||
             cudaStreamCreateWithFlags(&g_hs.comp[1], cudaStreamNonBlocking) ||
             cudaStreamCreateWithFlags(&g_hs.comp[2], cudaStreamNonBlocking) ||
-            cudaStreamCreateWithFlags(&g_hs.comp[3], cudaStreamNonBlocking))
+            cudaStreamCreateWithFlags(&g_hs.comp[3], cudaStreamNonBlocking) ||
+            cudaMallocHost(&g_hs.status_h, kMaxStripeLanes * sizeof(int)))
             return cuda_fail(cudaGetLastError(), "stream create");
         // keep freed pool memory cached across calls (default threshold 0 returns
         // it to the driver at every synchronization)
@@ -1319,13 +1321,25 @@ int imf_filter_host(const imf_image* src, imf_image* dst, const imf_kernel* kern
         cudaEventRecord(e_c, g_hs.comp[i]);
         cudaStreamWaitEvent(s, e_c, 0);
     }
-    for (int i = 0; i < std::min(nl, std::max(nstripe, 1)) && !rc; i++) rc = imf_workspace_status(dws[i], stream);  // synchronizes s
+    // every lane's status word in one pinned read; one synchronization for the call
+    const int nst = rc ? 0 : std::min(nl, std::max(nstripe, 1));
+    for (int i = 0; i < nst; i++) {
+        g_hs.status_h[i] = 0;
+        if (cudaError_t e = cudaMemcpyAsync(g_hs.status_h + i, dws[i], sizeof(int), cudaMemcpyDeviceToHost, s)) {
+            rc = cuda_fail(e, "status read");
+            break;
+        }
+    }
     if (dsrc) cudaFreeAsync(dsrc, s);
     if (ddst) cudaFreeAsync(ddst, s);
     for (int i = 0; i < nl; i++)
         if (dws[i]) cudaFreeAsync(dws[i], s);
     if (dtm) cudaFreeAsync(dtm, s);
-    cudaStreamSynchronize(s);
+    if (cudaError_t e = cudaStreamSynchronize(s)) {
+        if (!rc) rc = cuda_fail(e, "stream synchronize");
+    }
+    for (int i = 0; i < nst && !rc; i++)
+        if (g_hs.status_h[i]) rc = IMF_ERR_DEFECT;
     if (trace && !tl.empty()) {
         for (auto& kv : tl) {
             float ms = 0.f;
