@@ -1207,6 +1207,24 @@ int imf_filter_host(const imf_image* src, imf_image* dst, const imf_kernel* kern
     } else {
         cuts.push_back(OH);
     }
+    // The first stripe's input rows go up before the workspace is planned and
+    // allocated below (host work that would otherwise delay the first copy).
+    int pre_up_hi = -1;  // image 0: input rows [.., pre_up_hi) already uploaded
+    if (!rc && pipe) {
+        cudaEvent_t e_io = event();
+        cudaEventRecord(e_io, s);
+        cudaStreamWaitEvent(g_hs.up, e_io, 0);
+        const int lo = std::max(0, std::min(H, R0 + vshift - r));
+        const int need = std::min(H, cuts[1] - 1 + r + vshift + 1);
+        if (need > lo) {
+            const size_t off = (size_t)((long long)lo * src->stride_y) * dsz;
+            const size_t len = (size_t)((long long)(need - lo) * src->stride_y) * dsz;
+            if (cudaMemcpyAsync((char*)dsrc + off, (const char*)src->data + off,
+                                std::min(len, std::min(sb - off, sbA - off)), cudaMemcpyHostToDevice, g_hs.up))
+                rc = cuda_fail(cudaGetLastError(), "stripe upload");
+            pre_up_hi = need;
+        }
+    }
     // Workspace per compute lane: the largest any stripe's launch plan needs (a
     // one-image stripe plans fewer tiles than the whole call -- one chunk lane,
     // whose single chunk can exceed the call's two-lane chunks); plans depend
@@ -1243,7 +1261,7 @@ int imf_filter_host(const imf_image* src, imf_image* dst, const imf_kernel* kern
             const long long sdev = (long long)slot * src->stride_b, ddev = (long long)slot * dst->stride_b;
             if (ring && slot_free[slot]) cudaStreamWaitEvent(g_hs.up, slot_free[slot], 0);
             // input rows [first row the stripe reads, up_hi) of image bi are uploaded
-            int up_hi = std::max(0, std::min(H, R0 + vshift - r));
+            int up_hi = (bi == 0 && pre_up_hi >= 0) ? pre_up_hi : std::max(0, std::min(H, R0 + vshift - r));
             for (size_t si = 0; si + 1 < cuts.size() && !rc; si++) {
                 const int y0 = cuts[si], y1 = cuts[si + 1];
                 if (pipe) {
