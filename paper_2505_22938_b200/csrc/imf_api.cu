@@ -1081,6 +1081,7 @@ struct HostStreams {
     cudaStream_t up = nullptr, down = nullptr;
     cudaStream_t comp[kMaxStripeLanes] = {};  // comp[0] unused: lane 0 is the caller's stream
     int* status_h = nullptr;                  // pinned: the lanes' status words, read once per call
+    std::vector<cudaEvent_t> events;          // reused across calls (timing disabled)
 };
 thread_local HostStreams g_hs_dev[kMaxDev];  // per (thread, device), created once
 }  // namespace
@@ -1130,11 +1131,21 @@ int imf_filter_host(const imf_image* src, imf_image* dst, const imf_kernel* kern
     // IMF_HOST_TRACE=1: timed events, and a per-stripe timeline on stderr (dev aid)
     const bool trace = env_int("IMF_HOST_TRACE", 0) != 0;
     std::vector<std::pair<std::string, cudaEvent_t>> tl;
+    // events: from the per-(thread, device) pool (recycled: every use below is
+    // complete once the call returns), or created with timing for a trace
+    size_t ev_used = 0;
     auto event = [&]() {
         cudaEvent_t e = nullptr;
-        cudaEventCreateWithFlags(&e, trace ? cudaEventDefault : cudaEventDisableTiming);
-        evs.push_back(e);
-        return e;
+        if (trace) {
+            cudaEventCreateWithFlags(&e, cudaEventDefault);
+            evs.push_back(e);
+            return e;
+        }
+        if (ev_used == g_hs.events.size()) {
+            cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+            g_hs.events.push_back(e);
+        }
+        return g_hs.events[ev_used++];
     };
     auto mark = [&](const char* what, int i, cudaStream_t st) {
         if (!trace) return;
