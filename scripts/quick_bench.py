@@ -5,6 +5,7 @@
 import ctypes, json, os, sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT); sys.path.insert(0, os.path.join(ROOT, "tests", "golden"))
+sys.path.insert(0, os.path.join(ROOT, "tests"))
 import numpy as np, torch
 import cases as C
 from paper_2505_22938_b200 import FilterParams, ShapeSpec, _lib, make_kernel
@@ -62,6 +63,11 @@ if "c3" in which:
 if "c4" in which:
     img = C.baseline_input("c4")
     for s in C.C4_SHAPES: run(f"c4 {s[0]}{s[2]}", img, s, reps=3, gold=gold["c4/" + json.dumps(list(s))])
+if "c2smooth" in which:  # SURVEY 8(d) refine-stress distribution at the c2 shape (parity vs the C oracle)
+    import oracle
+    img = C.smooth_image((2160, 3840, 3), np.uint16, 2)
+    want = oracle.fast_filter(img, ShapeSpec("circle", 48), 0.5)
+    run("c2smooth", img, ("circle", 48, 0, 0.0), gold=C.digest(want))
 if "c5" in which:
     g5 = json.load(open(os.path.join(ROOT, "tests", "golden", "golden_c5.json")))
     run("c5 img0", C.baseline_input("c5", 0), ("circle", 64, 0, 0.0), reps=3, gold=g5.get("0"))

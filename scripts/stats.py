@@ -9,7 +9,7 @@ import numpy as np, torch
 import cases as C
 from paper_2505_22938_b200 import FilterParams, ShapeSpec, _lib
 from paper_2505_22938_b200.tiling import run_device
-img = C.baseline_input("c2")
+img = C.smooth_image((2160, 3840, 3), np.uint16, 2) if os.environ.get("STATS_IMG") == "smooth" else C.baseline_input("c2")
 if len(sys.argv) > 1:
     n = int(sys.argv[1]); img = img[:n, :n]
 t = torch.from_numpy(np.ascontiguousarray(img)).cuda().unsqueeze(0)
