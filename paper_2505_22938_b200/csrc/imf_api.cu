@@ -36,7 +36,13 @@ static int cuda_fail(cudaError_t e, const char* where) {
 
 namespace {
 
-constexpr size_t kSmemMax = 227 * 1024 - 1024;  // B200 opt-in 232448 B minus static smem headroom
+constexpr size_t kOptinSmem = 227 * 1024;       // B200 opt-in shared memory per block (232448 B)
+constexpr size_t kSmemMax = kOptinSmem - 1024;  // dynamic budget of kernels with <= 1 KB static smem
+// Static shared memory each K1 family declares (the kernel's own __shared__
+// variables; cuobjdump's SHARED also counts the 1 KB system reserve), rounded
+// up: a launch needs dynamic + static <= kOptinSmem.  tests/test_plan.py checks
+// the built kernels stay within these.
+constexpr size_t kStaticK1Sort = 2048, kStaticK1Bucket = 4096;
 constexpr int kK1Threads = 1024;      // k1_count (latency-bound: more warps)
 constexpr int kK1SortThreads = 512;   // k1_sort (per-warp digit counters)
 constexpr size_t kStatusBytes = 2048;    // status word at 0, footprint row table at kFpOffset
@@ -239,12 +245,12 @@ int make_plan(const imf_image* src, const imf_kernel* k, const imf_options* opt,
     // K1 variant and its memory for the ranked pixels per tile g.N (chosen
     // again once a footprint shrinks N)
     auto choose_k1 = [&]() {
-        // k1_sort holds 1 KB of static shared memory for footprint tiles
         p.k1_f32b_g = false;
-        const size_t k1s_max = kSmemMax - (g.fp ? 1024 : 0);
+        const size_t k1s_max = kOptinSmem - kStaticK1Sort;
         p.k1_count = g.dtype != DT_F32 && k1_count_smem_bytes(g.dtype, g.Npad) <= kSmemMax;
         p.k1b_smem = k1_f32_bucket_smem_bytes(g.N);
-        p.k1_f32b = g.dtype == DT_F32 && env_int("IMF_F32_BUCKET", 1) && g.Sw <= 160 && p.k1b_smem <= kSmemMax;
+        p.k1_f32b = g.dtype == DT_F32 && env_int("IMF_F32_BUCKET", 1) && g.Sw <= 160 &&
+                    p.k1b_smem <= kOptinSmem - kStaticK1Bucket;
         // f32 tiles beyond shared-memory entries, and u16 tiles beyond the 64K-bin
         // counting sort (S > ~180): the bucket transform with global entries
         // (u16 keys v << 16: every bucket is one value, ties only)
@@ -285,9 +291,12 @@ int make_plan(const imf_image* src, const imf_kernel* k, const imf_options* opt,
     // -7 %), not on the 16-bit-entry kernel in between (161..192, r=64: its
     // register spills cost K1 more than the 10 % fewer pixels save; path
     // +13 %).  IMF_F32_FOOTPRINT: 0 never, 1 auto, 2 always.
+    // (decided on the tile size, not on the whole-tile K1 choice above: the
+    // footprint can bring a tile back under the shared-entry kernel's limit)
     const int f32fp = env_int("IMF_F32_FOOTPRINT", 1);
-    const bool own16 = p.k1_f32b_g && ((g.Sw + 31) >> 5) <= 6;
-    const bool fp_k1 = k1reg || (g.dtype == DT_F32 && p.k1_f32b && (f32fp == 2 || (f32fp == 1 && !own16)));
+    const bool own16 = g.Sw > 160 && ((g.Sw + 31) >> 5) <= 6;
+    const bool fp_k1 = k1reg || (g.dtype == DT_F32 && env_int("IMF_F32_BUCKET", 1) &&
+                                 (f32fp == 2 || (f32fp == 1 && !own16)));
     if (p.pair && k->shape_code != IMF_SHAPE_SQUARE && fp_k1 && g.Sh <= 256 && env_int("IMF_FOOTPRINT", 1)) {
         // the table depends on the kernel's row spans and the tile geometry only:
         // memoized per thread (the host pipeline plans every stripe of a frame)

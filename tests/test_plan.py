@@ -90,3 +90,27 @@ def test_large_u16_tiles_use_the_global_counting_sort():
 def test_direct_selection_for_tiny_windows():
     p, _ = plan((512, 512, 1), ShapeSpec("circle", 2), dtype=2)
     assert p["k2"] == 0
+
+
+def test_kernel_static_shared_memory_within_the_planner_reservations():
+    """The planner sizes dynamic shared memory as opt-in minus a per-family
+    static reservation (imf_api.cu kStaticK1*): every built kernel's own static
+    shared memory (cuobjdump SHARED minus the 1 KB system reserve) must fit."""
+    import os
+    import re
+    import shutil
+    import subprocess
+    cuobjdump = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(cuobjdump):
+        pytest.skip("cuobjdump not available")
+    out = subprocess.run([cuobjdump, "-res-usage", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    limits = {"k1_sort": 2048, "k1_f32_bucket": 4096, "k1_count": 1024, "k2_": 1024, "k_direct": 1024,
+              "k2_select": 1024}
+    seen = 0
+    for name, shared in re.findall(r"Function (\S+):\s*\n\s*REG:\d+ STACK:\d+ SHARED:(\d+)", out):
+        for prefix, lim in limits.items():
+            if re.search(r"\d" + prefix, name):
+                seen += 1
+                assert int(shared) - 1024 <= lim, (name, shared, lim)
+                break
+    assert seen > 50
