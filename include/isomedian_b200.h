@@ -132,7 +132,9 @@ int imf_workspace_status(void* workspace, void* stream);
  * stripe i and the download of stripe i-1 run concurrently (three streams,
  * event-ordered); batches of more than two such images reuse two device
  * image slots (image b in slot b % 2).  Device buffers come from the
- * stream-ordered pool (cudaMallocAsync).  Host buffers should be pinned for
+ * stream-ordered pool (cudaMallocAsync); the streams, events and pinned
+ * status words it uses are kept per (calling thread, device) and released
+ * when the thread exits.  Host buffers should be pinned for
  * full copy bandwidth.  dst must be dense (every byte of its extent belongs
  * to an element, e.g. C-contiguous: row ranges are copied back as whole byte
  * ranges), else IMF_ERR_INVALID.  opt->row_begin/row_end select an output

@@ -867,14 +867,22 @@ static int filter_impl(const imf_image* src, imf_image* dsts, int n, const int32
     cudaStream_t ls[2] = {s, nullptr};
     cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
     if (lanes == 2) {
-        // one lane-2 stream per (thread, device), created once and kept
-        static thread_local cudaStream_t lane2[kMaxDev] = {};
+        // one lane-2 stream per (thread, device), created once, destroyed when
+        // the thread exits
+        struct Lane2 {
+            cudaStream_t s[kMaxDev] = {};
+            ~Lane2() {
+                for (int d = 0; d < kMaxDev; d++)
+                    if (s[d] && cudaSetDevice(d) == cudaSuccess) cudaStreamDestroy(s[d]);
+            }
+        };
+        static thread_local Lane2 lane2;
         int dev = 0;
         if (cudaError_t e = cudaGetDevice(&dev)) return cuda_fail(e, "cudaGetDevice");
-        if (!lane2[dev])
-            if (cudaError_t e = cudaStreamCreateWithFlags(&lane2[dev], cudaStreamNonBlocking))
+        if (!lane2.s[dev])
+            if (cudaError_t e = cudaStreamCreateWithFlags(&lane2.s[dev], cudaStreamNonBlocking))
                 return cuda_fail(e, "lane stream");
-        ls[1] = lane2[dev];
+        ls[1] = lane2.s[dev];
         cudaEventCreateWithFlags(&fork_ev, cudaEventDisableTiming);
         cudaEventCreateWithFlags(&join_ev, cudaEventDisableTiming);
         cudaEventRecord(fork_ev, s);  // after the status memset
@@ -1091,8 +1099,24 @@ struct HostStreams {
     cudaStream_t comp[kMaxStripeLanes] = {};  // comp[0] unused: lane 0 is the caller's stream
     int* status_h = nullptr;                  // pinned: the lanes' status words, read once per call
     std::vector<cudaEvent_t> events;          // reused across calls (timing disabled)
+    void release() {  // the thread's resources on the current device
+        for (cudaStream_t* p : {&up, &down, &comp[1], &comp[2], &comp[3]})
+            if (*p) cudaStreamDestroy(*p), *p = nullptr;
+        for (cudaEvent_t e : events) cudaEventDestroy(e);
+        events.clear();
+        if (status_h) cudaFreeHost(status_h), status_h = nullptr;
+    }
 };
-thread_local HostStreams g_hs_dev[kMaxDev];  // per (thread, device), created once
+// per (thread, device), created on first use; released when the thread exits
+// (threads that come and go, e.g. one per filter_multi call, leak nothing)
+struct HostStreamSet {
+    HostStreams dev[kMaxDev];
+    ~HostStreamSet() {
+        for (int d = 0; d < kMaxDev; d++)
+            if (dev[d].up && cudaSetDevice(d) == cudaSuccess) dev[d].release();
+    }
+};
+thread_local HostStreamSet g_hs_set;
 }  // namespace
 
 int imf_filter_host(const imf_image* src, imf_image* dst, const imf_kernel* kernel, int32_t target,
@@ -1117,7 +1141,7 @@ int imf_filter_host(const imf_image* src, imf_image* dst, const imf_kernel* kern
     int dev = 0;
     if (cudaGetDevice(&dev)) return IMF_ERR_CUDA;
     if (dev >= kMaxDev) return IMF_ERR_INVALID;
-    HostStreams& g_hs = g_hs_dev[dev];
+    HostStreams& g_hs = g_hs_set.dev[dev];
     if (!g_hs.up) {
         if (cudaStreamCreateWithFlags(&g_hs.up, cudaStreamNonBlocking) ||
             cudaStreamCreateWithFlags(&g_hs.down, cudaStreamNonBlocking) ||
