@@ -19,6 +19,7 @@ GPU the call raises.
 
 from __future__ import annotations
 
+import collections
 import ctypes
 import threading
 from dataclasses import dataclass
@@ -235,8 +236,10 @@ class _Workspace:
     by) its own stream, so the caching allocator's stream tracking is exact.
     """
 
+    MAX_ENTRIES = 8  # least recently used (device, stream) workspaces beyond this are dropped
+
     def __init__(self):
-        self.buf = {}
+        self.buf = collections.OrderedDict()
         self.lock = threading.Lock()
 
     def get(self, device, nbytes: int, stream=None):
@@ -251,6 +254,12 @@ class _Workspace:
                 with torch.cuda.stream(stream):
                     cur = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=torch.device("cuda", idx))
                 self.buf[key] = cur
+            self.buf.move_to_end(key)
+            # callers that make a stream per call must not pin a workspace per
+            # stream: a dropped buffer was only ever used on its own stream, so
+            # the caching allocator reuses it there in stream order
+            while len(self.buf) > self.MAX_ENTRIES:
+                self.buf.popitem(last=False)
             return cur
 
 

@@ -185,3 +185,21 @@ def test_filter_batch_multi_device_resident(boundary):
     got = filter_batch_multi(imgs, params, devices=[0, 0])
     want = filter_batch(imgs, params)
     assert torch.equal(got, want)
+
+
+def test_workspace_cache_is_bounded_under_stream_churn():
+    """A new stream per call must not pin a workspace per stream."""
+    import torch
+
+    from paper_2505_22938_b200 import FilterParams, ShapeSpec, filter_image
+    from paper_2505_22938_b200.tiling import _WS
+    img = torch.from_numpy(np.random.default_rng(4).integers(0, 256, (200, 180), dtype=np.uint8)).cuda()
+    params = FilterParams(shape=ShapeSpec("circle", 9))
+    want = oracle.fast_filter(img.cpu().numpy(), params.shape, 0.5)
+    for _ in range(20):
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            out = filter_image(img, params)
+        s.synchronize()
+        assert out.cpu().numpy().tobytes() == want.tobytes()
+    assert len(_WS.buf) <= _WS.MAX_ENTRIES
