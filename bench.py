@@ -363,6 +363,12 @@ def run_ours(args):
     from paper_2505_22938_b200.tiling import run_device, workspace_for
 
     rank, world, local = dist_env()
+    if local >= torch.cuda.device_count():
+        # one rank per GPU: asking for more ranks than visible GPUs is a launch error
+        if rank == 0 or local == 0:
+            print(json.dumps({"error": f"rank {rank} needs GPU {local}, only "
+                                       f"{torch.cuda.device_count()} visible"}), flush=True)
+        raise SystemExit(2)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
