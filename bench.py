@@ -364,10 +364,10 @@ def run_ours(args):
 
     rank, world, local = dist_env()
     if local >= torch.cuda.device_count():
-        # one rank per GPU: asking for more ranks than visible GPUs is a launch error
-        if rank == 0 or local == 0:
-            print(json.dumps({"error": f"rank {rank} needs GPU {local}, only "
-                                       f"{torch.cuda.device_count()} visible"}), flush=True)
+        # one rank per GPU: more ranks than visible GPUs is a launch error (torchrun
+        # then stops the other ranks)
+        print(f"bench.py: rank {rank} needs GPU {local}, only {torch.cuda.device_count()} visible",
+              file=sys.stderr, flush=True)
         raise SystemExit(2)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
