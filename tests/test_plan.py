@@ -114,3 +114,29 @@ def test_kernel_static_shared_memory_within_the_planner_reservations():
                 assert int(shared) - 1024 <= lim, (name, shared, lim)
                 break
     assert seen > 50
+
+
+def test_random_plans_are_consistent():
+    """Seeded random geometries: the plan's tile counts, padding, footprint and
+    workspace agree with each other and with imf_workspace_size."""
+    import numpy as np
+    rng = np.random.default_rng(123)
+    L = _lib.load()
+    for _ in range(150):
+        dt = int(rng.integers(0, 3))
+        kind = str(rng.choice(["circle", "square", "regular_polygon"]))
+        r = int(rng.integers(0, 125))
+        spec = ShapeSpec(kind, r, sides=int(rng.integers(3, 13)), rotation_deg=float(rng.uniform(0, 360))) \
+            if kind == "regular_polygon" else ShapeSpec(kind, r)
+        h, w, c = int(rng.integers(1, 3000)), int(rng.integers(1, 3000)), int(rng.choice([1, 3]))
+        p, k = plan((h, w, c), spec, dtype=dt)
+        assert p["N"] <= p["Sw"] * p["Sh"] and p["Npad"] == (p["N"] + 63) // 64 * 64
+        assert p["Sw"] <= 255 and p["Sh"] <= 255 and p["Sw"] - p["Tw"] == 2 * r
+        tiles = -(-h // p["Th"]) * -(-w // p["Tw"]) * c
+        assert p["tiles"] == tiles and 1 <= p["chunk"] <= tiles
+        if p["fp"]:
+            assert p["N"] == brute_footprint(k, p["Tw"], p["Th"], p["Sw"], p["Sh"], r)
+        ks, keep = _kernel_struct(k)
+        img = _lib.ImfImage(0x1000, dt, 1, h, w, c, 0, w * c, c, 1)
+        opt = _lib.ImfOptions(0, 0, 0, 0)
+        assert L.imf_workspace_size(ctypes.byref(img), ctypes.byref(ks), ctypes.byref(opt)) == p["ws"]
