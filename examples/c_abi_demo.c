@@ -10,6 +10,9 @@
  *       -Wl,-rpath,$PWD/paper_2505_22938_b200 -o /tmp/c_abi_demo
  *   /tmp/c_abi_demo            # filter on cuda:0 and check
  *   /tmp/c_abi_demo --plan     # host-only: plan and workspace size (no GPU needed)
+ *   /tmp/c_abi_demo --device   # device pointers: imf_filter on a stream with a caller-owned
+ *                              # workspace (build with -DWITH_CUDART -I/usr/local/cuda/include
+ *                              # -L/usr/local/cuda/lib64 -lcudart)
  */
 #include <math.h>
 #include <stdint.h>
@@ -18,6 +21,9 @@
 #include <string.h>
 
 #include "isomedian_b200.h"
+#ifdef WITH_CUDART
+#include <cuda_runtime.h>
+#endif
 
 enum { R = 6, H = 57, W = 83, C = 3 };
 
@@ -63,9 +69,33 @@ int main(int argc, char** argv) {
                (long long)info[1], (long long)info[4]);
         return st;
     }
-    const int st = imf_filter_host(&is, &os, &k, t, NULL, t, t, &opt, NULL);
+    int st;
+    if (argc > 1 && strcmp(argv[1], "--device") == 0) {
+#ifdef WITH_CUDART
+        /* the asynchronous entry: device buffers, caller-owned workspace, a stream */
+        const size_t bytes = sizeof(uint16_t) * H * W * C, ws_bytes = imf_workspace_size(&is, &k, &opt);
+        void *dsrc, *ddst, *ws;
+        cudaStream_t stream;
+        if (cudaMalloc(&dsrc, bytes) || cudaMalloc(&ddst, bytes) || cudaMalloc(&ws, ws_bytes) ||
+            cudaStreamCreate(&stream))
+            return 2;
+        cudaMemcpyAsync(dsrc, src, bytes, cudaMemcpyHostToDevice, stream);
+        imf_image ds = is, dd = os;
+        ds.data = dsrc;
+        dd.data = ddst;
+        st = imf_filter(&ds, &dd, &k, t, NULL, t, t, &opt, ws, ws_bytes, stream);
+        cudaMemcpyAsync(dst, ddst, bytes, cudaMemcpyDeviceToHost, stream);
+        if (st == IMF_OK) st = imf_workspace_status(ws, stream);  /* synchronizes the stream */
+        cudaFree(dsrc), cudaFree(ddst), cudaFree(ws), cudaStreamDestroy(stream);
+#else
+        fprintf(stderr, "--device needs a -DWITH_CUDART build\n");
+        return 2;
+#endif
+    } else {
+        st = imf_filter_host(&is, &os, &k, t, NULL, t, t, &opt, NULL);
+    }
     if (st != IMF_OK) {
-        fprintf(stderr, "imf_filter_host: %s (%s)\n", imf_strerror(st), imf_last_error());
+        fprintf(stderr, "imf_filter: %s (%s)\n", imf_strerror(st), imf_last_error());
         return 1;
     }
     uint16_t win[(2 * R + 1) * (2 * R + 1)];
