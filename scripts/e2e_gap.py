@@ -1,3 +1,5 @@
+"""Host->host time of c2 split into the Python prologue, the C call and the gap
+between calls (dev aid):  python scripts/e2e_gap.py"""
 import os, sys, time, json, ctypes
 sys.path.insert(0, "/root/repo"); sys.path.insert(0, "/root/repo/tests/golden")
 import numpy as np, torch

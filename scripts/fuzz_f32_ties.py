@@ -1,3 +1,6 @@
+"""Large tie-heavy f32 frames (quantized normals, flat corners, circles and
+polygons r=32..100) against the C oracle, with and without the f32 footprint
+(dev aid):  python scripts/fuzz_f32_ties.py"""
 import sys, numpy as np, time
 sys.path.insert(0, "/root/repo"); sys.path.insert(0, "/root/repo/tests")
 import oracle

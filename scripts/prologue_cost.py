@@ -1,3 +1,5 @@
+"""Cost of run_host's Python prologue with the C call stubbed out, plus a
+cProfile breakdown (dev aid):  python scripts/prologue_cost.py"""
 import sys, time, ctypes
 sys.path.insert(0, "/root/repo"); sys.path.insert(0, "/root/repo/tests/golden")
 import numpy as np, torch

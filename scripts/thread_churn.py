@@ -1,3 +1,6 @@
+"""300 short-lived host threads each filtering through imf_filter_host (and
+filter_multi every 50): per-thread CUDA resources are released at thread
+exit (dev aid):  python scripts/thread_churn.py"""
 import sys, threading, time
 sys.path.insert(0, "/root/repo"); sys.path.insert(0, "/root/repo/tests")
 import numpy as np, torch, oracle
