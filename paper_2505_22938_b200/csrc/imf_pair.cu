@@ -82,6 +82,22 @@ __device__ __forceinline__ void acc_ge4(uint32_t& acc, uint32_t d1, uint32_t d2)
         : "r"(x));
 }
 
+// Four tests into ONE dot product: PRMT in sign-replicate mode gathers the
+// answer bytes of d1 and d2 as [A1, A2, B1, B2] = 0xff (I >= P) or 0x00, and
+// IDP.4A against the unsigned weights [1, 1, 128, 128] accumulates -(A + 128 B)
+// (2 instructions per 4 tests instead of PRMT + LOP3 + LEA.HI).  A run of
+// acc_dp4 calls may count at most 127 A-tests before dp4_unpack.
+__device__ __forceinline__ void acc_dp4(int& acc, uint32_t d1, uint32_t d2) {
+    const uint32_t x = prmt(d1, d2, 0xFBD9);
+    asm("dp4a.s32.u32 %0, %1, %2, %0;" : "+r"(acc) : "r"(x), "r"(0x80800101u));
+}
+
+// -(A + 128 B) with A <= 127 -> packed (A | B << 16).
+__device__ __forceinline__ uint32_t dp4_unpack(int acc) {
+    const uint32_t v = (uint32_t)(-acc);
+    return (v & 127u) | ((v >> 7) << 16);
+}
+
 // Byte-lane counters [A1, A2, B1, B2] -> packed (A | B << 16).
 __device__ __forceinline__ uint32_t unpack4(uint32_t acc) {
     return (acc & 0x00ff00ffu) + ((acc >> 8) & 0x00ff00ffu);
@@ -92,25 +108,32 @@ __device__ __forceinline__ uint32_t unpack4(uint32_t acc) {
 template <int U>  // column-loop unroll (8 for circles: c2 / c5 gain; 4 elsewhere: c4 loses at 8)
 __device__ __forceinline__ void vcount(uint32_t b, const int2* __restrict__ v, int ne, int n, uint32_t K,
                                        uint32_t& ge_in, uint32_t& ge_out) {
-    uint32_t ai = 0, ao = 0, ri = 0, ro = 0;
+    // one entry per kernel column, alternating parity: each of the even
+    // (aligned) and odd lists holds <= 125 columns (build_pair_tab checks
+    // <= 127), so each list is one acc_dp4 run
+    int ai = 0, ao = 0;
+    uint32_t ri = 0, ro = 0;
     int k = 0;
 #pragma unroll U
     for (; k + 1 < ne; k += 2) {
         const int2 o0 = v[k], o1 = v[k + 1];
-        acc_ge4(ai, lds32(b + o0.x) + K, lds32(b + o1.x) + K);
-        acc_ge4(ao, lds32(b + o0.y) + K, lds32(b + o1.y) + K);
+        acc_dp4(ai, lds32(b + o0.x) + K, lds32(b + o1.x) + K);
+        acc_dp4(ao, lds32(b + o0.y) + K, lds32(b + o1.y) + K);
     }
     if (k < ne) {
         const int2 o = v[k];
         acc_ge2(ri, lds32(b + o.x) + K);
         acc_ge2(ro, lds32(b + o.y) + K);
     }
+    ri += dp4_unpack(ai);
+    ro += dp4_unpack(ao);
+    ai = ao = 0;
 #pragma unroll U
     for (k = ne; k + 1 < n; k += 2) {
         const int2 o0 = v[k], o1 = v[k + 1];
-        acc_ge4(ai, prmt(lds32(b + o0.x), lds32(b + o0.x + 4), 0x5432) + K,
+        acc_dp4(ai, prmt(lds32(b + o0.x), lds32(b + o0.x + 4), 0x5432) + K,
                 prmt(lds32(b + o1.x), lds32(b + o1.x + 4), 0x5432) + K);
-        acc_ge4(ao, prmt(lds32(b + o0.y), lds32(b + o0.y + 4), 0x5432) + K,
+        acc_dp4(ao, prmt(lds32(b + o0.y), lds32(b + o0.y + 4), 0x5432) + K,
                 prmt(lds32(b + o1.y), lds32(b + o1.y + 4), 0x5432) + K);
     }
     if (k < n) {
@@ -118,14 +141,31 @@ __device__ __forceinline__ void vcount(uint32_t b, const int2* __restrict__ v, i
         acc_ge2(ri, prmt(lds32(b + o.x), lds32(b + o.x + 4), 0x5432) + K);
         acc_ge2(ro, prmt(lds32(b + o.y), lds32(b + o.y + 4), 0x5432) + K);
     }
-    ge_in = unpack4(ai) + ri;
-    ge_out = unpack4(ao) + ro;
+    ge_in = dp4_unpack(ai) + ri;
+    ge_out = dp4_unpack(ao) + ro;
 }
 
-// Packed count of [I >= P] over one horizontal list.
+// Packed count of [I >= P] over one horizontal list (acc_dp4 runs when both
+// parity lists hold <= 127 rows -- a row's entering column parity follows the
+// kernel's shape, so e.g. a large square puts every row in one list).
 __device__ __forceinline__ uint32_t hcount(uint32_t b, const int* __restrict__ h, int ne, int n, uint32_t K) {
-    uint32_t a = 0, rr = 0;
+    uint32_t rr = 0;
     int k = 0;
+    if (ne <= 127 && n - ne <= 127) {
+        int a = 0;
+#pragma unroll 2
+        for (; k + 1 < ne; k += 2) acc_dp4(a, lds32(b + h[k]) + K, lds32(b + h[k + 1]) + K);
+        if (k < ne) acc_ge2(rr, lds32(b + h[k]) + K);
+        rr += dp4_unpack(a);
+        a = 0;
+#pragma unroll 2
+        for (k = ne; k + 1 < n; k += 2)
+            acc_dp4(a, prmt(lds32(b + h[k]), lds32(b + h[k] + 4), 0x5432) + K,
+                    prmt(lds32(b + h[k + 1]), lds32(b + h[k + 1] + 4), 0x5432) + K);
+        if (k < n) acc_ge2(rr, prmt(lds32(b + h[k]), lds32(b + h[k] + 4), 0x5432) + K);
+        return dp4_unpack(a) + rr;
+    }
+    uint32_t a = 0;
 #pragma unroll 2
     for (; k + 1 < ne; k += 2) acc_ge4(a, lds32(b + h[k]) + K, lds32(b + h[k + 1]) + K);
     if (k < ne) acc_ge2(rr, lds32(b + h[k]) + K);
@@ -999,6 +1039,7 @@ bool build_pair_tab(const int* row_dy, const int* row_xlo, const int* row_xhi, i
         if (pass == 0) p.nv_even = k;
     }
     p.nv = ncols;
+    if (p.nv_even > 127 || ncols - p.nv_even > 127) return false;  // vcount's acc_dp4 runs
     auto fill_h = [&](int* dst, bool hi, int& ne) {
         int kk = 0;
         for (int pass = 0; pass < 2; pass++) {
