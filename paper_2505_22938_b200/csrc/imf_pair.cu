@@ -201,6 +201,7 @@ struct PairCtx {
     int N, r, R2p1;
     uint32_t rowk_a;      // SH_POLY: shared address of the 256-entry per-(dy+128) range table
     int nR2p1;            // -(r(r+1)+1)
+    uint32_t x80;         // 0x80808080 in a register (SH_CIRCLE's LOP3 operand)
 };
 
 __device__ __forceinline__ uint32_t lds32c(uint32_t a) {
@@ -220,11 +221,17 @@ __device__ __forceinline__ uint32_t test8(const PairCtx& c, int v0, uint32_t Kc,
     const uint32_t w[4] = {q.x, q.y, q.z, q.w};
     uint32_t m = 0;
     if (SHAPE == SH_CIRCLE) {
+        // each rank's signed bytes isolated by ONE LOP3 ((a ^ 0x80808080) & mask,
+        // the XOR constant held in a register) and squared against themselves:
+        // 2 LOP3 + 2 IDP.4A per two ranks (b & mask against the full b needs 3 LOP3)
 #pragma unroll
         for (int i = 3; i >= 0; i--) {
-            const int b = (int)((w[i] + Kc) ^ 0x80808080u);
-            const int slo = __dp4a(b, b & 0xffff, c.nR2p1);
-            const int shi = __dp4a(b, (int)((uint32_t)b & 0xffff0000u), c.nR2p1);
+            const uint32_t a = w[i] + Kc;
+            uint32_t blo, bhi;
+            asm("lop3.b32 %0, %1, %2, 0x0000ffff, 0x28;" : "=r"(blo) : "r"(a), "r"(c.x80));
+            asm("lop3.b32 %0, %1, %2, 0xffff0000, 0x28;" : "=r"(bhi) : "r"(a), "r"(c.x80));
+            const int slo = __dp4a((int)blo, (int)blo, c.nR2p1);
+            const int shi = __dp4a((int)bhi, (int)bhi, c.nR2p1);
             m = __funnelshift_l((uint32_t)shi, m, 1);
             m = __funnelshift_l((uint32_t)slo, m, 1);
         }
@@ -678,8 +685,9 @@ __global__ void __launch_bounds__(512, 2) k2_pair(Geom g, PairParams p, const __
     // compiler, which would otherwise rebuild them inside every refine step)
     uint32_t om_a = OMG ? 0u : (uint32_t)__cvta_generic_to_shared(om_sh);
     int nR2p1 = -p.R2p1;
-    asm volatile("" : "+r"(om_a), "+r"(nR2p1));
-    const PairCtx c{om_a, om, span_s, N, r, p.R2p1, (uint32_t)__cvta_generic_to_shared(rowk), nR2p1};
+    uint32_t x80 = 0x80808080u;
+    asm volatile("" : "+r"(om_a), "+r"(nR2p1), "+r"(x80));
+    const PairCtx c{om_a, om, span_s, N, r, p.R2p1, (uint32_t)__cvta_generic_to_shared(rowk), nR2p1, x80};
     const int R = TY / G;
     const int g0 = G >> 1;
     const int cs = (T >> 1) & ~1;  // seed column (even: a pair base)
