@@ -251,20 +251,18 @@ __device__ __forceinline__ uint32_t test8(const PairCtx& c, int v0, uint32_t Kc,
             m = __funnelshift_l((uint32_t)tlo, m, 1);
         }
     } else if (SHAPE == SH_SQUARE) {
-        // bytes (dx+128, dy+128) of two ranks; per rank spread into 16-bit halves,
-        // bit 15 of h + (0x8000 - (128 - r)) is [d >= -r] and of h + (0x8000 - (129 + r))
-        // is [d > r]; inside iff both halves pass: (t >> 15) == 0x10001, whose
-        // sign-bit form is (t >> 15) + 0x7ffeffff
-        const uint32_t KA = (uint32_t)(0x8000 - (128 - c.r)) * 0x10001u;
-        const uint32_t KB = (uint32_t)(0x8000 - (129 + c.r)) * 0x10001u;
+        // bytes (dx+128, dy+128) of two ranks; VABSDIFF4 gives |dx|, |dy| per
+        // byte (<= 127), + (127 - r) per byte sets bit 7 exactly where |d| > r
+        // (no carry leaves a byte); a rank is outside iff either of its bytes
+        // has bit 7: n = ~(z | z << 8) holds membership in bits 15 (low rank)
+        // and 31 (high rank)
+        const uint32_t K127 = (uint32_t)(127 - c.r) * 0x01010101u;
 #pragma unroll
         for (int i = 3; i >= 0; i--) {
-            const uint32_t a = w[i] + Kc;
-            const uint32_t h1 = prmt(a, 0u, 0x4342u), h0 = prmt(a, 0u, 0x4140u);
-            const uint32_t t1 = (h1 + KA) & ~(h1 + KB) & 0x80008000u;
-            const uint32_t t0 = (h0 + KA) & ~(h0 + KB) & 0x80008000u;
-            m = __funnelshift_l((t1 >> 15) + 0x7ffeffffu, m, 1);
-            m = __funnelshift_l((t0 >> 15) + 0x7ffeffffu, m, 1);
+            const uint32_t z = __vabsdiffu4(w[i] + Kc, 0x80808080u) + K127;
+            const uint32_t n = ~(z | (z << 8));
+            m = __funnelshift_l(n, m, 1);
+            m = __funnelshift_l(n << 16, m, 1);
         }
     } else if (SHAPE == SH_POLY) {
         // row table T[dy+128] = (0x8000 - (128+xlo)) | (0x8000 - (128+xhi)) << 16
@@ -960,6 +958,8 @@ __global__ void __launch_bounds__(512, 2) k2_pair(Geom g, PairParams p, const __
             wb = gather_pair(g, tc, po, om, mB0, okr, po.okB, po.d + po.dx);
         }
         const int nsteps = down ? (rend - 1 - row0) : (row0 - gi * R);
+        // test hook: an inconsistent count (core.py:31-36 defect path)
+        const bool dbg = p.debug_defect && bt == 0 && g.tile_begin == 0 && u == 0;
         int row = row0;
         for (int s = 0; s < nsteps; s++) {
             const uint32_t K = pivot_k(PA >> hs, PB >> hs);
@@ -978,8 +978,7 @@ __global__ void __launch_bounds__(512, 2) k2_pair(Geom g, PairParams p, const __
             store_out(g, wb);
             cA += dA;
             cB += dB;
-            // test hook: an inconsistent count (core.py:31-36 defect path)
-            if (p.debug_defect && bt == 0 && g.tile_begin == 0 && u == 0 && s == 0) cA += 1 << 20;
+            if (dbg && s == 0) cA += 1 << 20;
             const int tA = target_at2(g, p, tc, row, j0);
             const int tB = target_at2(g, p, tc, row, j1);
             int mA, mB;
