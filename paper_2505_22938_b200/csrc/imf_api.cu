@@ -438,6 +438,22 @@ cudaError_t allow_smem(F* f, int optin) {
                                 optin - (int)a.sharedSizeBytes);
 }
 
+// Kernel rows symmetric in x (xlo = -(xhi - 1), xhi exclusive) and in y (rows dy
+// and -dy alike): the pair kernel's SH_POLYSYM membership test applies.
+bool kernel_symmetric(const imf_kernel* k) {
+    const int r = k->radius;
+    if (r > 127 || k->nrows > 2 * r + 1) return false;
+    std::vector<int> w(2 * r + 1, 0);
+    for (int i = 0; i < k->nrows; i++) {
+        const int dy = k->row_dy[i];
+        if (dy < -r || dy > r || k->row_xlo[i] != 1 - k->row_xhi[i]) return false;
+        w[dy + r] = k->row_xhi[i] - k->row_xlo[i];
+    }
+    for (int dy = 0; dy <= r; dy++)
+        if (w[r + dy] != w[r - dy]) return false;
+    return true;
+}
+
 cudaError_t set_attrs() {
     int dev = 0, optin = 0;
     cudaError_t e = cudaGetDevice(&dev);
@@ -496,6 +512,8 @@ cudaError_t set_attrs() {
     if (!e) e = allow_smem(k2_pair<SH_SQUARE, true>, optin);
     if (!e) e = allow_smem(k2_pair<SH_POLY, false>, optin);
     if (!e) e = allow_smem(k2_pair<SH_POLY, true>, optin);
+    if (!e) e = allow_smem(k2_pair<SH_POLYSYM, false>, optin);
+    if (!e) e = allow_smem(k2_pair<SH_POLYSYM, true>, optin);
     if (!e) e = allow_smem(k2_pair<SH_CIRCLEW, false>, optin);
     if (!e) e = allow_smem(k2_pair<SH_CIRCLEW, true>, optin);
     if (!e) g_attr_mask.fetch_or(bit, std::memory_order_release);
@@ -846,6 +864,7 @@ static int filter_impl(const imf_image* src, imf_image* dsts, int n, const int32
         pp.shape = !bytes_ok ? (kernel->shape_code == IMF_SHAPE_CIRCLE ? SH_CIRCLEW : SH_SPAN)
                    : kernel->shape_code == IMF_SHAPE_CIRCLE ? SH_CIRCLE
                    : kernel->shape_code == IMF_SHAPE_SQUARE ? SH_SQUARE : SH_POLY;
+        if (pp.shape == SH_POLY && kernel_symmetric(kernel) && env_int("IMF_POLYSYM", 1)) pp.shape = SH_POLYSYM;
         pp.R2p1 = r * (r + 1) + 1;
         pp.target = targets[0];
         pp.tmap = target_map;
@@ -925,6 +944,8 @@ static int filter_impl(const imf_image* src, imf_image* dsts, int n, const int32
                 case SH_SQUARE * 2 + 1: IMF_K2P_LAUNCH(SH_SQUARE, true); break;
                 case SH_POLY * 2: IMF_K2P_LAUNCH(SH_POLY, false); break;
                 case SH_POLY * 2 + 1: IMF_K2P_LAUNCH(SH_POLY, true); break;
+                case SH_POLYSYM * 2: IMF_K2P_LAUNCH(SH_POLYSYM, false); break;
+                case SH_POLYSYM * 2 + 1: IMF_K2P_LAUNCH(SH_POLYSYM, true); break;
                 case SH_CIRCLEW * 2: IMF_K2P_LAUNCH(SH_CIRCLEW, false); break;
                 case SH_CIRCLEW * 2 + 1: IMF_K2P_LAUNCH(SH_CIRCLEW, true); break;
                 case SH_SPAN * 2 + 1: IMF_K2P_LAUNCH(SH_SPAN, true); break;

@@ -54,9 +54,10 @@ size_t k2_smem_bytes(int N, int Npad, int ncols, int nrows, int r, int G, int Tw
 // Membership test families of the pair kernel (template parameter SHAPE).
 constexpr int SH_SPAN = 0;    // any convex kernel: per-row span table (kernels.py:127-182)
 constexpr int SH_CIRCLE = 1;  // 4(dx^2+dy^2) <= (2r+1)^2 (kernels.py:70-71), packed bytes + IDP.4A
-constexpr int SH_SQUARE = 2;  // |dx|, |dy| <= r (kernels.py:72-73), packed 16-bit range tests
+constexpr int SH_SQUARE = 2;  // |dx|, |dy| <= r (kernels.py:72-73), VABSDIFF4 on packed bytes
 constexpr int SH_POLY = 3;    // any convex kernel, per-row range constants looked up by dy byte
 constexpr int SH_CIRCLEW = 4; // circle, any tile (T + r > 128): unsigned-byte IDP.4A on x, y (see test8)
+constexpr int SH_POLYSYM = 5; // convex kernel symmetric in x and y: |dx| <= h(|dy|), VABSDIFF4 + byte table
 
 constexpr int PT_MAX = 250;  // >= kernel rows / columns (2r+1, r <= 124)
 

@@ -199,10 +199,16 @@ struct PairCtx {
     const uint16_t* om;   // generic pointer to omega rank 0
     const int* span;      // shared span table (2r+1)
     int N, r, R2p1;
-    uint32_t rowk_a;      // SH_POLY: shared address of the 256-entry per-(dy+128) range table
+    uint32_t rowk_a;      // SH_POLY: 256-entry per-(dy+128) range table; SH_POLYSYM: 128-byte table
     int nR2p1;            // -(r(r+1)+1)
     uint32_t x80;         // 0x80808080 in a register (SH_CIRCLE's LOP3 operand)
 };
+
+__device__ __forceinline__ uint32_t lds8(uint32_t a) {
+    unsigned short v;
+    asm volatile("ld.shared.u8 %0, [%1];" : "=h"(v) : "r"(a));
+    return v;
+}
 
 __device__ __forceinline__ uint32_t lds32c(uint32_t a) {
     uint32_t v;
@@ -263,6 +269,22 @@ __device__ __forceinline__ uint32_t test8(const PairCtx& c, int v0, uint32_t Kc,
             const uint32_t n = ~(z | (z << 8));
             m = __funnelshift_l(n, m, 1);
             m = __funnelshift_l(n << 16, m, 1);
+        }
+    } else if (SHAPE == SH_POLYSYM) {
+        // kernels symmetric in x and y (the regular polygons of kernels.py:45-64):
+        // inside iff |dx| <= h(|dy|).  VABSDIFF4 gives |dx|, |dy| bytes of two
+        // ranks; a 128-byte shared table gives 127 - h(|dy|) (128 for rows
+        // outside the kernel), so |dx| + that has bit 7 exactly outside
+        // (<= 255: no carry leaves a byte); bits 7 / 23 of the complement are
+        // the two ranks' membership
+#pragma unroll
+        for (int i = 3; i >= 0; i--) {
+            const uint32_t z = __vabsdiffu4(w[i] + Kc, 0x80808080u);
+            const uint32_t t0 = lds8(c.rowk_a + prmt(z, 0u, 0x4441u));
+            const uint32_t t1 = lds8(c.rowk_a + prmt(z, 0u, 0x4443u));
+            const uint32_t n = ~(z + prmt(t0, t1, 0x5410u));
+            m = __funnelshift_l(n << 8, m, 1);
+            m = __funnelshift_l(n << 24, m, 1);
         }
     } else if (SHAPE == SH_POLY) {
         // row table T[dy+128] = (0x8000 - (128+xlo)) | (0x8000 - (128+xhi)) << 16
@@ -663,6 +685,16 @@ __global__ void __launch_bounds__(512, 2) k2_pair(Geom g, PairParams p, const __
         if (tid < 32) hist[tid] = 0;
         for (int i = tid; i <= TY; i += blockDim.x) rowd[i] = 0;
         for (int i = tid; i < 2 * r + 1; i += blockDim.x) span_s[i] = kt.span[i];
+        if (SHAPE == SH_POLYSYM) {  // 127 - h(|dy|), h = the row's half-width (xlo = -h)
+            for (int i = tid; i < 128; i += blockDim.x) {
+                int v = 128;
+                if (i <= r) {
+                    const int sp = kt.span[i + r];
+                    if (sp >> 16) v = 127 + (int)(short)(sp & 0xffff);
+                }
+                reinterpret_cast<uint8_t*>(rowk)[i] = (uint8_t)v;
+            }
+        }
         if (SHAPE == SH_POLY) {
             for (int i = tid; i < 256; i += blockDim.x) {
                 const int dy = i - 128;
@@ -1013,6 +1045,8 @@ IMF_K2P(SH_CIRCLE, true)
 IMF_K2P(SH_SQUARE, true)
 IMF_K2P(SH_POLY, false)
 IMF_K2P(SH_POLY, true)
+IMF_K2P(SH_POLYSYM, false)
+IMF_K2P(SH_POLYSYM, true)
 IMF_K2P(SH_CIRCLEW, false)
 IMF_K2P(SH_CIRCLEW, true)
 #undef IMF_K2P
