@@ -242,19 +242,19 @@ __device__ __forceinline__ uint32_t test8(const PairCtx& c, int v0, uint32_t Kc,
             m = __funnelshift_l((uint32_t)slo, m, 1);
         }
     } else if (SHAPE == SH_CIRCLEW) {
-        // Wide tiles: dx may exceed a signed byte, so expand instead
-        //   (x-cx)^2 + (y-cy)^2 - r(r+1) - 1 = (x^2 + y^2 + Kw) - 2 (x cx + y cy)
-        // with unsigned-byte dot products on the raw entry x | y << 8 (Kc holds
-        // cx | cy << 8): 2 IDP.4A + 1 IMAD per rank; the sign bit is membership.
-        const int Kw = cx * cx + cy * cy + c.nR2p1;
-        const uint32_t Clo = Kc, Chi = Kc << 16;
+        // Wide tiles (|dx| up to 254): VABSDIFF4 of the raw entries x | y << 8
+        // against cx | cy << 8 (Kc, both halves) gives |dx|, |dy| as unsigned
+        // bytes; each rank's pair masked out by one LOP3 and squared by an
+        // unsigned IDP.4A against -(r(r+1)+1): the sign bit is membership
+        // (sums <= 2 * 254^2, no wrap).  3.5 instructions per rank.
 #pragma unroll
         for (int i = 3; i >= 0; i--) {
-            const uint32_t q = w[i];
-            const int slo = __dp4a(q, q & 0xffffu, (unsigned)Kw), shi = __dp4a(q, q & 0xffff0000u, (unsigned)Kw);
-            const int tlo = slo - 2 * (int)__dp4a(q, Clo, 0u), thi = shi - 2 * (int)__dp4a(q, Chi, 0u);
-            m = __funnelshift_l((uint32_t)thi, m, 1);
-            m = __funnelshift_l((uint32_t)tlo, m, 1);
+            const uint32_t z = __vabsdiffu4(w[i], Kc);
+            const uint32_t blo = z & 0xffffu, bhi = z & 0xffff0000u;
+            const uint32_t slo = __dp4a(blo, blo, (unsigned)c.nR2p1);
+            const uint32_t shi = __dp4a(bhi, bhi, (unsigned)c.nR2p1);
+            m = __funnelshift_l(shi, m, 1);
+            m = __funnelshift_l(slo, m, 1);
         }
     } else if (SHAPE == SH_SQUARE) {
         // bytes (dx+128, dy+128) of two ranks; VABSDIFF4 gives |dx|, |dy| per
@@ -349,10 +349,10 @@ __device__ __forceinline__ uint32_t walk_init(Walk& w, int P, int cnt, int t, in
 }
 
 // Per-window constant of the membership test (walk_init's packed form, or
-// cx | cy << 8 for SH_CIRCLEW).
+// (cx | cy << 8) in both halves for SH_CIRCLEW).
 template <int SHAPE>
 __device__ __forceinline__ uint32_t window_key(int cx, int cy) {
-    if (SHAPE == SH_CIRCLEW) return (uint32_t)cx | ((uint32_t)cy << 8);
+    if (SHAPE == SH_CIRCLEW) return ((uint32_t)cx | ((uint32_t)cy << 8)) * 0x10001u;
     return (uint32_t)((128 - cx) + ((128 - cy) << 8)) * 0x10001u;
 }
 
