@@ -892,21 +892,32 @@ __global__ void __launch_bounds__(512, 2) k2_pair(Geom g, PairParams p, const __
                                       : hcount(b, kt.he, p.nhe_even, p.nh, K);
         }
         gbar();
-        if (half == 0 && q < TH) {
-            int d0, d1;
-            half_diff(gin[32 + q], gin[q], d0, d1);
-            deltas[gi * T + 2 * q] = d0;
-            deltas[gi * T + 2 * q + 1] = d1;
+        // the down warp turns the step deltas into prefix sums by one warp
+        // scan: pref[k] = sum of deltas of steps 0..k-1, kept for k = 1..T in
+        // deltas[gi*T + k - 1] (pref[0] = 0), so window j's count below P is
+        // C0 + pref[j] - pref[cs] with no per-thread loop over the steps
+        if (half == 0) {
+            int d0 = 0, d1 = 0;
+            if (q < TH) half_diff(gin[32 + q], gin[q], d0, d1);
+            const int pr = d0 + d1;
+            int incl = pr;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int t = __shfl_up_sync(0xffffffffu, incl, o);
+                if (q >= o) incl += t;
+            }
+            if (q < TH) {
+                deltas[gi * T + 2 * q] = incl - pr + d0;  // pref[2q + 1]
+                deltas[gi * T + 2 * q + 1] = incl;        // pref[2q + 2]
+            }
         }
         gbar();
+        // (giving one warp the columns far from cs and the other the near ones
+        // measured slower on the smooth field, no faster on noise)
         const int j = half * 32 + q;
         if (j < T) {
-            int cnt = C0;
-            if (j > cs) {
-                for (int i = cs; i < j; i++) cnt += deltas[gi * T + i];
-            } else {
-                for (int i = j; i < cs; i++) cnt -= deltas[gi * T + i];
-            }
+            auto pref = [&](int k) { return k ? deltas[gi * T + k - 1] : 0; };
+            const int cnt = C0 + pref(j) - pref(cs);
             const int tgt = target_at2(g, p, tc, row, j);
             int m = (j == cs) ? seedP[gi] : refine8<SHAPE, OMG>(c, j + r, row + r, P, cnt, tgt);
             if (m < 0) {
@@ -1014,7 +1025,7 @@ __global__ void __launch_bounds__(512, 2) k2_pair(Geom g, PairParams p, const __
             const int tA = target_at2(g, p, tc, row, j0);
             const int tB = target_at2(g, p, tc, row, j1);
             int mA, mB;
-            if (p.refine_mode == 1)
+            if (p.refine_mode & 1)
                 refine8x2_seq<SHAPE, OMG>(c, j0 + r, row + r, PA, cA, tA, PB, cB, tB, mA, mB);
             else
                 refine8x2<SHAPE, OMG>(c, j0 + r, row + r, PA, cA, tA, PB, cB, tB, mA, mB);
