@@ -132,6 +132,17 @@ __device__ __forceinline__ TileCoord tile_coord(const Geom& g, long long t64) {
     return tc;
 }
 
+// tile_coord computed once per CTA (thread 0) and broadcast through shared
+// memory: its magic-number divisions cost every warp ~40 instructions
+// otherwise.  Block-wide barrier: call from every thread, before any other
+// barrier-dependent work.
+__device__ __forceinline__ TileCoord tile_coord_cta(const Geom& g, long long t64) {
+    __shared__ TileCoord s_tc;
+    if (threadIdx.x == 0) s_tc = tile_coord(g, t64);
+    __syncthreads();
+    return s_tc;
+}
+
 // Image coordinates of input-tile pixel (ly, lx), clamped to the image.
 __device__ __forceinline__ long long src_offset(const Geom& g, const TileCoord& tc, int ly, int lx) {
     int y = tc.oy0 + ly - g.r + g.vshift;

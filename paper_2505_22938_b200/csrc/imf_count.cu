@@ -56,7 +56,7 @@ __global__ void __launch_bounds__(1024) k1_count_reg(Geom g, uint16_t* __restric
     constexpr int NW = NB / 2;
     using T = typename std::conditional<DT == DT_U8, uint8_t, uint16_t>::type;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const TileCoord tc = tile_coord(g, g.tile_begin + blockIdx.x);
+    const TileCoord tc = tile_coord_cta(g, g.tile_begin + blockIdx.x);
     const int S = g.Sw, SH = g.Sh;
     uint32_t* hw = reinterpret_cast<uint32_t*>(smem);
     uint32_t* dummy = hw + NW;  // 32 words: per-lane sink for the atomics of unranked slots
