@@ -866,6 +866,7 @@ static int filter_impl(const imf_image* src, imf_image* dsts, int n, const int32
                    : kernel->shape_code == IMF_SHAPE_SQUARE ? SH_SQUARE : SH_POLY;
         if (pp.shape == SH_POLY && kernel_symmetric(kernel) && env_int("IMF_POLYSYM", 1)) pp.shape = SH_POLYSYM;
         pp.R2p1 = r * (r + 1) + 1;
+        pp.nR2p1 = -pp.R2p1;
         pp.target = targets[0];
         pp.tmap = target_map;
         pp.G = p.G;

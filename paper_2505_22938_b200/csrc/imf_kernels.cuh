@@ -74,6 +74,7 @@ struct PairTab {
 struct PairParams {
     int shape;       // SH_*: membership test family (packed ones require T + r <= 128)
     int R2p1;        // r(r+1) + 1
+    int nR2p1;       // -(r(r+1) + 1), the membership tests' IDP.4A addend (read from the constant bank)
     int nv, nv_even;
     int nh, nhe_even, nhx_even;
     int target;

@@ -714,9 +714,9 @@ __global__ void __launch_bounds__(512, 2) k2_pair(Geom g, PairParams p, const __
     // omega's shared address and -(r(r+1)+1) held in registers (opaque to the
     // compiler, which would otherwise rebuild them inside every refine step)
     uint32_t om_a = OMG ? 0u : (uint32_t)__cvta_generic_to_shared(om_sh);
-    int nR2p1 = -p.R2p1;
+    const int nR2p1 = p.nR2p1;
     uint32_t x80 = 0x80808080u;
-    asm volatile("" : "+r"(om_a), "+r"(nR2p1), "+r"(x80));
+    asm volatile("" : "+r"(om_a), "+r"(x80));
     const PairCtx c{om_a, om, span_s, N, r, p.R2p1, (uint32_t)__cvta_generic_to_shared(rowk), nR2p1, x80};
     const int R = TY / G;
     const int g0 = G >> 1;
