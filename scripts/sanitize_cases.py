@@ -17,6 +17,8 @@ cases = [
     ("uint16", (270, 260), ("circle", 100, 0, 0.0), {}),                   # k1_count_g, wide circle
     ("uint8", (120, 130, 3), ("regular_polygon", 20, 6, 10.0), {}),
     ("uint8", (120, 130), ("square", 9, 0, 0.0), {}),
+    ("uint8", (120, 130, 3), ("regular_polygon", 20, 6, 0.0), {}),         # symmetric polygon (VABSDIFF4 + table)
+    ("uint8", (140, 130), ("regular_polygon", 24, 12, 0.0), {}),
     ("uint8", (90, 100), ("regular_polygon", 30, 3, 29.0), {"IMF_PAIR": "0"}),  # general path
     ("float32", (140, 150), ("circle", 2, 0, 0.0), {}),                    # direct
     ("float32", (160, 170), ("circle", 20, 0, 0.0), {}),                   # f32 bucket, footprint
