@@ -104,7 +104,7 @@ def _kernel_struct(kernel):
 
 
 def _targets(kernel, percentile, out_shape):
-    from paper_2505_22938_b200.kernels import target_rank
+    from .kernel_geom import target_rank
     if np.isscalar(percentile) or np.ndim(percentile) == 0:
         return target_rank(kernel.area, float(percentile)), None
     pmap = np.asarray(percentile, dtype=np.float64)
@@ -113,12 +113,12 @@ def _targets(kernel, percentile, out_shape):
 
 
 def _run(which, image, shape, percentile, boundary, threads, tile_size=None, forwarding=True):
-    from paper_2505_22938_b200.kernels import make_kernel
+    from .kernel_geom import kernel_of  # the oracle's own rasterization (kernels.py:127-182)
     image = np.asarray(image)
     if image.ndim == 3:
         return np.stack([_run(which, image[..., c], shape, percentile, boundary, threads,
                               tile_size, forwarding) for c in range(image.shape[2])], axis=-1)
-    kernel = make_kernel(shape)
+    kernel = kernel_of(shape)
     r = shape.radius
     H, W = image.shape
     bnd = 1 if boundary == "valid" else 0

@@ -18,6 +18,19 @@ def _run(which, name, recipe, p):
     return fn(img, ShapeSpec(*p["shape"]), perc, p["boundary"], threads=4)
 
 
+def test_oracle_kernel_geometry_matches_reference_digests(golden):
+    """The oracle rasterizes kernels itself (oracle/kernel_geom.py, not the
+    product's make_kernel): every span table equals the real reference's."""
+    from oracle.kernel_geom import kernel_of, target_rank
+    bad = [spec for key, dig in golden["kernels"].items()
+           for spec in [tuple(json.loads(key))]
+           if C.kernel_digest(kernel_of(ShapeSpec(*spec))) != dig]
+    assert not bad, bad[:5]
+    assert len(golden["kernels"]) >= 300
+    for area, p, want in [(21, 0.5, 10), (21, 0.0, 0), (21, 1.0, 20), (9, 0.3, 2), (1, 0.7, 0)]:
+        assert target_rank(area, p) == want
+
+
 @pytest.mark.parametrize("which", ["fast", "brute"])
 def test_oracle_matches_reference_small(which, golden_small):
     bad = []
