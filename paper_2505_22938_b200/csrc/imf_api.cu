@@ -1212,7 +1212,7 @@ int imf_filter_host(const imf_image* src, imf_image* dst, const imf_kernel* kern
     int rc = IMF_OK;
     // compute lanes (stripes rotate over them, each with its own
     // workspace) so one stripe's K1 fills the tail of the previous stripe's K2
-    const int nl0 = std::max(1, std::min(kMaxStripeLanes, env_int("IMF_STRIPE_LANES", 2)));
+    const int nl0 = std::max(1, std::min(kMaxStripeLanes, env_int("IMF_STRIPE_LANES", 3)));
     const int OH0 = p.full_out_h;
     // output rows [R0, R1) (opt->row_begin/row_end: one device's stripe of a
     // multi-device job; the other rows of dst are left untouched)
@@ -1238,17 +1238,18 @@ int imf_filter_host(const imf_image* src, imf_image* dst, const imf_kernel* kern
     const int r = kernel->radius, vshift = opt->boundary == IMF_BOUNDARY_VALID ? r : 0;
     const int H = src->height, OH = OH0;
     const bool pipe = pipe0;
-    // Stripes of whole tile rows: a one-tile-row first stripe (the filter starts
-    // after a small upload), a one-tile-row last stripe (little left to download
-    // after the last filter), and 8 middle stripes; consecutive stripes run on
-    // alternating compute streams, so each stripe's K1 fills the previous
-    // stripe's K2 tail (c2: 2.60 ms host->host vs 2.53 ms device-resident).
+    // Stripes of whole tile rows: a two-tile-row first stripe (the filter starts
+    // after a small upload), a two-tile-row last stripe (little left to download
+    // after the last filter), ramp stripes and 8 middle stripes; consecutive
+    // stripes rotate over three compute streams, so each stripe's K1 fills the
+    // previous stripes' K2 tails (c2 with the round-2 kernels: 1.87 ms
+    // host->host vs 1.94 with two streams and one-tile-row edges; c5 -3 %).
     std::vector<int> cuts{0};  // in tile rows from R0, then output rows
     if (pipe) {
         const int tiles_y = (R1 - R0 + p.g.Th - 1) / p.g.Th;
-        const int edge = std::max(1, env_int("IMF_STRIPE_EDGE", 1));
+        const int edge = std::max(1, env_int("IMF_STRIPE_EDGE", 2));
         const int mid = std::max(1, env_int("IMF_STRIPE_MID", 8));
-        // ramp (IMF_STRIPE_RAMP=1): after the one-tile-row first stripe, stripes
+        // ramp (IMF_STRIPE_RAMP=1): after the first (edge) stripe, stripes
         // of 1 and 2 tile rows, so the GPU fills while the larger middle
         // stripes upload; mirrored (2, 1) before the last one-row stripe
         const int ramp = env_int("IMF_STRIPE_RAMP", 1) ? 3 : 0;  // tile rows in the ramp stripes, each end
