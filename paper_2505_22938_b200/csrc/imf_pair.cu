@@ -105,7 +105,7 @@ __device__ __forceinline__ uint32_t unpack4(uint32_t acc) {
 
 // Packed counts of [I >= P] over the vertical list at window-pair base `b`
 // (entering and exiting lists; byte-lane accumulators, <= 2 * 124 + 1 columns).
-template <int U>  // column-loop unroll (8 for circles: c2 / c5 gain; 4 elsewhere: c4 loses at 8)
+template <int U>  // column-loop unroll: 4 (round-2 end, with the 2-instruction acc_dp4: circles 8 -> 4 c2 / c5 -0.5 to -1 %, 16 +9 %, 2 +2 %)
 __device__ __forceinline__ void vcount(uint32_t b, const int2* __restrict__ v, int ne, int n, uint32_t K,
                                        uint32_t& ge_in, uint32_t& ge_out) {
     // one entry per kernel column, alternating parity: each of the even
@@ -780,7 +780,7 @@ __global__ void __launch_bounds__(512, 2) k2_pair(Geom g, PairParams p, const __
         const uint32_t K0 = pivot_k(P0 >> hs, P0 >> hs);
         for (int y = ytop + tid; y < ybot; y += blockDim.x) {  // step y -> y+1 at column cs
             uint32_t gi_, go_;
-            vcount<SHAPE == SH_CIRCLE ? 8 : 4>(I_a + 2 * (y * Sw + cs), kt.v, p.nv_even, p.nv, K0, gi_, go_);
+            vcount<4>(I_a + 2 * (y * Sw + cs), kt.v, p.nv_even, p.nv, K0, gi_, go_);
             deltas[y] = (int)(go_ & 0xffffu) - (int)(gi_ & 0xffffu);
         }
         __syncthreads();
@@ -1009,11 +1009,11 @@ __global__ void __launch_bounds__(512, 2) k2_pair(Geom g, PairParams p, const __
             uint32_t ge_in, ge_out;
             int dA, dB;
             if (down) {
-                vcount<SHAPE == SH_CIRCLE ? 8 : 4>(I_a + 2 * (row * Sw + j0), kt.v, p.nv_even, p.nv, K, ge_in, ge_out);
+                vcount<4>(I_a + 2 * (row * Sw + j0), kt.v, p.nv_even, p.nv, K, ge_in, ge_out);
                 half_diff(ge_out, ge_in, dA, dB);
                 row++;
             } else {
-                vcount<SHAPE == SH_CIRCLE ? 8 : 4>(I_a + 2 * ((row - 1) * Sw + j0), kt.v, p.nv_even, p.nv, K, ge_in, ge_out);
+                vcount<4>(I_a + 2 * ((row - 1) * Sw + j0), kt.v, p.nv_even, p.nv, K, ge_in, ge_out);
                 half_diff(ge_in, ge_out, dA, dB);
                 row--;
             }
