@@ -418,7 +418,7 @@ __device__ int refine8(const PairCtx& c, int cx, int cy, int P, int cnt, int t) 
     Walk w;
     const uint32_t mask = walk_init(w, P, cnt, t, cx, cy);
     w.Kc = window_key<SHAPE>(cx, cy);
-    walk_step<SHAPE, OMG>(c, w, mask, cx, cy);
+    walk_step2<SHAPE, OMG>(c, w, mask, cx, cy);
     while (!w.done) walk_step2<SHAPE, OMG>(c, w, 0xffu, cx, cy);
     return walk_result(c, w);
 }
