@@ -157,17 +157,23 @@ __global__ void __launch_bounds__(1024) k1_count_reg(Geom g, uint16_t* __restric
     else
         hist16_exclusive_scan(hw, NW);
     __syncthreads();
+    // scatter, one register row at a time: the row's NK prefix words are all
+    // loaded before any omega store (a load after a store to omega could
+    // alias it, so the compiler would otherwise wait out every load's latency)
 #pragma unroll
-    for (int j = 0; j < NK; j++)
+    for (int j = 0; j < NK; j++) {
+        uint32_t hv[NK];
+#pragma unroll
+        for (int k = 0; k < NK; k++) hv[k] = hw[(v[j][k] >> 1) & (NW - 1)];  // unranked: a valid word, unused
 #pragma unroll
         for (int k = 0; k < NK; k++) {
             const uint32_t val = v[j][k];
             if (val != 0xffffffffu) {
-                const uint32_t sh = (val & 1) << 4;
-                const uint32_t rank = ((hw[(val & 0xffffu) >> 1] >> sh) & 0xffffu) + (val >> 16);
+                const uint32_t rank = ((hv[k] >> ((val & 1) << 4)) & 0xffffu) + (val >> 16);
                 om[rank] = (uint16_t)((lane + 32 * k) | ((wid + 32 * j) << 8));
             }
         }
+    }
     for (int i = g.N + tid; i < g.Npad; i += blockDim.x) om[i] = 0xffffu;
     __syncthreads();
     if (g.k1_bulk)
