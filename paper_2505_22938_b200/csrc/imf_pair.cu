@@ -533,15 +533,18 @@ struct PairOut {
     bool okA, okB;      // the pair's columns lie inside the output
 };
 
+// (omega in shared memory: read through its shared address, an LDS, not a
+// generic load of the generic pointer)
+template <bool OMG>
 __device__ __forceinline__ Pend gather_pair(const Geom& g, const TileCoord& tc, const PairOut& po,
-                                            const uint16_t* om, int m, bool okrow, bool okcol,
+                                            const uint16_t* om, uint32_t om_a, int m, bool okrow, bool okcol,
                                             long long d) {
     Pend o;
     o.ok = okrow && okcol;
     o.d = d;
     o.v = 0;
     if (o.ok) {
-        const uint32_t e = om[m];
+        const uint32_t e = OMG ? (uint32_t)om[m] : lds16(om_a + 2 * m);
         const int ly = (int)(e >> 8), lx = (int)(e & 0xff);
         const long long so = po.interior ? po.sbase + (ly * po.sy + lx * po.sx) : src_offset(g, tc, ly, lx);
         if (g.dtype == DT_U8)
@@ -997,8 +1000,8 @@ __global__ void __launch_bounds__(512, 2) k2_pair(Geom g, PairParams p, const __
         Pend wa{0, 0, false}, wb{0, 0, false};
         if (down) {
             const bool okr = tc.oy0 + row0 < g.out_h;
-            wa = gather_pair(g, tc, po, om, mA0, okr, po.okA, po.d);
-            wb = gather_pair(g, tc, po, om, mB0, okr, po.okB, po.d + po.dx);
+            wa = gather_pair<OMG>(g, tc, po, om, c.om_a, mA0, okr, po.okA, po.d);
+            wb = gather_pair<OMG>(g, tc, po, om, c.om_a, mB0, okr, po.okB, po.d + po.dx);
         }
         const int nsteps = down ? (rend - 1 - row0) : (row0 - gi * R);
         // test hook: an inconsistent count (core.py:31-36 defect path)
@@ -1036,8 +1039,8 @@ __global__ void __launch_bounds__(512, 2) k2_pair(Geom g, PairParams p, const __
             }
             po.d += down ? po.drow : -po.drow;
             const bool okr = tc.oy0 + row < g.out_h;
-            wa = gather_pair(g, tc, po, om, mA, okr, po.okA, po.d);
-            wb = gather_pair(g, tc, po, om, mB, okr, po.okB, po.d + po.dx);
+            wa = gather_pair<OMG>(g, tc, po, om, c.om_a, mA, okr, po.okA, po.d);
+            wb = gather_pair<OMG>(g, tc, po, om, c.om_a, mB, okr, po.okB, po.d + po.dx);
             to_state<SHAPE>(c, hs, mA, tA, j0 + r, row + r, PA, cA);
             to_state<SHAPE>(c, hs, mB, tB, j1 + r, row + r, PB, cB);
         }
