@@ -19,12 +19,15 @@
 //   and PRMT the middle halves.
 // * Refine (core.py:87-146, ordinal.py:175-199).  Eight ranks per step from one
 //   LDS.128 of omega.  Circle membership 4(dx^2+dy^2) <= (2r+1)^2 (kernels.py:
-//   70-71) is evaluated on packed bytes: omega entry x | y << 8 plus a per-window
-//   constant gives (dx+128, dy+128) bytes for two ranks at once, XOR 0x80
-//   makes them signed, and IDP.4A squares-and-adds them against -(r(r+1)+1);
-//   the sign bit is the membership bit (funnel-shifted into the step mask).
-//   Requires |dx|, |dy| <= 127 over the tile: T + r <= 128.  Square / polygon
-//   kernels use the span table (kernels.py:127-182) per rank.
+//   70-71) is evaluated on packed bytes: omega entry x | y << 8 plus a
+//   per-window constant gives (dx+128, dy+128) bytes for two ranks at once,
+//   XOR 0x80 makes them signed, and IDP.4A squares-and-adds them against
+//   -(r(r+1)+1); the sign bit is the membership bit (funnel-shifted into the
+//   step mask).  Wide tiles, squares and x/y-symmetric polygons take |dx|,
+//   |dy| bytes from VABSDIFF4 of the raw entries against cx | cy << 8 and
+//   test them against r(r+1), r or a per-|dy| table;
+//   other polygons use a per-dy range table, any kernel the span table
+//   (kernels.py:127-182).
 //
 // Layout (shared memory): omega (rank -> x | y << 8, 8 sentinel entries each
 // side, 16-byte aligned so rank 8k starts a 16-byte chunk), then the ordinal
@@ -229,7 +232,8 @@ __device__ __forceinline__ uint32_t test8(const PairCtx& c, int v0, uint32_t Kc,
     if (SHAPE == SH_CIRCLE) {
         // each rank's signed bytes isolated by ONE LOP3 ((a ^ 0x80808080) & mask,
         // the XOR constant held in a register) and squared against themselves:
-        // 2 LOP3 + 2 IDP.4A per two ranks (b & mask against the full b needs 3 LOP3)
+        // 2 LOP3 + 2 IDP.4A per two ranks (b & mask against the full b needs 3
+        // LOP3; VABSDIFF4 on the raw entries, as below, measured 1.7 % slower)
 #pragma unroll
         for (int i = 3; i >= 0; i--) {
             const uint32_t a = w[i] + Kc;
@@ -246,7 +250,7 @@ __device__ __forceinline__ uint32_t test8(const PairCtx& c, int v0, uint32_t Kc,
         // against cx | cy << 8 (Kc, both halves) gives |dx|, |dy| as unsigned
         // bytes; each rank's pair masked out by one LOP3 and squared by an
         // unsigned IDP.4A against -(r(r+1)+1): the sign bit is membership
-        // (sums <= 2 * 254^2, no wrap).  3.5 instructions per rank.
+        // (sums <= 2 * 255^2, no wrap).  3.5 instructions per rank.
 #pragma unroll
         for (int i = 3; i >= 0; i--) {
             const uint32_t z = __vabsdiffu4(w[i], Kc);
@@ -257,15 +261,15 @@ __device__ __forceinline__ uint32_t test8(const PairCtx& c, int v0, uint32_t Kc,
             m = __funnelshift_l(slo, m, 1);
         }
     } else if (SHAPE == SH_SQUARE) {
-        // bytes (dx+128, dy+128) of two ranks; VABSDIFF4 gives |dx|, |dy| per
-        // byte (<= 127), + (127 - r) per byte sets bit 7 exactly where |d| > r
-        // (no carry leaves a byte); a rank is outside iff either of its bytes
-        // has bit 7: n = ~(z | z << 8) holds membership in bits 15 (low rank)
-        // and 31 (high rank)
+        // VABSDIFF4 of the raw entries against cx | cy << 8 gives |dx|, |dy|
+        // per byte (<= 127 for tile pixels), + (127 - r) per byte sets bit 7
+        // exactly where |d| > r (no carry leaves a tile pixel's byte); a rank is
+        // outside iff either of its bytes has bit 7: n = ~(z | z << 8) holds
+        // membership in bits 15 (low rank) and 31 (high rank)
         const uint32_t K127 = (uint32_t)(127 - c.r) * 0x01010101u;
 #pragma unroll
         for (int i = 3; i >= 0; i--) {
-            const uint32_t z = __vabsdiffu4(w[i] + Kc, 0x80808080u) + K127;
+            const uint32_t z = __vabsdiffu4(w[i], Kc) + K127;
             const uint32_t n = ~(z | (z << 8));
             m = __funnelshift_l(n, m, 1);
             m = __funnelshift_l(n << 16, m, 1);
@@ -279,7 +283,7 @@ __device__ __forceinline__ uint32_t test8(const PairCtx& c, int v0, uint32_t Kc,
         // the two ranks' membership
 #pragma unroll
         for (int i = 3; i >= 0; i--) {
-            const uint32_t z = __vabsdiffu4(w[i] + Kc, 0x80808080u);
+            const uint32_t z = __vabsdiffu4(w[i], Kc);
             const uint32_t t0 = lds8(c.rowk_a + prmt(z, 0u, 0x4441u));
             const uint32_t t1 = lds8(c.rowk_a + prmt(z, 0u, 0x4443u));
             const uint32_t n = ~(z + prmt(t0, t1, 0x5410u));
@@ -348,11 +352,13 @@ __device__ __forceinline__ uint32_t walk_init(Walk& w, int P, int cnt, int t, in
     return mask;
 }
 
-// Per-window constant of the membership test (walk_init's packed form, or
-// (cx | cy << 8) in both halves for SH_CIRCLEW).
+// Per-window constant of the membership test: (cx | cy << 8) in both halves
+// for the VABSDIFF4 tests, walk_init's (128 - cx, 128 - cy) form for SH_CIRCLE
+// and SH_POLY.
 template <int SHAPE>
 __device__ __forceinline__ uint32_t window_key(int cx, int cy) {
-    if (SHAPE == SH_CIRCLEW) return ((uint32_t)cx | ((uint32_t)cy << 8)) * 0x10001u;
+    if (SHAPE == SH_CIRCLEW || SHAPE == SH_SQUARE || SHAPE == SH_POLYSYM)
+        return ((uint32_t)cx | ((uint32_t)cy << 8)) * 0x10001u;
     return (uint32_t)((128 - cx) + ((128 - cy) << 8)) * 0x10001u;
 }
 
@@ -688,8 +694,8 @@ __global__ void __launch_bounds__(512, 2) k2_pair(Geom g, PairParams p, const __
         if (tid < 32) hist[tid] = 0;
         for (int i = tid; i <= TY; i += blockDim.x) rowd[i] = 0;
         for (int i = tid; i < 2 * r + 1; i += blockDim.x) span_s[i] = kt.span[i];
-        if (SHAPE == SH_POLYSYM) {  // 127 - h(|dy|), h = the row's half-width (xlo = -h)
-            for (int i = tid; i < 128; i += blockDim.x) {
+        if (SHAPE == SH_POLYSYM) {  // 127 - h(|dy|), h = the row's half-width (xlo = -h); 256 entries
+            for (int i = tid; i < 256; i += blockDim.x) {  // (|dy| of the sentinel entries exceeds 127)
                 int v = 128;
                 if (i <= r) {
                     const int sp = kt.span[i + r];
