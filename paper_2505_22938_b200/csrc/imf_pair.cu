@@ -279,17 +279,18 @@ __device__ __forceinline__ uint32_t test8(const PairCtx& c, int v0, uint32_t Kc,
         // inside iff |dx| <= h(|dy|).  VABSDIFF4 gives |dx|, |dy| bytes of two
         // ranks; a 128-byte shared table gives 127 - h(|dy|) (128 for rows
         // outside the kernel), so |dx| + that has bit 7 exactly outside
-        // (<= 255: no carry leaves a byte); bits 7 / 23 of the complement are
-        // the two ranks' membership
+        // (<= 255: no carry leaves a byte); bits 7 / 23 are the two ranks'
+        // outside bits, complemented once per 8 ranks
 #pragma unroll
         for (int i = 3; i >= 0; i--) {
             const uint32_t z = __vabsdiffu4(w[i], Kc);
             const uint32_t t0 = lds8(c.rowk_a + prmt(z, 0u, 0x4441u));
             const uint32_t t1 = lds8(c.rowk_a + prmt(z, 0u, 0x4443u));
-            const uint32_t n = ~(z + prmt(t0, t1, 0x5410u));
-            m = __funnelshift_l(n << 8, m, 1);
-            m = __funnelshift_l(n << 24, m, 1);
+            const uint32_t o = z + prmt(t0, t1, 0x5410u);  // bits 7 / 23: OUTSIDE
+            m = __funnelshift_l(o << 8, m, 1);
+            m = __funnelshift_l(o << 24, m, 1);
         }
+        m = ~m & 0xffu;  // outside bits -> membership, once per 8 ranks
     } else if (SHAPE == SH_POLY) {
         // row table T[dy+128] = (0x8000 - (128+xlo)) | (0x8000 - (128+xhi)) << 16
         // (0 for rows outside the kernel): with the dx byte h in both halves,
