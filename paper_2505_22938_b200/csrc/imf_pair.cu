@@ -264,16 +264,18 @@ __device__ __forceinline__ uint32_t test8(const PairCtx& c, int v0, uint32_t Kc,
         // VABSDIFF4 of the raw entries against cx | cy << 8 gives |dx|, |dy|
         // per byte (<= 127 for tile pixels), + (127 - r) per byte sets bit 7
         // exactly where |d| > r (no carry leaves a tile pixel's byte); a rank is
-        // outside iff either of its bytes has bit 7: n = ~(z | z << 8) holds
-        // membership in bits 15 (low rank) and 31 (high rank)
+        // outside iff either of its bytes has bit 7: z | z << 8 holds the
+        // outside bits in bits 15 (low rank) and 31 (high rank), complemented
+        // once per 8 ranks
         const uint32_t K127 = (uint32_t)(127 - c.r) * 0x01010101u;
 #pragma unroll
         for (int i = 3; i >= 0; i--) {
             const uint32_t z = __vabsdiffu4(w[i], Kc) + K127;
-            const uint32_t n = ~(z | (z << 8));
-            m = __funnelshift_l(n, m, 1);
-            m = __funnelshift_l(n << 16, m, 1);
+            const uint32_t o = z | (z << 8);  // bits 15 / 31: OUTSIDE
+            m = __funnelshift_l(o, m, 1);
+            m = __funnelshift_l(o << 16, m, 1);
         }
+        m = ~m & 0xffu;  // outside bits -> membership, once per 8 ranks
     } else if (SHAPE == SH_POLYSYM) {
         // kernels symmetric in x and y (the regular polygons of kernels.py:45-64):
         // inside iff |dx| <= h(|dy|).  VABSDIFF4 gives |dx|, |dy| bytes of two
